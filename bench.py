@@ -1,0 +1,480 @@
+#!/usr/bin/env python3
+"""D2Q37 FP64 hot-path benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+Workload (BASELINE configs 3/4): a 4096 x 16384 lattice per GPU (weak
+scaling; the global lattice is 4096 x 16384*N, split into y-slabs), config-0
+Rayleigh-Taylor-like init, periodic x, top/bottom specular walls, omega 0.8
+(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the SoA store.
+value = whole-job MLUPS over the K timed steps (max over ranks of the device
+time).  Inputs are larger than L2 (2 x 19.9 GB per GPU vs 126 MB), so no
+explicit flush is needed.
+
+Also reported (N=1): propagate GB/s on config 1 and collide GFLOP/s on
+config 2 (the other two BASELINE metrics), the SoA/CSoA x fused/unfused
+step variants, the roofline of the dominant kernel, the e2e rate through the
+public API with host buffers, and the reference CPU path on this host.
+
+``--impl reference`` times the reference's own CPU step (oracle/_ref, the
+unmodified lbmbench library) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LX, LY_PER_GPU = 4096, 16384
+OMEGA = 0.8
+SEED = 12345
+BYTES_PER_SITE = 592  # 37 x 8 B read + 37 x 8 B write (BASELINE north_star)
+FLOPS_PER_SITE = 1522  # VelocityModel::kCollideFlopsPerSite (model.hpp:74-78)
+FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA cores), nominal -- no measured FP64 peak in MEASURED_PEAKS.json
+METRIC = "D2Q37 FP64 MLUPS (full step: propagate + bc + collide)"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- distributed plumbing
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = False
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = True
+
+    def barrier(self):
+        if self.pg:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if not self.pg:
+            return b
+        import torch.distributed as dist
+        obj = [b]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.pg:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------- GPU helpers
+
+def cuda_events():
+    import torch
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def time_steps(sim, steps: int, fn) -> float:
+    """Device time (ms) of `steps` calls of fn on the lattice stream (CUDA events)."""
+    import torch
+    s = torch.cuda.ExternalStream(sim.stream)
+    a, b = cuda_events()
+    sim.sync()
+    a.record(s)
+    for _ in range(steps):
+        fn()
+    b.record(s)
+    b.synchronize()
+    sim.sync()
+    return a.elapsed_time(b)
+
+
+def pin(arr: np.ndarray) -> bool:
+    import torch
+    rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+    return int(rc) == 0
+
+
+def unpin(arr: np.ndarray):
+    import torch
+    torch.cuda.cudart().cudaHostUnregister(arr.ctypes.data)
+
+
+def host_mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+# --------------------------------------------------------------------------- sub-benchmarks (N=1)
+
+def bench_propagate(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
+    """BASELINE config 1: 1024 x 8192 Philox input, repeated propagate prv -> nxt, 592 B/site."""
+    lx, ly = 1024, 8192
+    sim = lbm.Simulation("soa", lx, ly, device=0)
+    sim.init_philox(SEED)
+    sim.bc("periodic")
+    for _ in range(warmup):
+        sim.propagate_only(sync=False)
+    sim.set_profiling(True)
+    sim.kernel_times()
+    ms = time_steps(sim, reps, lambda: sim.propagate_only(sync=False))
+    kt = sim.kernel_times()["propagate"]
+    sim.set_profiling(False)
+    t = kt[0] / kt[1] / 1e3
+    gbs = lbm.propagate_gbps(lx, ly, 37, t, "nt")
+    sim.close()
+    return {"config": "c1: 1024x8192 SoA, Philox U[0,1) input, periodic halo, propagate prv->nxt",
+            "reps": reps, "ms_per_call": t * 1e3, "wall_ms_per_call": ms / reps, "GB_per_s": gbs,
+            "frac_of_hbm": gbs / hbm_peak, "mlups": lbm.mlups(lx, ly, t)}
+
+
+def bench_collide(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
+    """BASELINE config 2: 1024 x 8192 perturbed equilibrium, collide nxt -> prv, 1522 FLOP/site."""
+    lx, ly = 1024, 8192
+    sim = lbm.Simulation("soa", lx, ly, device=0)
+    sim.load(lbm.make_lattice("c2", lx, ly, SEED), which=1)
+    for _ in range(warmup):
+        sim.collide(1.0, sync=False)
+    sim.set_profiling(True)
+    sim.kernel_times()
+    time_steps(sim, reps, lambda: sim.collide(1.0, sync=False))
+    kt = sim.kernel_times()["collide"]
+    sim.set_profiling(False)
+    t = kt[0] / kt[1] / 1e3
+    gf = lbm.collide_gflops(lx, ly, FLOPS_PER_SITE, t)
+    gbs = lx * ly * BYTES_PER_SITE / t / 1e9
+    sim.close()
+    return {"config": "c2: 1024x8192 SoA, c2 perturbed equilibrium, collide nxt->prv, omega 1.0",
+            "reps": reps, "ms_per_call": t * 1e3, "GFLOP_per_s": gf, "mlups": lbm.mlups(lx, ly, t),
+            "frac_of_fp64_nominal": gf / (FP64_NOMINAL_TFLOPS * 1e3), "GB_per_s": gbs,
+            "frac_of_hbm": gbs / hbm_peak,
+            "frac_of_attainable": gf / min(FP64_NOMINAL_TFLOPS * 1e3, FLOPS_PER_SITE / BYTES_PER_SITE * hbm_peak)}
+
+
+def bench_variant(lbm, canon, layout, vl, variant, warmup, steps) -> dict:
+    sim = lbm.Simulation(layout, LX, canon.shape[2], vl, device=0, bc="wall", variant=variant)
+    sim.load(canon)
+    sim.step(OMEGA, warmup)
+    sim.set_profiling(True)
+    sim.kernel_times()
+    ms = time_steps(sim, steps, lambda: sim.step(OMEGA, 1, sync=False))
+    kt = sim.kernel_times()
+    sim.set_profiling(False)
+    sim.close()
+    sites = LX * canon.shape[2]
+    out = {"mlups": sites * steps / (ms / 1e3) / 1e6, "ms_per_step": ms / steps}
+    for k, (tot, n) in kt.items():
+        if n:
+            out[f"{k}_ms"] = tot / n
+    return out
+
+
+# --------------------------------------------------------------------------- CPU baseline / reference arm
+
+def reference_step_rate(lx=LX, ly=1024, iterations=3, warmup=1, workers=None):
+    """The unmodified reference step (oracle/_ref) on a bounded sample of the lattice."""
+    from oracle import pyoracle as po
+    workers = workers or os.cpu_count() or 1
+    init = po.orc_lattice("rt", lx, ly, seed=SEED)
+    sim = po.RefSim(po.AOS, lx, ly, 1, workers=workers)
+    sim.load(init)
+    med, _ = sim.time("step", omega=OMEGA, iterations=iterations, warmup=warmup)
+    return lx * ly / med / 1e6, med, workers
+
+
+def run_reference(args, dist):
+    from oracle import pyoracle as po
+    lx, ly = LX, 1024
+    workers = os.cpu_count() or 1
+    init = po.orc_lattice("rt", lx, ly, seed=SEED)
+    sim = po.RefSim(po.AOS, lx, ly, 1, workers=workers)
+    sim.load(init)
+    for _ in range(args.warmup):
+        sim.step(OMEGA, 1)
+    t0 = time.perf_counter()
+    times = []
+    for _ in range(args.steps):
+        a = time.perf_counter()
+        sim.step(OMEGA, 1)
+        times.append(time.perf_counter() - a)
+    total = time.perf_counter() - t0
+    value = lx * ly * args.steps / total / 1e6
+    sample = (f"{lx}x{ly} rows of the {LX}x{LY_PER_GPU * args.gpus} lattice per step (RT init, "
+              "reference step = periodic halo_exchange + propagate + collide; the reference has no wall bc), "
+              "AoS layout (its fastest step here), ThreadPool of all host threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"c3/c4-weak sample: {lx}x{ly} (RT init, omega {OMEGA})", "lx": lx,
+                       "ly_sample": ly, "layout": "aos", "workers": workers},
+            "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_ms_median": 1e3 * statistics.median(times)}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- main arm
+
+def run_b200(args, dist: Dist):
+    import torch
+    import paper_1804_01918_b200 as lbm
+
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    hbm_peak, peak_src = peaks()
+    n = dist.world
+    ly_local = args.ly
+    ly_global = ly_local * n
+    sites_local = LX * ly_local
+    rank = dist.rank
+
+    # ---- lattice + init (host canonical of this rank's slab: also the e2e input)
+    canon = np.empty((37, LX, ly_local), dtype=np.float64)
+    params = None if n == 1 else [float(ly_global), float(rank * ly_local)]
+    lbm.make_lattice("rt", LX, ly_local, SEED, params=params, out=canon)
+    if n == 1:
+        sim = lbm.Simulation(args.layout, LX, ly_local, args.vl, device=dev, bc="wall", variant=args.variant)
+    else:
+        uid = dist.bcast_bytes(lbm.nccl_unique_id() if rank == 0 else None)
+        sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
+                                  nccl_id=uid, bc="wall", variant=args.variant)
+    sim.load(canon)
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    sim.step(OMEGA, args.warmup)
+    sim.set_profiling(True)
+    sim.kernel_times()
+    dist.barrier()
+    torch.cuda.synchronize()
+    ms = time_steps(sim, args.steps, lambda: sim.step(OMEGA, 1, sync=False))
+    torch.cuda.synchronize()
+    dist.barrier()
+    kt = sim.kernel_times()
+    sim.set_profiling(False)
+    clk = clocks.stop()
+    halo_ms = sim.exposed_halo_ms() if n > 1 else 0.0
+    ms_max = dist.max(ms)
+    value = n * sites_local * args.steps / (ms_max / 1e3) / 1e6
+    launches = sum(c for _, c in kt.values())
+
+    fused_ms, fused_n = kt["fused"]
+    dom = "fused" if fused_n else "collide"
+    dom_ms = kt[dom][0] / max(1, kt[dom][1])
+    achieved = sites_local * BYTES_PER_SITE / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
+    step_ms = ms_max / args.steps
+    roofline = {"bound": "hbm", "kernel": "k_collide<FAST,SHIFT> (fused pull-gather + collide)",
+                "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak if achieved else None, "traffic": load_ncu_traffic(),
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
+                "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms,
+                "edge_ms": kt["edge"][0] / max(1, kt["edge"][1])}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(lbm, sim, canon, args, dist)
+
+    line = {"metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c3/c4-weak: {LX}x{ly_local} per GPU (global {LX}x{ly_global}), RT init, "
+                                   f"periodic x, top/bottom specular walls, omega {OMEGA}",
+                       "lx": LX, "ly_per_gpu": ly_local, "ly_global": ly_global, "layout": args.layout,
+                       "vl": args.vl if args.layout == "csoa" else 1, "variant": args.variant,
+                       "l2": "inputs larger than L2 (2 x 19.9 GB lattice per GPU vs 126 MB L2): no flush needed",
+                       "parallelism": f"y-slab x{n}" if n > 1 else "single GPU"},
+            "roofline": roofline, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
+            "exposed_halo_ms_per_step": halo_ms}
+
+    if n == 1 and not args.no_extras:
+        sim.close()
+        del sim
+        line["kernels"] = {"propagate_c1": bench_propagate(lbm, 5, 200, hbm_peak),
+                           "collide_c2": bench_collide(lbm, 5, 200, hbm_peak)}
+        variants = {}
+        for lay, vl, var in (("soa", 1, "unfused"), ("csoa", 32, "fused"), ("csoa", 32, "unfused")):
+            if (lay, var) == (args.layout, args.variant):
+                continue
+            variants[f"{lay}{vl if lay == 'csoa' else ''}-{var}"] = bench_variant(lbm, canon, lay, vl, var, 3, 20)
+        line["variants_c3"] = variants
+    if n == 1 and not args.no_cpu:
+        try:
+            v, med, workers = reference_step_rate()
+            line["cpu_baseline"] = {
+                "value": v, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                "sample": f"{LX}x1024 rows of the {LX}x{LY_PER_GPU} lattice, unmodified reference step "
+                          f"(oracle/_ref, AoS, periodic halo_exchange + propagate + collide), median of 3 steps"}
+        except Exception as e:  # the CPU baseline must not sink the GPU line
+            line["cpu_baseline"] = {"value": None, "unit": "MLUPS", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(lbm, sim, canon, args, dist: Dist):
+    """load(host) -> step x n -> dump(host) through the public API, host buffers pinned."""
+    nsteps = args.e2e_steps
+    need = canon.nbytes
+    if host_mem_available() < need * 1.5 and host_mem_available() > 0:
+        return {"value": None, "unit": "MLUPS", "skipped": "not enough host memory for a second buffer"}
+    out = np.empty_like(canon)
+    pinned = pin(canon) and pin(out)
+    sim.load(canon)
+    sim.step(OMEGA, nsteps)
+    sim.dump(out=out)
+    times = []
+    for _ in range(args.e2e_iters):
+        dist.barrier()
+        t0 = time.perf_counter()
+        sim.load(canon)
+        sim.step(OMEGA, nsteps)
+        sim.dump(out=out)
+        times.append(time.perf_counter() - t0)
+    if pinned:
+        unpin(canon)
+        unpin(out)
+    t = dist.max(min(times))
+    sites = LX * canon.shape[2] * dist.world
+    return {"value": sites * nsteps / t / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": canon.nbytes / nsteps,
+            "d2h_bytes_per_step": out.nbytes / nsteps, "steps_per_call": nsteps,
+            "h2d_bytes_per_call": canon.nbytes, "d2h_bytes_per_call": out.nbytes, "pinned": pinned,
+            "seconds_per_call": t,
+            "call": "Simulation.load(host canonical) + step(0.8, n, fused, wall) + dump(host canonical)"}
+
+
+def load_ncu_traffic():
+    """dram bytes/launch of the fused kernel from the committed ncu summary (profiles/), else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--layout", choices=["soa", "csoa"], default="soa")
+    ap.add_argument("--vl", type=int, default=32)
+    ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-iters", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)  # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        # rank 0 alone runs the CPU reference; other ranks exit 0 without work
+        if int(os.environ.get("RANK", "0")) == 0:
+            run_reference(args, None)
+        return
+    dist = Dist()
+    try:
+        run_b200(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+/*
+ * d2q37_b200.h -- C-ABI of the B200-native D2Q37 hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference lbmbench operator API
+ * (/root/reference/proj/include/lbm/{kernels,lattice,dump,model}.hpp).  Every
+ * entry point below names the reference interface it replaces.  Plain C types
+ * only (no torch, no CUDA types); host arrays are borrowed for the duration of
+ * the call; device state is owned by an opaque handle.
+ *
+ * Calls enqueue work on the handle's CUDA stream and return; d2q37_sync()
+ * waits and reports deferred errors (D2Q37_ERR_NON_PHYSICAL from the collide
+ * kernels' device flag).  load/dump/read calls are synchronous.  The C++
+ * header include/lbm_b200/lbm_b200.hpp wraps this into the reference's
+ * blocking, exception-throwing verbs.
+ *
+ * Canonical lattice order (all host arrays): (p*lx + x)*ly + y, p < 37
+ * (proj/include/lbm/dump.hpp:19-21).
+ */
+#ifndef D2Q37_B200_H
+#define D2Q37_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define D2Q37_NPOP 37
+#define D2Q37_NMOM 14
+#define D2Q37_HALO 3
+#define D2Q37_NCCL_ID_BYTES 128
+
+/* Status codes.  Reference exception types:
+ *   INVALID_ARGUMENT  <- std::invalid_argument / std::out_of_range
+ *                        (layout.cpp:14-23, kernels.cpp:181-183, :238-242, dump.cpp:37-38)
+ *   NON_PHYSICAL      <- lbm::NonPhysicalError (model.hpp:28-30, model.cpp:245)       */
+enum {
+    D2Q37_OK = 0,
+    D2Q37_ERR_INVALID_ARGUMENT = 1,
+    D2Q37_ERR_NON_PHYSICAL = 2,
+    D2Q37_ERR_CUDA = 3,
+    D2Q37_ERR_NCCL = 4,
+    D2Q37_ERR_UNSUPPORTED = 5
+};
+
+/* LayoutKind numbering of layout.hpp:12 {AoS, SoA, CSoA, CAoSoA}.  SoA and CSoA
+ * are device layouts here; AoS/CAoSoA return D2Q37_ERR_UNSUPPORTED. */
+enum { D2Q37_AOS = 0, D2Q37_SOA = 1, D2Q37_CSOA = 2, D2Q37_CAOSOA = 3 };
+
+/* Boundary condition of the y faces.  PERIODIC is the reference
+ * halo_exchange (kernels.cpp:197-234); WALL is the specular top/bottom wall
+ * of BASELINE config 0 (no reference counterpart).  x is always
+ * periodic. */
+enum { D2Q37_BC_PERIODIC = 0, D2Q37_BC_WALL = 1 };
+
+/* step() variants: UNFUSED = bc, propagate, collide (kernels.cpp:276-283);
+ * FUSED = bc, one pull-gather + collide kernel. */
+enum { D2Q37_UNFUSED = 0, D2Q37_FUSED = 1 };
+
+/* Arithmetic of the collide kernels.  FAST lets nvcc contract into DFMA (as the
+ * reference's -march=native build does); STRICT performs every operation as a
+ * separate IEEE op in the reference's source order (model.cpp:242-298), which
+ * reproduces a no-contraction build of the reference bit for bit. */
+enum { D2Q37_MATH_FAST = 0, D2Q37_MATH_STRICT = 1 };
+
+/* Host initialisers (lattice.hpp:28-40 plus the BASELINE recipes). */
+enum {
+    D2Q37_INIT_RANDOM = 0,      /* make_random_lattice (lattice.cpp:8-23); params unused     */
+    D2Q37_INIT_EQUILIBRIUM = 1, /* make_equilibrium_lattice (:25-34); params {rho,ux,uy,T}   */
+    D2Q37_INIT_SHEAR = 2,       /* make_shear_lattice (:36-47); params {amp, temp}           */
+    D2Q37_INIT_RT = 3,          /* BASELINE config 0/3/4 Rayleigh-Taylor-like init; optional   */
+                                /* params {ly_global, y0} for one y-slab of a taller lattice  */
+    D2Q37_INIT_C2 = 4,          /* BASELINE config 2 perturbed equilibrium                    */
+    D2Q37_INIT_PHILOX = 5       /* BASELINE config 1 i.i.d. U[0,1) (Philox4x32-10)            */
+};
+
+/* Model constants (VelocityModel accessors, model.hpp:54-59, plus the Hermite
+ * table eq_table_ of model.hpp:97 / model.cpp:197-234, row-major [i][k]). */
+typedef struct d2q37_model {
+    int cx[D2Q37_NPOP];
+    int cy[D2Q37_NPOP];
+    double w[D2Q37_NPOP];
+    double t0;
+    double eq[D2Q37_NPOP * D2Q37_NMOM];
+} d2q37_model;
+
+typedef struct d2q37_lattice d2q37_lattice;
+
+/* Thread-local message of the last failing call. */
+const char* d2q37_last_error(void);
+
+/* VelocityModel::d2q37() (model.hpp:52, model.cpp:183-240): velocity set,
+ * moment-matched weights and t0, Hermite table, derived on the host. */
+int d2q37_model_d2q37(d2q37_model* out);
+
+/* Descriptor(layout, Geometry{lx, ly, 3, 3, vl}) + LatticeState
+ * (layout.hpp:46-98, layout.cpp:50-59, lattice.hpp:13-24): zero-initialised
+ * double-buffered device storage.  vl is ignored for SoA. */
+int d2q37_create(int layout, int lx, int ly, int vl, int device, d2q37_lattice** out);
+int d2q37_destroy(d2q37_lattice* h);
+
+/* Constants used by collide (take them from the caller's VelocityModel). */
+int d2q37_set_model(d2q37_lattice* h, const d2q37_model* m);
+int d2q37_set_math(d2q37_lattice* h, int math);
+/* CUDA stream (cudaStream_t as void*) that all work of h is enqueued on; NULL = library-owned. */
+int d2q37_set_stream(d2q37_lattice* h, void* stream);
+void* d2q37_get_stream(d2q37_lattice* h);
+
+/* Descriptor queries (layout.hpp:54-65): lx, ly, vl, strip, sy, px. */
+int d2q37_geometry(const d2q37_lattice* h, int out[6]);
+/* Bytes of device memory owned by h (both buffers + exchange buffers). */
+size_t d2q37_device_bytes(const d2q37_lattice* h);
+/* LatticeState::time_step (lattice.hpp:23). */
+long d2q37_time_step(const d2q37_lattice* h);
+
+/* LatticeState::load / dump (lattice.hpp:18-19, dump.cpp:26-42): canonical
+ * host array of n = 37*lx*ly doubles into / out of the state buffer (prv). */
+int d2q37_load_canonical(d2q37_lattice* h, const double* host, size_t n);
+int d2q37_dump_canonical(d2q37_lattice* h, double* host, size_t n);
+/* from_canonical / to_canonical on one buffer: which = 0 prv, 1 nxt (dump.hpp:28-29). */
+int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n);
+int d2q37_dump_buffer(d2q37_lattice* h, int which, double* host, size_t n);
+/* Same with a canonical array already resident in device memory. */
+int d2q37_load_buffer_device(d2q37_lattice* h, int which, const double* dev, size_t n);
+int d2q37_dump_buffer_device(d2q37_lattice* h, int which, double* dev, size_t n);
+/* Field::data() of one buffer in the reference Descriptor element order
+ * elem(p,X,j,k) (layout.hpp:67-79), halos included: n = 37*(lx+6)*(ly/vl+6)*vl. */
+int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n);
+int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n);
+
+/* halo_exchange(prv) (kernels.hpp:29, kernels.cpp:197-234) as one fused edge
+ * kernel; bc = D2Q37_BC_PERIODIC reproduces the reference bit for bit, WALL
+ * mirrors the outer y faces (specular). */
+int d2q37_bc(d2q37_lattice* h, int bc);
+/* propagate(prv, nxt, offsets) (kernels.hpp:33, kernels.cpp:50-85).  Pass
+ * corrupt_population >= 0 to add +1 to that population's pull offset (the
+ * ValidationOptions::corrupt_population hook, validation.hpp:55-57). */
+int d2q37_propagate(d2q37_lattice* h);
+int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population);
+/* collide(nxt, prv, model, omega) (kernels.hpp:40, kernels.cpp:120-156). */
+int d2q37_collide(d2q37_lattice* h, double omega);
+/* step(state, model, omega) x nsteps (kernels.hpp:45, kernels.cpp:276-283). */
+int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc);
+/* std::swap(state.prv, state.nxt) (module.cpp:82, test_kernels.cpp:272): O(1). */
+int d2q37_swap_buffers(d2q37_lattice* h);
+/* Wait for h's stream; returns D2Q37_ERR_NON_PHYSICAL (and clears the flag) if
+ * any collide since the last sync saw !(rho > 0) (model.cpp:245). */
+int d2q37_sync(d2q37_lattice* h);
+
+/* Global sums over the physical sites of the state buffer (prv):
+ * out = {mass, x-momentum, y-momentum, energy sum |c|^2 f}; deterministic
+ * for a given geometry.  Conservation checks at full size. */
+int d2q37_moments(d2q37_lattice* h, double out[4]);
+
+/* Host initialisers -> canonical array (n = 37*lx*ly); params per kind above;
+ * nthreads host threads for the equilibrium evaluation (<= 0: all cores). */
+int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* params,
+                       const d2q37_model* m, double* out, size_t n, int nthreads);
+/* Device-side D2Q37_INIT_PHILOX straight into one buffer (bit-identical to the host one). */
+int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed);
+
+/* ---- Multi-GPU: 1-D y-slab decomposition (BASELINE config 4) ------------- */
+
+/* NCCL unique id for d2q37_create_slab (rank 0 creates, the caller broadcasts). */
+int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]);
+/* Rank `rank` of `nranks` owns global rows [rank*ly/nranks, (rank+1)*ly/nranks)
+ * of an lx x ly lattice; load/dump take that slab's canonical array (lx x ly/nranks).
+ * Halo rows travel by ncclSend/ncclRecv between y neighbours each step. */
+int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
+                      const unsigned char id[D2Q37_NCCL_ID_BYTES], d2q37_lattice** out);
+/* In-process emulation: nslabs slabs of one lx x ly lattice on one device whose
+ * halos move by device copies.  Same pack / edge / interior / boundary kernels
+ * as the NCCL path; used to prove slab invariance on a single GPU. */
+int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslabs,
+                       d2q37_lattice** out);
+/* step for every slab of a group created by d2q37_create_group. */
+int d2q37_group_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps, int variant, int bc);
+/* rank, nranks, first global row, rows of this slab. */
+int d2q37_slab_info(const d2q37_lattice* h, int out[4]);
+/* Per-kernel device timing (CUDA events recorded around each launch on the
+ * handle's stream while profiling is on).  d2q37_kernel_times returns the
+ * summed milliseconds and launch counts since the last call, per class:
+ * 0 edge (bc), 1 propagate, 2 collide, 3 fused propagate+collide, 4 pack. */
+int d2q37_set_profiling(d2q37_lattice* h, int on);
+int d2q37_kernel_times(d2q37_lattice* h, double ms[5], long counts[5]);
+/* Average device time (ms) of the last step's halo phase that was not hidden
+ * behind interior compute (0 for single-domain lattices); see DESIGN.md. */
+double d2q37_exposed_halo_ms(const d2q37_lattice* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* D2Q37_B200_H */

@@ -1,0 +1,951 @@
+// d2q37_capi.cu -- the C-ABI of include/d2q37_b200.h: device lattice handle,
+// storage, the per-step schedule (single domain and y-slab), load/dump.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "d2q37_b200.h"
+#include "d2q37_device.cuh"
+#include "d2q37_internal.h"
+#include "d2q37_kernels.cuh"
+
+using namespace d2q37;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr int kTransportNone = 0;
+constexpr int kTransportNccl = 1;
+constexpr int kTransportGroup = 2;
+constexpr int kEventRing = 64;
+
+}  // namespace
+
+namespace d2q37 {
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace d2q37
+
+struct d2q37_lattice {
+    int layout = D2Q37_SOA;
+    int device = 0;
+    DevGeo g{};
+    size_t buf_elems = 0;
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;  // index of the state buffer ("prv"); 1 - cur is "nxt"
+    ModelParams mp{};
+    int math = D2Q37_MATH_FAST;
+    Offsets off_pull{};
+    cudaStream_t stream = nullptr;
+    std::shared_ptr<CUstream_st> stream_owner;  // shared by the slabs of a group
+    int* d_flag = nullptr;
+    int* h_flag = nullptr;
+    double* d_part = nullptr;
+    double* stage = nullptr;
+    long time_step = 0;
+
+    // y-slab decomposition
+    int rank = 0, nranks = 1, y0 = 0, ly_global = 0;
+    int transport = kTransportNone;
+    int nslots = 0;
+    double* send_lo = nullptr;
+    double* send_hi = nullptr;
+    double* recv_lo = nullptr;
+    double* recv_hi = nullptr;
+    void* comm = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
+    cudaEvent_t ev_int[kEventRing] = {}, ev_wait[kEventRing] = {};
+    int ev_count = 0;
+    PackParams pack{};
+    EdgeParams edge_base{};
+    // optional per-kernel timing (d2q37_set_profiling): event pairs around launches
+    bool prof_on = false;
+    struct ProfEntry {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfEntry> prof_pending;
+    std::vector<cudaEvent_t> prof_free;
+    std::vector<d2q37_lattice*> group;  // transport == group: all slabs, in rank order
+};
+
+namespace {
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        const cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(D2Q37_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                                 \
+    } while (0)
+
+#define RET(call)                          \
+    do {                                   \
+        const int r_ = (call);             \
+        if (r_ != D2Q37_OK) return r_;     \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        cudaGetDevice(&now);
+        if (prev >= 0 && now != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Geometry checks of layout.cpp:12-24 plus the device limits.
+int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
+    if (layout == D2Q37_AOS || layout == D2Q37_CAOSOA)
+        return fail(D2Q37_ERR_UNSUPPORTED, "layout %d (AoS/CAoSoA) has no device implementation; use SoA or CSoA",
+                    layout);
+    if (layout != D2Q37_SOA && layout != D2Q37_CSOA) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown layout %d", layout);
+    if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");
+    if (lx > 65535) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lx > 65535 not supported");
+    if (layout == D2Q37_SOA) vl = 1;
+    if (layout == D2Q37_CSOA) {
+        if (!is_pow2(vl)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "vl must be a power of two");
+        if (ly % vl != 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "ly divisible by vl");
+        if (ly / vl < kHalo) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lane strip shorter than its halo (ly/vl < hy)");
+    }
+    g->lx = lx;
+    g->ly = ly;
+    g->vl = vl;
+    g->strip = ly / vl;
+    g->sy = g->strip + 2 * kHalo;
+    g->px = lx + 2 * kHalo;
+    // 256-byte alignment of every column's first physical element.
+    const int per = 32 / std::gcd(vl, 32);
+    g->pitch = (g->sy + per - 1) / per * per;
+    g->lead = (32 - (kHalo * vl) % 32) % 32;
+    g->plane = (long long)g->px * g->pitch * vl;
+    g->plane = (g->plane + 31) / 32 * 32;
+    return D2Q37_OK;
+}
+
+void fill_offsets(d2q37_lattice* h, int corrupt = -1) {
+    const DevGeo& g = h->g;
+    for (int p = 0; p < kNpop; ++p) {
+        // build_offset_table (kernels.cpp:180-195): pull from (x - cx, y - cy).
+        h->off_pull.o[p] = (long long)p * g.plane - ((long long)cx_of(p) * g.pitch + cy_of(p)) * g.vl;
+        if (p == corrupt) h->off_pull.o[p] += 1;
+    }
+}
+
+int upload_model(d2q37_lattice* h, const d2q37_model* m) {
+    for (int p = 0; p < kNpop; ++p)
+        if (m->cx[p] != cx_of(p) || m->cy[p] != cy_of(p))
+            return fail(D2Q37_ERR_INVALID_ARGUMENT,
+                        "model velocity %d is (%d,%d), the device velocity set expects (%d,%d)", p, m->cx[p],
+                        m->cy[p], cx_of(p), cy_of(p));
+    for (int i = 0; i < kNpop; ++i)
+        for (int k = 0; k < kNmom; ++k) {
+            const double v = m->eq[i * kNmom + k];
+            if (eq_structural_zero(i, k) && v != 0.0)
+                return fail(D2Q37_ERR_INVALID_ARGUMENT, "Hermite table entry (%d,%d) must be zero", i, k);
+            h->mp.eq[i][k] = v;
+        }
+    for (int i = 0; i < kNpop; ++i) h->mp.w[i] = m->w[i];
+    h->mp.t0 = m->t0;
+    return D2Q37_OK;
+}
+
+void make_slot_tables(d2q37_lattice* h) {
+    // Ghost row at distance d below the slab (gy = -d) is read only by
+    // populations with cy >= d (15 + 8 + 3 = 26 pop-rows); symmetric above.
+    EdgeParams& ep = h->edge_base;
+    std::memset(ep.lo_slot, -1, sizeof ep.lo_slot);
+    std::memset(ep.hi_slot, -1, sizeof ep.hi_slot);
+    int nlo = 0, nhi = 0;
+    for (int d = 1; d <= kHalo; ++d)
+        for (int p = 0; p < kNpop; ++p) {
+            if (cy_of(p) >= d) {
+                ep.lo_slot[d - 1][p] = (signed char)nlo;
+                h->pack.hi_d[nlo] = (signed char)d;  // our rows ny-d feed the hi neighbour's low ghosts
+                h->pack.hi_p[nlo] = (signed char)p;
+                ++nlo;
+            }
+            if (cy_of(p) <= -d) {
+                ep.hi_slot[d - 1][p] = (signed char)nhi;
+                h->pack.lo_d[nhi] = (signed char)d;
+                h->pack.lo_p[nhi] = (signed char)p;
+                ++nhi;
+            }
+        }
+    h->nslots = nlo;  // == nhi by the y-symmetry of the velocity set
+    h->pack.nslots = nlo;
+    for (int p = 0; p < kNpop; ++p)
+        for (int q = 0; q < kNpop; ++q)
+            if (cx_of(q) == cx_of(p) && cy_of(q) == -cy_of(p)) ep.ybar[p] = (signed char)q;
+}
+
+int new_stream(d2q37_lattice* h) {
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    h->stream_owner = std::shared_ptr<CUstream_st>(s, [](cudaStream_t p) { cudaStreamDestroy(p); });
+    h->stream = s;
+    return D2Q37_OK;
+}
+
+int alloc_lattice(d2q37_lattice* h) {
+    DeviceGuard dg(h->device);
+    const DevGeo& g = h->g;
+    h->buf_elems = size_t(g.lead + kNpop * g.plane + 32);
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&h->buf[b], h->buf_elems * sizeof(double)));
+        CK(cudaMemset(h->buf[b], 0, h->buf_elems * sizeof(double)));  // AlignedBuffer is zeroed (layout.cpp:101)
+    }
+    CK(cudaMalloc(&h->d_flag, sizeof(int)));
+    CK(cudaMemset(h->d_flag, 0, sizeof(int)));
+    CK(cudaMallocHost(&h->h_flag, sizeof(int)));
+    CK(cudaMalloc(&h->d_part, size_t(g.lx) * 4 * sizeof(double)));
+    if (!h->stream) RET(new_stream(h));
+    make_slot_tables(h);
+    fill_offsets(h);
+    return D2Q37_OK;
+}
+
+int alloc_exchange(d2q37_lattice* h) {
+    DeviceGuard dg(h->device);
+    const size_t n = size_t(h->nslots) * h->g.lx;
+    CK(cudaMalloc(&h->send_lo, n * sizeof(double)));
+    CK(cudaMalloc(&h->send_hi, n * sizeof(double)));
+    CK(cudaMalloc(&h->recv_lo, n * sizeof(double)));
+    CK(cudaMalloc(&h->recv_hi, n * sizeof(double)));
+    CK(cudaMemset(h->recv_lo, 0, n * sizeof(double)));
+    CK(cudaMemset(h->recv_hi, 0, n * sizeof(double)));
+    h->pack.send_lo = h->send_lo;
+    h->pack.send_hi = h->send_hi;
+    CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming));
+    for (int i = 0; i < kEventRing; ++i) {
+        CK(cudaEventCreate(&h->ev_int[i]));
+        CK(cudaEventCreate(&h->ev_wait[i]));
+    }
+    return D2Q37_OK;
+}
+
+void free_lattice(d2q37_lattice* h) {
+    DeviceGuard dg(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+    for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->send_lo, h->send_hi, h->recv_lo, h->recv_hi})
+        if (p) cudaFree(p);
+    if (h->d_flag) cudaFree(h->d_flag);
+    if (h->h_flag) cudaFreeHost(h->h_flag);
+    if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_recv) cudaEventDestroy(h->ev_recv);
+    for (int i = 0; i < kEventRing; ++i) {
+        if (h->ev_int[i]) cudaEventDestroy(h->ev_int[i]);
+        if (h->ev_wait[i]) cudaEventDestroy(h->ev_wait[i]);
+    }
+    for (auto& e : h->prof_pending) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    for (cudaEvent_t e : h->prof_free) cudaEventDestroy(e);
+    if (h->comm) nccl_comm_destroy(h->comm);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    h->stream_owner.reset();
+    (void)cudaGetLastError();  // teardown errors must not leak into later launches
+}
+
+size_t canon_count(const d2q37_lattice* h) { return size_t(kNpop) * h->g.lx * h->g.ly; }
+
+int check_handle(const d2q37_lattice* h) {
+    if (!h) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null lattice handle");
+    return D2Q37_OK;
+}
+
+cudaEvent_t prof_event(d2q37_lattice* h) {
+    if (h->prof_free.empty()) {
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    cudaEvent_t e = h->prof_free.back();
+    h->prof_free.pop_back();
+    return e;
+}
+
+// Records an event pair around the launches in its scope when profiling is on.
+struct ProfScope {
+    d2q37_lattice* h;
+    int cls;
+    cudaEvent_t a = nullptr;
+    ProfScope(d2q37_lattice* h_, int cls_) : h(h_), cls(cls_) {
+        if (h->prof_on) {
+            a = prof_event(h);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = prof_event(h);
+            cudaEventRecord(b, h->stream);
+            h->prof_pending.push_back({cls, a, b});
+        }
+    }
+};
+
+enum { kProfEdge = 0, kProfPropagate = 1, kProfCollide = 2, kProfFused = 3, kProfPack = 4, kProfClasses = 5 };
+
+Segments all_sites(const DevGeo& g) {
+    Segments s;
+    s.q0[0] = 0;
+    s.q0[1] = 0;
+    s.nq = g.ly;
+    return s;
+}
+
+int face_lo_of(const d2q37_lattice* h, int bc) {
+    if (h->nranks == 1) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
+    if (h->rank == 0 && bc == D2Q37_BC_WALL) return kFaceWall;
+    return kFaceRemote;
+}
+int face_hi_of(const d2q37_lattice* h, int bc) {
+    if (h->nranks == 1) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
+    if (h->rank == h->nranks - 1 && bc == D2Q37_BC_WALL) return kFaceWall;
+    return kFaceRemote;
+}
+int lo_peer_of(const d2q37_lattice* h, int bc) {
+    return face_lo_of(h, bc) == kFaceRemote ? (h->rank - 1 + h->nranks) % h->nranks : -1;
+}
+int hi_peer_of(const d2q37_lattice* h, int bc) {
+    return face_hi_of(h, bc) == kFaceRemote ? (h->rank + 1) % h->nranks : -1;
+}
+
+int validate_bc(const d2q37_lattice* h, int bc) {
+    if (bc != D2Q37_BC_PERIODIC && bc != D2Q37_BC_WALL) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown bc %d", bc);
+    if (bc == D2Q37_BC_WALL && h->ly_global < kHalo)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "wall bc needs ly >= 3 (single specular image)");
+    if (h->nranks > 1 && h->g.strip < kHalo)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "slab lane strip shorter than the halo");
+    return D2Q37_OK;
+}
+
+int edge(d2q37_lattice* h, int bc, int filter) {
+    EdgeParams ep = h->edge_base;
+    ep.face_lo = face_lo_of(h, bc);
+    ep.face_hi = face_hi_of(h, bc);
+    ep.filter = filter;
+    ep.recv_lo = h->recv_lo;
+    ep.recv_hi = h->recv_hi;
+    ProfScope ps(h, kProfEdge);
+    CK(launch_edge(h->buf[h->cur], h->g, ep, h->stream));
+    return D2Q37_OK;
+}
+
+bool remote_faces(const d2q37_lattice* h, int bc) {
+    return face_lo_of(h, bc) == kFaceRemote || face_hi_of(h, bc) == kFaceRemote;
+}
+
+// Pack the slab's boundary rows and (NCCL) start the exchange on the comm
+// stream.  Group transport moves the data in group_exchange().
+int exchange_begin(d2q37_lattice* h, int bc) {
+    {
+        ProfScope ps(h, kProfPack);
+        CK(launch_pack(h->buf[h->cur], h->g, h->pack, h->stream));
+    }
+    if (h->transport == kTransportNccl) {
+        CK(cudaEventRecord(h->ev_pack, h->stream));
+        CK(cudaStreamWaitEvent(h->comm_stream, h->ev_pack, 0));
+        std::string why;
+        const int rc = nccl_exchange(h->comm, h->comm_stream, h->send_lo, h->recv_lo, lo_peer_of(h, bc), h->send_hi,
+                                     h->recv_hi, hi_peer_of(h, bc), size_t(h->nslots) * h->g.lx, &why);
+        if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+        CK(cudaEventRecord(h->ev_recv, h->comm_stream));
+    }
+    return D2Q37_OK;
+}
+
+int exchange_wait(d2q37_lattice* h) {
+    if (h->transport == kTransportNccl) CK(cudaStreamWaitEvent(h->stream, h->ev_recv, 0));
+    return D2Q37_OK;
+}
+
+int group_exchange(std::vector<d2q37_lattice*>& slabs, int bc) {
+    const int n = int(slabs.size());
+    for (int r = 0; r < n; ++r) {
+        d2q37_lattice* h = slabs[r];
+        const size_t bytes = size_t(h->nslots) * h->g.lx * sizeof(double);
+        const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+        if (lo >= 0) CK(cudaMemcpyAsync(h->recv_lo, slabs[lo]->send_hi, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        if (hi >= 0) CK(cudaMemcpyAsync(h->recv_hi, slabs[hi]->send_lo, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    return D2Q37_OK;
+}
+
+bool can_split(const d2q37_lattice* h) { return h->g.strip >= 2 * kHalo + 1; }
+
+// Sites whose pull stencil stays inside the slab's own rows: q in [3vl, ly-3vl).
+Segments interior(const DevGeo& g) {
+    Segments s;
+    s.q0[0] = kHalo * g.vl;
+    s.q0[1] = 0;
+    s.nq = g.ly - 2 * kHalo * g.vl;
+    return s;
+}
+Segments boundary(const DevGeo& g) {
+    Segments s;
+    s.q0[0] = 0;
+    s.q0[1] = g.ly - kHalo * g.vl;
+    s.nq = kHalo * g.vl;
+    return s;
+}
+
+int collide_launch(d2q37_lattice* h, int src, int dst, double omega, bool shift, const Segments& seg, int nseg) {
+    ProfScope ps(h, shift ? kProfFused : kProfCollide);
+    CK(launch_collide(h->buf[src], h->buf[dst], h->g, h->off_pull, h->mp, omega, h->math == D2Q37_MATH_STRICT, shift,
+                      seg, nseg, h->d_flag, h->stream));
+    return D2Q37_OK;
+}
+
+// One time step on a single domain: edge -> fused (or propagate + collide).
+int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
+    RET(edge(h, bc, kEdgeAll));
+    const Segments all = all_sites(h->g);
+    if (variant == D2Q37_FUSED) {
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1));
+        h->cur = 1 - h->cur;
+    } else {
+        {
+            ProfScope ps(h, kProfPropagate);
+            CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, all, 1, h->stream));
+        }
+        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1));
+    }
+    ++h->time_step;
+    return D2Q37_OK;
+}
+
+// Slab step, phase 1 (before the halos are needed): local ghosts + interior.
+int slab_phase1(d2q37_lattice* h, double omega, int variant, int bc) {
+    RET(edge(h, bc, kEdgeLocal));
+    if (variant == D2Q37_FUSED && can_split(h)) {
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, interior(h->g), 1));
+        if (h->transport == kTransportNccl) CK(cudaEventRecord(h->ev_int[h->ev_count % kEventRing], h->stream));
+    }
+    return D2Q37_OK;
+}
+
+// Slab step, phase 2 (after the halos landed): remote ghosts + boundary rows.
+int slab_phase2(d2q37_lattice* h, double omega, int variant, int bc) {
+    RET(exchange_wait(h));
+    const bool split = variant == D2Q37_FUSED && can_split(h);
+    if (h->transport == kTransportNccl && split) {
+        CK(cudaEventRecord(h->ev_wait[h->ev_count % kEventRing], h->stream));
+        ++h->ev_count;
+    }
+    RET(edge(h, bc, kEdgeRemote));
+    const Segments all = all_sites(h->g);
+    if (variant == D2Q37_FUSED) {
+        if (split)
+            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, boundary(h->g), 2));
+        else
+            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1));
+        h->cur = 1 - h->cur;
+    } else {
+        CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, all, 1, h->stream));
+        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1));
+    }
+    ++h->time_step;
+    return D2Q37_OK;
+}
+
+int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n, bool src_device) {
+    RET(check_handle(h));
+    if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 (prv) or 1 (nxt)");
+    if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "from_canonical: dimension mismatch");
+    if (!src) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null canonical array");
+    DeviceGuard dg(h->device);
+    const DevGeo& g = h->g;
+    double* dst = h->buf[which == 0 ? h->cur : 1 - h->cur];
+    const size_t plane_vals = size_t(g.lx) * g.ly;
+    if (g.vl == 1 && !src_device) {
+        // SoA: one pitched copy per population straight from the host array.
+        for (int p = 0; p < kNpop; ++p)
+            CK(cudaMemcpy2DAsync(dst + col_base(g, kHalo) + p * g.plane, size_t(g.pitch) * sizeof(double),
+                                 src + p * plane_vals, size_t(g.ly) * sizeof(double), size_t(g.ly) * sizeof(double),
+                                 size_t(g.lx), cudaMemcpyHostToDevice, h->stream));
+    } else {
+        if (!src_device && !h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
+        for (int p = 0; p < kNpop; ++p) {
+            const double* plane = src + p * plane_vals;
+            if (!src_device) {
+                CK(cudaMemcpyAsync(h->stage, plane, plane_vals * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+                plane = h->stage;
+            }
+            CK(launch_scatter(dst, g, plane, p, h->stream));
+        }
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return D2Q37_OK;
+}
+
+int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool out_device) {
+    RET(check_handle(h));
+    if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 (prv) or 1 (nxt)");
+    if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "to_canonical: dimension mismatch");
+    if (!out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null canonical array");
+    DeviceGuard dg(h->device);
+    const DevGeo& g = h->g;
+    const double* src = h->buf[which == 0 ? h->cur : 1 - h->cur];
+    const size_t plane_vals = size_t(g.lx) * g.ly;
+    if (g.vl == 1 && !out_device) {
+        for (int p = 0; p < kNpop; ++p)
+            CK(cudaMemcpy2DAsync(out + p * plane_vals, size_t(g.ly) * sizeof(double), src + col_base(g, kHalo) + p * g.plane,
+                                 size_t(g.pitch) * sizeof(double), size_t(g.ly) * sizeof(double), size_t(g.lx),
+                                 cudaMemcpyDeviceToHost, h->stream));
+    } else {
+        if (!out_device && !h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
+        for (int p = 0; p < kNpop; ++p) {
+            double* plane = out_device ? out + p * plane_vals : h->stage;
+            CK(launch_gather(src, g, plane, p, h->stream));
+            if (!out_device)
+                CK(cudaMemcpyAsync(out + p * plane_vals, h->stage, plane_vals * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h->stream));
+        }
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return D2Q37_OK;
+}
+
+int create_impl(int layout, int lx, int ly, int vl, int device, d2q37_lattice** out, int rank, int nranks) {
+    if (!out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad rank %d / %d", rank, nranks);
+    if (ly % nranks != 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "ly=%d not divisible by %d slabs", ly, nranks);
+    std::unique_ptr<d2q37_lattice> h(new (std::nothrow) d2q37_lattice());
+    if (!h) return fail(D2Q37_ERR_CUDA, "out of host memory");
+    RET(make_geometry(layout, lx, ly / nranks, vl, &h->g));
+    h->layout = layout;
+    h->device = device;
+    h->rank = rank;
+    h->nranks = nranks;
+    h->y0 = rank * (ly / nranks);
+    h->ly_global = ly;
+    d2q37_model m;
+    build_model(&m);
+    RET(upload_model(h.get(), &m));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(D2Q37_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
+    const int rc = alloc_lattice(h.get());
+    if (rc != D2Q37_OK) {
+        free_lattice(h.get());
+        return rc;
+    }
+    *out = h.release();
+    return D2Q37_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+const char* d2q37_last_error(void) { return g_last_error.c_str(); }
+
+int d2q37_model_d2q37(d2q37_model* out) {
+    if (!out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null model");
+    try {
+        build_model(out);
+    } catch (const std::exception& e) {
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "%s", e.what());
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_create(int layout, int lx, int ly, int vl, int device, d2q37_lattice** out) {
+    return create_impl(layout, lx, ly, vl, device, out, 0, 1);
+}
+
+int d2q37_destroy(d2q37_lattice* h) {
+    if (!h) return D2Q37_OK;
+    free_lattice(h);
+    delete h;
+    return D2Q37_OK;
+}
+
+int d2q37_set_model(d2q37_lattice* h, const d2q37_model* m) {
+    RET(check_handle(h));
+    if (!m) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null model");
+    return upload_model(h, m);
+}
+
+int d2q37_set_math(d2q37_lattice* h, int math) {
+    RET(check_handle(h));
+    if (math != D2Q37_MATH_FAST && math != D2Q37_MATH_STRICT) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown math mode");
+    h->math = math;
+    return D2Q37_OK;
+}
+
+int d2q37_set_stream(d2q37_lattice* h, void* stream) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    CK(cudaStreamSynchronize(h->stream));
+    h->stream_owner.reset();
+    h->stream = static_cast<cudaStream_t>(stream);
+    if (!h->stream) RET(new_stream(h));
+    return D2Q37_OK;
+}
+
+void* d2q37_get_stream(d2q37_lattice* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int d2q37_geometry(const d2q37_lattice* h, int out[6]) {
+    RET(check_handle(h));
+    out[0] = h->g.lx;
+    out[1] = h->g.ly;
+    out[2] = h->g.vl;
+    out[3] = h->g.strip;
+    out[4] = h->g.sy;
+    out[5] = h->g.px;
+    return D2Q37_OK;
+}
+
+size_t d2q37_device_bytes(const d2q37_lattice* h) {
+    if (!h) return 0;
+    return 2 * h->buf_elems * sizeof(double) + 4 * size_t(h->nslots) * h->g.lx * sizeof(double) * (h->send_lo ? 1 : 0);
+}
+
+long d2q37_time_step(const d2q37_lattice* h) { return h ? h->time_step : -1; }
+
+int d2q37_load_canonical(d2q37_lattice* h, const double* host, size_t n) {
+    return load_canonical_impl(h, 0, host, n, false);
+}
+int d2q37_dump_canonical(d2q37_lattice* h, double* host, size_t n) { return dump_canonical_impl(h, 0, host, n, false); }
+int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n) {
+    return load_canonical_impl(h, which, host, n, false);
+}
+int d2q37_dump_buffer(d2q37_lattice* h, int which, double* host, size_t n) {
+    return dump_canonical_impl(h, which, host, n, false);
+}
+int d2q37_load_buffer_device(d2q37_lattice* h, int which, const double* dev, size_t n) {
+    return load_canonical_impl(h, which, dev, n, true);
+}
+int d2q37_dump_buffer_device(d2q37_lattice* h, int which, double* dev, size_t n) {
+    return dump_canonical_impl(h, which, dev, n, true);
+}
+
+static size_t padded_count(const d2q37_lattice* h) {
+    return size_t(kNpop) * h->g.px * h->g.sy * h->g.vl;
+}
+
+int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
+    RET(check_handle(h));
+    if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
+    if (n != padded_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "padded size mismatch (want %zu)", padded_count(h));
+    DeviceGuard dg(h->device);
+    std::vector<double> dev(h->buf_elems);
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(dev.data(), h->buf[which == 0 ? h->cur : 1 - h->cur], h->buf_elems * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    const DevGeo& g = h->g;
+    size_t i = 0;
+    for (int p = 0; p < kNpop; ++p)
+        for (int X = 0; X < g.px; ++X)
+            for (int j = 0; j < g.sy; ++j)
+                for (int k = 0; k < g.vl; ++k) host[i++] = dev[size_t(elem_of(g, p, X, j, k))];
+    return D2Q37_OK;
+}
+
+int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n) {
+    RET(check_handle(h));
+    if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
+    if (n != padded_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "padded size mismatch (want %zu)", padded_count(h));
+    DeviceGuard dg(h->device);
+    double* d = h->buf[which == 0 ? h->cur : 1 - h->cur];
+    std::vector<double> dev(h->buf_elems);
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(dev.data(), d, h->buf_elems * sizeof(double), cudaMemcpyDeviceToHost));
+    const DevGeo& g = h->g;
+    size_t i = 0;
+    for (int p = 0; p < kNpop; ++p)
+        for (int X = 0; X < g.px; ++X)
+            for (int j = 0; j < g.sy; ++j)
+                for (int k = 0; k < g.vl; ++k) dev[size_t(elem_of(g, p, X, j, k))] = host[i++];
+    CK(cudaMemcpy(d, dev.data(), h->buf_elems * sizeof(double), cudaMemcpyHostToDevice));
+    return D2Q37_OK;
+}
+
+int d2q37_bc(d2q37_lattice* h, int bc) {
+    RET(check_handle(h));
+    RET(validate_bc(h, bc));
+    DeviceGuard dg(h->device);
+    if (h->nranks > 1 && remote_faces(h, bc)) {
+        if (h->transport == kTransportGroup) {
+            // every slab of the group packs, then halos move, then edges run
+            for (d2q37_lattice* s : h->group) RET(exchange_begin(s, bc));
+            RET(group_exchange(h->group, bc));
+            for (d2q37_lattice* s : h->group) RET(edge(s, bc, kEdgeAll));
+            return D2Q37_OK;
+        }
+        RET(exchange_begin(h, bc));
+        RET(exchange_wait(h));
+    }
+    return edge(h, bc, kEdgeAll);
+}
+
+int d2q37_propagate(d2q37_lattice* h) { return d2q37_propagate_corrupt(h, -1); }
+
+int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    if (corrupt_population >= kNpop) return fail(D2Q37_ERR_INVALID_ARGUMENT, "corrupt_population out of range");
+    Offsets off = h->off_pull;
+    if (corrupt_population >= 0) off.o[corrupt_population] += 1;
+    ProfScope ps(h, kProfPropagate);
+    CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, off, all_sites(h->g), 1, h->stream));
+    return D2Q37_OK;
+}
+
+int d2q37_collide(d2q37_lattice* h, double omega) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1);
+}
+
+int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) {
+    RET(check_handle(h));
+    RET(validate_bc(h, bc));
+    if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    DeviceGuard dg(h->device);
+    if (h->transport == kTransportGroup) {
+        d2q37_lattice** slabs = h->group.data();
+        return d2q37_group_step(slabs, int(h->group.size()), omega, nsteps, variant, bc);
+    }
+    for (int s = 0; s < nsteps; ++s) {
+        if (h->nranks > 1 && remote_faces(h, bc)) {
+            RET(exchange_begin(h, bc));
+            RET(slab_phase1(h, omega, variant, bc));
+            RET(slab_phase2(h, omega, variant, bc));
+        } else {
+            RET(step_local(h, omega, variant, bc));
+        }
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_swap_buffers(d2q37_lattice* h) {
+    RET(check_handle(h));
+    h->cur = 1 - h->cur;
+    return D2Q37_OK;
+}
+
+int d2q37_sync(d2q37_lattice* h) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    CK(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->comm_stream) CK(cudaStreamSynchronize(h->comm_stream));
+    if (*h->h_flag) {
+        *h->h_flag = 0;
+        CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_moments(d2q37_lattice* h, double out[4]) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    CK(launch_moments(h->buf[h->cur], h->g, h->d_part, h->stream));
+    std::vector<double> part(size_t(h->g.lx) * 4);
+    CK(cudaMemcpyAsync(part.data(), h->d_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < 4; ++i) out[i] = 0.0;
+    for (int x = 0; x < h->g.lx; ++x)
+        for (int i = 0; i < 4; ++i) out[i] += part[size_t(x) * 4 + i];
+    return D2Q37_OK;
+}
+
+int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* params, const d2q37_model* m,
+                       double* out, size_t n, int nthreads) {
+    if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");
+    if (!out || n != size_t(kNpop) * lx * ly) return fail(D2Q37_ERR_INVALID_ARGUMENT, "output size mismatch");
+    if ((kind == D2Q37_INIT_EQUILIBRIUM || kind == D2Q37_INIT_SHEAR) && !params)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "initialiser needs params");
+    d2q37_model local;
+    if (!m) {
+        build_model(&local);
+        m = &local;
+    }
+    try {
+        make_lattice(kind, lx, ly, seed, params, *m, out, nthreads);
+    } catch (const std::exception& e) {
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "%s", e.what());
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
+    RET(check_handle(h));
+    if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
+    DeviceGuard dg(h->device);
+    CK(launch_philox(h->buf[which == 0 ? h->cur : 1 - h->cur], h->g, seed, h->y0, h->ly_global, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return D2Q37_OK;
+}
+
+// ---- multi-GPU ------------------------------------------------------------
+
+int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]) {
+    std::string why;
+    const int rc = nccl_unique_id(id, &why);
+    if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+    return D2Q37_OK;
+}
+
+int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
+                      const unsigned char id[D2Q37_NCCL_ID_BYTES], d2q37_lattice** out) {
+    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks));
+    d2q37_lattice* h = *out;
+    if (nranks == 1) return D2Q37_OK;
+    auto bail = [&](int rc) {
+        d2q37_destroy(h);
+        *out = nullptr;
+        return rc;
+    };
+    if (!id) return bail(fail(D2Q37_ERR_INVALID_ARGUMENT, "null NCCL id"));
+    int rc = alloc_exchange(h);
+    if (rc != D2Q37_OK) return bail(rc);
+    {
+        DeviceGuard dg(device);
+        if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(D2Q37_ERR_CUDA, "comm stream creation failed"));
+        std::string why;
+        rc = nccl_comm_init(&h->comm, nranks, id, rank, &why);
+        if (rc != D2Q37_OK) return bail(fail(rc, "%s", why.c_str()));
+    }
+    h->transport = kTransportNccl;
+    return D2Q37_OK;
+}
+
+int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslabs, d2q37_lattice** out) {
+    if (!out || nslabs < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad group arguments");
+    std::vector<d2q37_lattice*> slabs(nslabs, nullptr);
+    auto bail = [&](int rc) {
+        for (d2q37_lattice* s : slabs) d2q37_destroy(s);
+        return rc;
+    };
+    for (int r = 0; r < nslabs; ++r) {
+        int rc = create_impl(layout, lx, ly, vl, device, &slabs[r], r, nslabs);
+        if (rc != D2Q37_OK) return bail(rc);
+        if (nslabs > 1) {
+            rc = alloc_exchange(slabs[r]);
+            if (rc != D2Q37_OK) return bail(rc);
+        }
+    }
+    // One stream for the whole group: slabs never wait on each other inside a kernel.
+    for (int r = 1; r < nslabs; ++r) {
+        cudaStreamSynchronize(slabs[r]->stream);
+        slabs[r]->stream_owner = slabs[0]->stream_owner;
+        slabs[r]->stream = slabs[0]->stream;
+    }
+    for (int r = 0; r < nslabs; ++r) {
+        if (nslabs > 1) slabs[r]->transport = kTransportGroup;
+        slabs[r]->group = slabs;
+        out[r] = slabs[r];
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nsteps, int variant, int bc) {
+    if (!slabs_in || nslabs < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad group");
+    std::vector<d2q37_lattice*> slabs(slabs_in, slabs_in + nslabs);
+    for (d2q37_lattice* h : slabs) {
+        RET(check_handle(h));
+        RET(validate_bc(h, bc));
+    }
+    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    DeviceGuard dg(slabs[0]->device);
+    for (int s = 0; s < nsteps; ++s) {
+        if (nslabs == 1 || !remote_faces(slabs[0], bc)) {
+            for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
+            continue;
+        }
+        for (d2q37_lattice* h : slabs) RET(exchange_begin(h, bc));
+        for (d2q37_lattice* h : slabs) RET(slab_phase1(h, omega, variant, bc));
+        RET(group_exchange(slabs, bc));
+        for (d2q37_lattice* h : slabs) RET(slab_phase2(h, omega, variant, bc));
+    }
+    return D2Q37_OK;
+}
+
+int d2q37_set_profiling(d2q37_lattice* h, int on) {
+    RET(check_handle(h));
+    h->prof_on = on != 0;
+    return D2Q37_OK;
+}
+
+int d2q37_kernel_times(d2q37_lattice* h, double ms[5], long counts[5]) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    CK(cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < kProfClasses; ++i) {
+        ms[i] = 0.0;
+        counts[i] = 0;
+    }
+    for (auto& e : h->prof_pending) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, e.a, e.b));
+        ms[e.cls] += t;
+        counts[e.cls] += 1;
+        h->prof_free.push_back(e.a);
+        h->prof_free.push_back(e.b);
+    }
+    h->prof_pending.clear();
+    return D2Q37_OK;
+}
+
+int d2q37_slab_info(const d2q37_lattice* h, int out[4]) {
+    RET(check_handle(h));
+    out[0] = h->rank;
+    out[1] = h->nranks;
+    out[2] = h->y0;
+    out[3] = h->g.ly;
+    return D2Q37_OK;
+}
+
+double d2q37_exposed_halo_ms(const d2q37_lattice* h) {
+    if (!h || h->transport != kTransportNccl || h->ev_count == 0) return 0.0;
+    DeviceGuard dg(h->device);
+    cudaStreamSynchronize(h->stream);
+    const int n = std::min(h->ev_count, kEventRing);
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->ev_int[i], h->ev_wait[i]) == cudaSuccess) sum += std::max(0.f, ms);
+    }
+    return sum / n;
+}
+
+}  // extern "C"

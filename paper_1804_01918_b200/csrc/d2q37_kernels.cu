@@ -1,0 +1,321 @@
+// d2q37_kernels.cu -- sm_100a kernels of the D2Q37 hot path.
+//
+//   k_propagate        propagate (kernels.cpp:50-85): per site, 37 pull loads
+//                      from up to 3 sites away, 37 streaming stores.
+//   k_collide<S,SHIFT> collide (kernels.cpp:120-156, model.cpp:242-298) and,
+//                      with SHIFT, the fused propagate+collide step kernel.
+//   k_edge             bc: every ghost slot of the padded store in one pass
+//                      (kernels.cpp:197-234 periodic, or specular walls, or
+//                      slab halos received from the neighbour ranks).
+//   k_pack             slab boundary rows -> contiguous send buffers.
+//   k_scatter/k_gather canonical plane <-> padded layout (dump.cpp:26-42).
+//   k_philox           BASELINE config-1 input generation on the device.
+//   k_moments          global mass / momentum / energy sums per column.
+//
+// All of them are HBM-streaming kernels (no tensor-core-shaped work: collide
+// is 2.57 FLOP/B, below the FP64 ridge).
+#include <cuda_runtime.h>
+
+#include "d2q37_device.cuh"
+#include "d2q37_kernels.cuh"
+
+namespace d2q37 {
+
+// ---------------------------------------------------------------------------
+// Streaming loads / stores.  Inputs are read once per launch (ld.global.nc);
+// outputs are not re-read before the lattice (GBs) has cycled through the
+// 126 MB L2, so they are written evict-first (st.global.cs).
+
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldg(p); }
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __restrict__ src,
+                                                              double* __restrict__ dst, DevGeo g, Offsets off,
+                                                              Segments seg) {
+    const int z = blockIdx.z;
+    const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= seg.q0[z] + seg.nq) return;
+    const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    double f[kNpop];
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + off.o[p]);
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);
+}
+
+template <bool STRICT, bool SHIFT>
+__global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
+    k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, ModelParams mp,
+              double omega, Segments seg, int* __restrict__ flag) {
+    const int z = blockIdx.z;
+    const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= seg.q0[z] + seg.nq) return;
+    const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    double f[kNpop];
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + (SHIFT ? off.o[p] : p * g.plane));
+    const bool bad = collide_site<STRICT>(f, omega, mp);
+    if (bad) *flag = 1;
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);
+}
+
+// ---------------------------------------------------------------------------
+// Edge (bc) kernel.  Thread t < nrows covers the ghost rows of every padded
+// column (6 rows x vl lanes per (p, X)); t >= nrows covers the physical rows of
+// the 6 ghost columns.  Every ghost slot is computed from its final physical
+// source directly (ghost-column images of ghost rows included), so one pass
+// reproduces the reference's y-then-x fill order.
+
+__device__ __forceinline__ int wrapi(int v, int n) {
+    const int r = v % n;
+    return r < 0 ? r + n : r;
+}
+
+__global__ void __launch_bounds__(256) k_edge(double* __restrict__ buf, DevGeo g, EdgeParams ep) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nrows = (long long)kNpop * g.px * 6 * g.vl;
+    if (t < nrows) {
+        const int k = int(t % g.vl);
+        const int r = int((t / g.vl) % 6);
+        const int X = int((t / (6LL * g.vl)) % g.px);
+        const int p = int(t / (6LL * g.vl * g.px));
+        const int xs = wrapi(X - kHalo, g.lx);
+        const int Xs = xs + kHalo;
+        int j, y, q = p;
+        bool remote = false;
+        const double* rbuf = nullptr;
+        int slot = -1;
+        if (r < 3) {  // low-y ghost rows of lane k
+            j = r;
+            const int yraw = k * g.strip + r - kHalo;
+            if (k > 0) {
+                y = yraw;
+            } else if (ep.face_lo == kFacePeriodic) {
+                y = wrapi(yraw, g.ly);
+            } else if (ep.face_lo == kFaceWall) {
+                y = -1 - yraw;
+                q = ep.ybar[p];
+            } else {
+                remote = true;
+                slot = ep.lo_slot[kHalo - r - 1][p];
+                rbuf = ep.recv_lo;
+                y = 0;
+            }
+        } else {  // high-y ghost rows of lane k
+            const int h = r - 3;
+            j = g.strip + kHalo + h;
+            const int yraw = (k + 1) * g.strip + h;
+            if (k < g.vl - 1) {
+                y = yraw;
+            } else if (ep.face_hi == kFacePeriodic) {
+                y = yraw % g.ly;
+            } else if (ep.face_hi == kFaceWall) {
+                y = 2 * g.ly - 1 - yraw;
+                q = ep.ybar[p];
+            } else {
+                remote = true;
+                slot = ep.hi_slot[h][p];
+                rbuf = ep.recv_hi;
+                y = 0;
+            }
+        }
+        if (remote) {
+            if (!(ep.filter & kEdgeRemote) || slot < 0) return;
+            buf[elem_of(g, p, X, j, k)] = rbuf[(long long)slot * g.lx + xs];
+        } else {
+            if (!(ep.filter & kEdgeLocal)) return;
+            buf[elem_of(g, p, X, j, k)] = buf[elem_of(g, q, Xs, y % g.strip + kHalo, y / g.strip)];
+        }
+        return;
+    }
+    if (!(ep.filter & kEdgeLocal)) return;
+    const long long u = t - nrows;
+    const long long ncols = (long long)kNpop * 6 * g.ly;
+    if (u >= ncols) return;
+    const int qq = int(u % g.ly);
+    const int c = int((u / g.ly) % 6);
+    const int p = int(u / (6LL * g.ly));
+    const int X = c < 3 ? c : g.lx + kHalo + (c - 3);
+    const int Xs = wrapi(X - kHalo, g.lx) + kHalo;
+    buf[col_base(g, X) + p * g.plane + qq] = buf[col_base(g, Xs) + p * g.plane + qq];
+}
+
+// Slab boundary rows -> send buffers, [slot][x] contiguous.  send_hi carries
+// rows ny-d of the (d, p) entries with cy_p >= d (the receiver's low ghosts),
+// send_lo rows d-1 of the entries with cy_p <= -d.
+__global__ void k_pack(const double* __restrict__ buf, DevGeo g, PackParams pp) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = pp.nslots * g.lx;
+    if (t >= 2 * total) return;
+    const bool hi = t >= total;
+    const int u = hi ? t - total : t;
+    const int slot = u / g.lx, x = u % g.lx;
+    const int d = hi ? pp.hi_d[slot] : pp.lo_d[slot];
+    const int p = hi ? pp.hi_p[slot] : pp.lo_p[slot];
+    const int y = hi ? g.ly - d : d - 1;
+    const double v = buf[elem_of(g, p, x + kHalo, y % g.strip + kHalo, y / g.strip)];
+    (hi ? pp.send_hi : pp.send_lo)[u] = v;
+}
+
+// canonical plane p (x-major, y-minor, lx*ly values) <-> padded store
+__global__ void k_scatter(double* __restrict__ buf, DevGeo g, const double* __restrict__ canon, int p) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)g.lx * g.ly) return;
+    const int x = int(t / g.ly), q = int(t % g.ly);
+    const int y = (q % g.vl) * g.strip + q / g.vl;
+    buf[col_base(g, x + kHalo) + p * g.plane + q] = canon[(long long)x * g.ly + y];
+}
+
+__global__ void k_gather(const double* __restrict__ buf, DevGeo g, double* __restrict__ canon, int p) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)g.lx * g.ly) return;
+    const int x = int(t / g.ly), q = int(t % g.ly);
+    const int y = (q % g.vl) * g.strip + q / g.vl;
+    canon[(long long)x * g.ly + y] = buf[col_base(g, x + kHalo) + p * g.plane + q];
+}
+
+// Philox4x32-10, key = seed, counter = site-major index (x*ly_global + y)*37 + p.
+__device__ __forceinline__ double philox_u01_dev(unsigned long long seed, unsigned long long ctr) {
+    unsigned int c0 = (unsigned int)ctr, c1 = (unsigned int)(ctr >> 32), c2 = 0u, c3 = 0u;
+    unsigned int k0 = (unsigned int)seed, k1 = (unsigned int)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const unsigned int hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const unsigned int hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const unsigned int n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    const unsigned long long bits = (unsigned long long)c0 | ((unsigned long long)c1 << 32);
+    return (double)(bits >> 11) * 0x1.0p-53;
+}
+
+__global__ void k_philox(double* __restrict__ buf, DevGeo g, unsigned long long seed, int y0, int ly_global) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= g.ly) return;
+    const int x = blockIdx.y;
+    const int y = (q % g.vl) * g.strip + q / g.vl;
+    const unsigned long long site = (unsigned long long)x * ly_global + (unsigned long long)(y0 + y);
+    const long long e = col_base(g, x + kHalo) + q;
+#pragma unroll 1
+    for (int p = 0; p < kNpop; ++p) buf[e + p * g.plane] = philox_u01_dev(seed, site * kNpop + p);
+}
+
+// Per-column sums {mass, jx, jy, sum |c|^2 f} in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_moments(const double* __restrict__ buf, DevGeo g, double* __restrict__ part) {
+    __shared__ double red[4][256];
+    const int X = blockIdx.x + kHalo;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = threadIdx.x; q < g.ly; q += blockDim.x) {
+        const long long e = col_base(g, X) + q;
+#pragma unroll
+        for (int p = 0; p < kNpop; ++p) {
+            const double v = buf[e + p * g.plane];
+            s[0] += v;
+            s[1] += cx_of(p) * v;
+            s[2] += cy_of(p) * v;
+            s[3] += (cx_of(p) * cx_of(p) + cy_of(p) * cy_of(p)) * v;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red[i][threadIdx.x] = s[i];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) part[blockIdx.x * 4 + i] = red[i][0];
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+
+static dim3 stream_grid(const DevGeo& g, const Segments& seg, int nseg) {
+    return dim3((seg.nq + kStreamThreads - 1) / kStreamThreads, g.lx, nseg);
+}
+
+cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+                             const Segments& seg, int nseg, cudaStream_t s) {
+    if (seg.nq <= 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    k_propagate<<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+                           const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
+                           int nseg, int* flag, cudaStream_t s) {
+    if (seg.nq <= 0) return cudaSuccess;
+    const dim3 grid = stream_grid(g, seg, nseg);
+    if (strict) {
+        if (shift)
+            k_collide<true, true><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+        else
+            k_collide<true, false><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+    } else {
+        if (shift)
+            k_collide<false, true><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+        else
+            k_collide<false, false><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s) {
+    long long total = (long long)kNpop * g.px * 6 * g.vl;
+    if (ep.filter & kEdgeLocal) total += (long long)kNpop * 6 * g.ly;
+    const long long blocks = (total + 255) / 256;
+    (void)cudaGetLastError();
+    k_edge<<<(unsigned)blocks, 256, 0, s>>>(buf, g, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const double* buf, const DevGeo& g, const PackParams& pp, cudaStream_t s) {
+    const int total = 2 * pp.nslots * g.lx;
+    if (total == 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    k_pack<<<(total + 255) / 256, 256, 0, s>>>(buf, g, pp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_plane, int p, cudaStream_t s) {
+    const long long n = (long long)g.lx * g.ly;
+    (void)cudaGetLastError();
+    k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf, g, canon_plane, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const double* buf, const DevGeo& g, double* canon_plane, int p, cudaStream_t s) {
+    const long long n = (long long)g.lx * g.ly;
+    (void)cudaGetLastError();
+    k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf, g, canon_plane, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed, int y0, int ly_global,
+                          cudaStream_t s) {
+    (void)cudaGetLastError();
+    k_philox<<<dim3((g.ly + 255) / 256, g.lx), 256, 0, s>>>(buf, g, seed, y0, ly_global);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s) {
+    (void)cudaGetLastError();
+    k_moments<<<g.lx, 256, 0, s>>>(buf, g, part);
+    return cudaGetLastError();
+}
+
+}  // namespace d2q37

@@ -1,0 +1,59 @@
+// d2q37_kernels.cuh -- launch interface of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "d2q37_device.cuh"
+
+namespace d2q37 {
+
+// 128-thread CTAs; the collide kernels keep f[37] in registers (~160 regs),
+// so at most 3 CTAs (12 warps) are resident per SM.
+constexpr int kStreamThreads = 128;
+constexpr int kCollideMinBlocks = 3;
+
+// Up to two q-ranges per launch (blockIdx.z selects one); each has nq sites
+// per column.  q indexes a column's physical elements in memory order.
+struct Segments {
+    int q0[2];
+    int nq;
+};
+
+enum { kFacePeriodic = 0, kFaceWall = 1, kFaceRemote = 2 };
+enum { kEdgeLocal = 1, kEdgeRemote = 2, kEdgeAll = 3 };
+
+struct EdgeParams {
+    const double* recv_lo;  // [slot][x]: neighbour's rows ny-d for (d, p) with cy_p >= d
+    const double* recv_hi;  // [slot][x]: neighbour's rows d-1 for (d, p) with cy_p <= -d
+    int face_lo, face_hi;
+    int filter;
+    int pad_;
+    signed char lo_slot[kHalo][kNpop];  // (d-1, p) -> slot or -1
+    signed char hi_slot[kHalo][kNpop];
+    signed char ybar[kNpop];            // y-mirror (cx, -cy)
+};
+
+constexpr int kMaxSlots = 32;  // 26 for D2Q37
+
+struct PackParams {
+    double* send_lo;
+    double* send_hi;
+    int nslots;
+    signed char lo_d[kMaxSlots], lo_p[kMaxSlots];  // entries of send_lo (cy_p <= -d)
+    signed char hi_d[kMaxSlots], hi_p[kMaxSlots];  // entries of send_hi (cy_p >= d)
+};
+
+cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+                             const Segments& seg, int nseg, cudaStream_t s);
+cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+                           const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
+                           int nseg, int* flag, cudaStream_t s);
+cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s);
+cudaError_t launch_pack(const double* buf, const DevGeo& g, const PackParams& pp, cudaStream_t s);
+cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_plane, int p, cudaStream_t s);
+cudaError_t launch_gather(const double* buf, const DevGeo& g, double* canon_plane, int p, cudaStream_t s);
+cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed, int y0, int ly_global,
+                          cudaStream_t s);
+cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
+
+}  // namespace d2q37

@@ -1,0 +1,358 @@
+"""Parity of the sm_100a kernels with the oracle and the compiled reference.
+
+Mirrors the reference's own kernel tests (proj/tests/test_kernels.cpp,
+acceptance.cpp, test_validation.cpp): propagate and bc bit-exact, collide
+bit-exact in STRICT math against the no-contraction oracle and within the
+BASELINE tolerance (1e-12 after one step, 1e-9 after 100) in FAST math,
+layout / variant / slab invariance bit for bit.  Everything runs through the
+C-ABI library (paper_1804_01918_b200/lib/libd2q37_b200.so).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, macros_fields, max_rel
+
+pytestmark = pytest.mark.gpu
+
+GEOMS = [(16, 32), (64, 128)]
+LAYOUTS = [("soa", 1), ("csoa", 1), ("csoa", 2), ("csoa", 4), ("csoa", 8)]
+
+
+def sim_of(lbm, layout, lx, ly, vl=1, **kw):
+    return lbm.Simulation(layout, lx, ly, vl, device=0, **kw)
+
+
+# --------------------------------------------------------------------------- propagate / bc (bit-exact)
+
+@pytest.mark.parametrize("lx,ly", GEOMS)
+@pytest.mark.parametrize("layout,vl", LAYOUTS)
+def test_propagate_bitwise_vs_oracle(gpu, lbm, po, lx, ly, layout, vl):
+    """test_kernels.cpp:148-169 / acceptance C3: halo_exchange + propagate == oracle_propagate."""
+    init = lbm.make_lattice("random", lx, ly, seed=1001 + lx)
+    want = po.orc_propagate(init, po.BC_PERIODIC)
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.load(init)
+    s.bc("periodic")
+    s.propagate_only()
+    assert np.array_equal(s.dump(which=1), want)
+
+
+@pytest.mark.parametrize("layout,vl,lx,ly", [("csoa", 4, 5, 12), ("soa", 1, 5, 2), ("soa", 1, 1, 8),
+                                             ("csoa", 32, 8, 96)])
+def test_propagate_edge_geometries(gpu, lbm, po, layout, vl, lx, ly):
+    """Strip == halo depth (test_kernels.cpp:171-189), ly=2 < halo (:191-209), lx=1, vl=32 warp-wide clusters."""
+    init = lbm.make_lattice("random", lx, ly, seed=606)
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.load(init)
+    s.bc("periodic")
+    s.propagate_only()
+    assert np.array_equal(s.dump(which=1), po.orc_propagate(init, po.BC_PERIODIC))
+
+
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 4)])
+def test_golden_reference_propagate_and_halo(gpu, lbm, layout, vl):
+    """Against fixtures written by the reference itself (tests/golden/make_golden.py)."""
+    for name in ("ref_random_16x32.npz", "ref_random_5x12.npz"):
+        g = golden(name)
+        lx, ly = int(g["lx"]), int(g["ly"])
+        vl_ = 1 if layout == "soa" else int(g["vl_csoa"])
+        s = sim_of(lbm, layout, lx, ly, vl_)
+        s.load(g["init"])
+        s.bc("periodic")
+        assert np.array_equal(s.read_padded(), g[f"padded_{layout}"]), "halo_exchange padded buffer differs"
+        s.propagate_only()
+        assert np.array_equal(s.dump(which=1), g[f"propagate_{layout}"])
+
+
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 2), ("csoa", 8)])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_bc_padded_bitwise_vs_oracle(gpu, lbm, po, layout, vl, bc):
+    """Every ghost slot (corners included) equals the oracle's halo fill, bit for bit."""
+    lx, ly = 7, 48
+    init = lbm.make_lattice("random", lx, ly, seed=123)
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.load(init)
+    s.bc(bc)
+    want = po.orc_halo_fill(po.orc_to_padded(init, vl), lx, ly, vl, po.BC_WALL if bc == "wall" else po.BC_PERIODIC)
+    assert np.array_equal(s.read_padded(), want)
+
+
+def test_bc_idempotent(gpu, lbm):
+    """test_kernels.cpp:211-218."""
+    s = sim_of(lbm, "csoa", 4, 16, 4)
+    s.load(lbm.make_lattice("random", 4, 16, seed=11))
+    s.bc("periodic")
+    first = s.read_padded()
+    s.bc("periodic")
+    assert np.array_equal(first, s.read_padded())
+
+
+def test_delta_impulse(gpu, lbm):
+    """test_kernels.cpp:114-133: 1.0 at (3,5) in c=(1,0) lands at (4,5)."""
+    m = lbm.model()
+    p10 = int(np.nonzero((m.velocities[:, 0] == 1) & (m.velocities[:, 1] == 0))[0][0])
+    for layout, vl in (("soa", 1), ("csoa", 2)):
+        init = np.zeros((37, 8, 8))
+        init[p10, 3, 5] = 1.0
+        s = sim_of(lbm, layout, 8, 8, vl)
+        s.load(init)
+        s.bc("periodic")
+        s.propagate_only()
+        out = s.dump(which=1)
+        want = np.zeros_like(out)
+        want[p10, 4, 5] = 1.0
+        assert np.array_equal(out, want)
+
+
+def test_wall_delta_impulse_reflects(gpu, lbm):
+    """Wall KAT: 1.0 in c=(1,-1) at (x0, 0) reappears only at (x0+1, 0) in ybar = (1,1)."""
+    m = lbm.model()
+    v = m.velocities
+    p7 = int(np.nonzero((v[:, 0] == 1) & (v[:, 1] == -1))[0][0])
+    p8 = int(np.nonzero((v[:, 0] == 1) & (v[:, 1] == 1))[0][0])
+    init = np.zeros((37, 8, 16))
+    init[p7, 3, 0] = 1.0
+    s = sim_of(lbm, "soa", 8, 16)
+    s.load(init)
+    s.bc("wall")
+    s.propagate_only()
+    out = s.dump(which=1)
+    want = np.zeros_like(out)
+    want[p8, 4, 0] = 1.0
+    assert np.array_equal(out, want)
+
+
+def test_lx_ly_periodicity_identity(gpu, lbm):
+    """test_kernels.cpp:262-276: lx*ly propagates return to the start."""
+    lx, ly = 4, 8
+    init = lbm.make_lattice("random", lx, ly, seed=77)
+    s = sim_of(lbm, "soa", lx, ly)
+    s.load(init)
+    for _ in range(lx * ly):
+        s.propagate()
+    assert np.array_equal(s.dump(), init)
+
+
+def test_wall_propagate_conserves_mass_bitwise_per_plane_pair(gpu, lbm):
+    """Propagate + wall bc is a permutation of (population, site) values: the multiset is preserved."""
+    lx, ly = 12, 40
+    init = lbm.make_lattice("random", lx, ly, seed=9)
+    s = sim_of(lbm, "csoa", lx, ly, 4)
+    s.load(init)
+    s.bc("wall")
+    s.propagate_only()
+    out = s.dump(which=1)
+    assert np.array_equal(np.sort(out.reshape(-1)), np.sort(init.reshape(-1)))
+
+
+def test_corrupted_offset_detected(gpu, lbm, po):
+    """test_validation.cpp:49-67: corrupt_population must produce a divergence."""
+    init = lbm.make_lattice("random", 16, 32, seed=5)
+    s = sim_of(lbm, "csoa", 16, 32, 2)
+    s.load(init)
+    s.bc("periodic")
+    s.propagate_only(corrupt_population=5)
+    got, want = s.dump(which=1), po.orc_propagate(init)
+    diff = np.argwhere(got != want)
+    assert len(diff) > 0 and set(diff[:, 0]) == {5}
+
+
+# --------------------------------------------------------------------------- collide
+
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 4)])
+@pytest.mark.parametrize("omega", [1.0, 1.2, 1.7])
+def test_collide_strict_bitwise_vs_oracle(gpu, lbm, po, layout, vl, omega):
+    """STRICT math == the no-contraction oracle bit for bit (same constants, same op order)."""
+    lx, ly = 16, 32
+    init = lbm.make_lattice("random", lx, ly, seed=4096)
+    want, bad = po.orc_collide(init, omega)
+    assert not bad
+    s = sim_of(lbm, layout, lx, ly, vl, math="strict")
+    s.load(init, which=1)
+    s.collide(omega)
+    assert np.array_equal(s.dump(), want)
+
+
+@pytest.mark.parametrize("omega", [1.0, 1.2, 1.7])
+def test_collide_fast_vs_reference_golden(gpu, lbm, omega):
+    """FAST math vs the reference's FMA build: <= 1e-12 relative, with the reference's own constants."""
+    gm = golden("ref_model.npz")
+    mdl = lbm.Model.from_arrays(gm["cx"], gm["cy"], gm["w"], gm["t0"], gm["eq"])
+    g = golden("ref_random_16x32.npz")
+    s = sim_of(lbm, "soa", 16, 32, mdl=mdl)
+    s.load(g["init"], which=1)
+    s.collide(float(g["omega_collide"]))
+    assert max_rel(s.dump(), g["collide"]) <= 1e-12
+
+
+def test_collide_nonphysical_raises(gpu, lbm):
+    """test_kernels.cpp:424-433: rho <= 0 -> NonPhysicalError."""
+    s = sim_of(lbm, "soa", 8, 16)
+    s.load(-np.ones((37, 8, 16)), which=1)
+    with pytest.raises(lbm.NonPhysicalError):
+        s.collide(1.0)
+    s.sync()  # flag cleared
+
+
+def test_collide_equilibrium_fixed_point(gpu, lbm):
+    """test_kernels.cpp:302-341: uniform equilibrium stays uniform and near-fixed (2e-14)."""
+    m = lbm.model()
+    s = sim_of(lbm, "csoa", 4, 16, 2)
+    s.load(lbm.make_lattice("equilibrium", 4, 16, params=[1.0, 0.0, 0.0, m.t0]), which=1)
+    s.collide(1.7)
+    out = s.dump()
+    for p in range(37):
+        assert np.all(out[p] == out[p, 0, 0])
+        assert abs(out[p, 0, 0] - m.weights[p]) <= 2e-14 * m.weights[p]
+
+
+# --------------------------------------------------------------------------- full steps
+
+@pytest.mark.parametrize("variant", ["fused", "unfused"])
+def test_step_vs_reference_golden(gpu, lbm, variant):
+    """10 periodic reference steps (CSoA vl=4 in the reference) within 1e-12 (1e-9 is the 100-step bar)."""
+    gm = golden("ref_model.npz")
+    mdl = lbm.Model.from_arrays(gm["cx"], gm["cy"], gm["w"], gm["t0"], gm["eq"])
+    for name in ("ref_random_16x32.npz", "ref_random_5x12.npz"):
+        g = golden(name)
+        lx, ly = int(g["lx"]), int(g["ly"])
+        s = sim_of(lbm, "soa", lx, ly, mdl=mdl, variant=variant)
+        s.load(g["init"])
+        s.step(float(g["omega_step"]), int(g["steps"]), bc="periodic")
+        assert s.time_step == int(g["steps"])
+        assert max_rel(s.dump(), g["step"]) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["fused", "unfused"])
+def test_step_strict_bitwise_vs_oracle(gpu, lbm, po, variant):
+    lx, ly = 32, 64
+    init = lbm.make_lattice("random", lx, ly, seed=88)
+    want, _ = po.orc_step(init, 0.9, 3, po.BC_WALL)
+    s = sim_of(lbm, "csoa", lx, ly, 4, math="strict", variant=variant, bc="wall")
+    s.load(init)
+    s.step(0.9, 3)
+    assert np.array_equal(s.dump(), want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("csoa", 32, "unfused")])
+def test_config0_100_steps(gpu, lbm, po, layout, vl, variant):
+    """BASELINE config 0: 256x1024 RT init, wall bc, omega 0.8, 100 steps: <= 1e-9 on f and derived fields."""
+    lx, ly, omega = 256, 1024, 0.8
+    init = lbm.make_lattice("rt", lx, ly, seed=12345)
+    s1 = sim_of(lbm, layout, lx, ly, vl, bc="wall", variant=variant)
+    s1.load(init)
+    s1.step(omega, 1)
+    one = s1.dump()
+    want1, _ = po.orc_step(init, omega, 1, po.BC_WALL)
+    assert max_rel(one, want1) <= 1e-12
+    s1.step(omega, 99)
+    got = s1.dump()
+    want, bad = po.orc_step(init, omega, 100, po.BC_WALL)
+    assert not bad
+    assert max_rel(got, want) <= 1e-9
+    rg, uxg, uyg, tg = macros_fields(po, got)
+    rw, uxw, uyw, tw = macros_fields(po, want)
+    assert max_rel(rg, rw) <= 1e-9
+    assert max_rel(tg, tw) <= 1e-9
+    speed = max(np.max(np.abs(uxw)), np.max(np.abs(uyw)))
+    assert np.max(np.abs(uxg - uxw)) <= 1e-9 * speed
+    assert np.max(np.abs(uyg - uyw)) <= 1e-9 * speed
+
+
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_layouts_and_variants_bitwise_identical(gpu, lbm, bc):
+    """acceptance C5 / test_kernels.cpp:383-397: dumps are layout-, vl- and variant-independent bit for bit."""
+    lx, ly = 24, 192
+    init = lbm.make_lattice("random", lx, ly, seed=13)
+    outs = []
+    for layout, vl in (("soa", 1), ("csoa", 2), ("csoa", 8), ("csoa", 32)):
+        for variant in ("fused", "unfused"):
+            s = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
+            s.load(init)
+            s.step(1.3, 4)
+            outs.append(s.dump())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 4, "fused")])
+def test_slab_group_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, vl, variant):
+    """GPU-count invariance (test_kernels.cpp:361-381 analogue): y-slabs == one domain, bit for bit."""
+    lx, ly = 16, 256
+    init = lbm.make_lattice("random", lx, ly, seed=21)
+    ref = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
+    ref.load(init)
+    ref.step(1.1, 5)
+    grp = lbm.SlabGroup(layout, lx, ly, vl, nslabs, bc=bc, variant=variant)
+    grp.load(init)
+    grp.step(1.1, 5)
+    assert np.array_equal(grp.dump(), ref.dump())
+
+
+def test_step_conserves_mass(gpu, lbm):
+    """test_kernels.cpp:343-359: global mass drift over 20 steps < 1e-11."""
+    s = sim_of(lbm, "csoa", 16, 32, 4)
+    s.load(lbm.make_lattice("random", 16, 32, seed=51))
+    m0 = s.moments()[0]
+    s.step(1.1, 20)
+    assert s.time_step == 20
+    assert abs(s.moments()[0] - m0) / m0 < 1e-11
+
+
+def test_step_no_nan_1000_steps(gpu, lbm):
+    """test_kernels.cpp:399-422 (stability, theta in [0.8, 1.2])."""
+    m = lbm.model()
+    for omega in (0.3, 1.0, 1.9):
+        s = sim_of(lbm, "csoa", 8, 16, 2)
+        s.load(lbm.make_lattice("random", 8, 16, seed=3))
+        s.step(omega, 1000)
+        assert np.all(np.isfinite(s.dump()))
+    del m
+
+
+# --------------------------------------------------------------------------- full BASELINE sizes
+
+@pytest.mark.slow
+def test_config1_full_size_propagate_bitwise(gpu, lbm):
+    """Config 1 at full size (1024x8192): device Philox == host Philox, propagate == np.roll oracle."""
+    lx, ly = 1024, 8192
+    s = sim_of(lbm, "soa", lx, ly)
+    s.init_philox(12345)
+    a = s.dump()
+    host = lbm.make_lattice("philox", lx, ly, seed=12345)
+    assert np.array_equal(a, host)
+    s.bc("periodic")
+    s.propagate_only()
+    got = s.dump(which=1)
+    v = lbm.model().velocities
+    for p in range(37):
+        assert np.array_equal(got[p], np.roll(a[p], shift=(int(v[p, 0]), int(v[p, 1])), axis=(0, 1))), p
+
+
+@pytest.mark.slow
+def test_config2_full_size_collide(gpu, lbm, po):
+    """Config 2 at full size (1024x8192): FAST collide within 1e-12 of the oracle."""
+    lx, ly = 1024, 8192
+    init = lbm.make_lattice("c2", lx, ly, seed=12345)
+    s = sim_of(lbm, "soa", lx, ly)
+    s.load(init, which=1)
+    s.collide(1.0)
+    want, bad = po.orc_collide(init, 1.0)
+    assert not bad
+    assert max_rel(s.dump(), want) <= 1e-12
+
+
+@pytest.mark.slow
+def test_config3_size_conservation(gpu, lbm):
+    """4096x16384 RT, wall, 20 fused steps: mass / energy conserved, momentum stays ~0 (size-independent)."""
+    s = sim_of(lbm, "soa", 4096, 16384, bc="wall")
+    s.load(lbm.make_lattice("rt", 4096, 16384, seed=12345))
+    m0 = s.moments()
+    s.step(0.8, 20)
+    m1 = s.moments()
+    assert abs(m1[0] - m0[0]) / m0[0] < 1e-11
+    assert abs(m1[3] - m0[3]) / m0[3] < 1e-11
+    assert abs(m1[1]) < 1e-6 * m0[0]
