@@ -176,6 +176,13 @@ int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslab
                        d2q37_lattice** out);
 /* step for every slab of a group created by d2q37_create_group. */
 int d2q37_group_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps, int variant, int bc);
+/* The halo message layout: entry i of send_lo / recv_hi is (distance d, population p)
+ * = (lo_d[i], lo_p[i]) with cy_p <= -d (the low neighbour's high ghost row d),
+ * entry i of send_hi / recv_lo is (hi_d[i], hi_p[i]) with cy_p >= d.  Returns the
+ * entry count (26 for D2Q37): 26 * lx doubles per face instead of 111 * lx. */
+int d2q37_halo_plan(int lo_d[32], int lo_p[32], int hi_d[32], int hi_p[32]);
+/* Peer ranks {lo, hi} of `rank` for a bc (-1 = wall / no neighbour). Host-only. */
+int d2q37_slab_neighbors(int rank, int nranks, int bc, int out[2]);
 /* rank, nranks, first global row, rows of this slab. */
 int d2q37_slab_info(const d2q37_lattice* h, int out[4]);
 /* Per-kernel device timing (CUDA events recorded around each launch on the

@@ -126,6 +126,8 @@ def _load():
         "d2q37_create_group": (i, [i, i, i, i, i, i, P(vp)]),
         "d2q37_group_step": (i, [P(vp), i, d, i, i, i]),
         "d2q37_slab_info": (i, [vp, P(C.c_int)]),
+        "d2q37_halo_plan": (i, [P(C.c_int)] * 4),
+        "d2q37_slab_neighbors": (i, [i, i, i, P(C.c_int)]),
         "d2q37_exposed_halo_ms": (d, [vp]),
         "d2q37_set_profiling": (i, [vp, i]),
         "d2q37_kernel_times": (i, [vp, _dp, P(C.c_long)]),
@@ -284,6 +286,24 @@ def make_lattice(kind: str, lx: int, ly: int, seed: int = 12345, params=None, md
     _check(_load().d2q37_make_lattice(INITS[kind], lx, ly, seed, None if par is None else _ptr(par),
                                       C.byref(m), _ptr(out), out.size, nthreads))
     return out
+
+
+def halo_plan():
+    """(lo_entries, hi_entries): lists of (d, p) of the slab halo messages (d2q37_halo_plan)."""
+    arrs = [(C.c_int * 32)() for _ in range(4)]
+    n = _load().d2q37_halo_plan(*arrs)
+    if n < 0:
+        raise RuntimeError("asymmetric halo plan")
+    lo = [(arrs[0][i], arrs[1][i]) for i in range(n)]
+    hi = [(arrs[2][i], arrs[3][i]) for i in range(n)]
+    return lo, hi
+
+
+def slab_neighbors(rank: int, nranks: int, bc: str = "periodic"):
+    """(lo_peer, hi_peer) of a y-slab rank; -1 where the face is a wall."""
+    out = (C.c_int * 2)()
+    _check(_load().d2q37_slab_neighbors(rank, nranks, BCS[bc], out))
+    return out[0], out[1]
 
 
 def nccl_unique_id() -> bytes:

@@ -926,6 +926,32 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[5], long counts[5]) {
     return D2Q37_OK;
 }
 
+int d2q37_halo_plan(int lo_d[32], int lo_p[32], int hi_d[32], int hi_p[32]) {
+    int n_lo = 0, n_hi = 0;
+    for (int d = 1; d <= kHalo; ++d)
+        for (int p = 0; p < kNpop; ++p) {
+            if (cy_of(p) <= -d) {
+                lo_d[n_lo] = d;
+                lo_p[n_lo++] = p;
+            }
+            if (cy_of(p) >= d) {
+                hi_d[n_hi] = d;
+                hi_p[n_hi++] = p;
+            }
+        }
+    return n_lo == n_hi ? n_lo : -1;
+}
+
+int d2q37_slab_neighbors(int rank, int nranks, int bc, int out[2]) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad rank");
+    d2q37_lattice tmp;
+    tmp.rank = rank;
+    tmp.nranks = nranks;
+    out[0] = lo_peer_of(&tmp, bc);
+    out[1] = hi_peer_of(&tmp, bc);
+    return D2Q37_OK;
+}
+
 int d2q37_slab_info(const d2q37_lattice* h, int out[4]) {
     RET(check_handle(h));
     out[0] = h->rank;
