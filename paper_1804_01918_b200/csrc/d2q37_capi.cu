@@ -170,6 +170,21 @@ int upload_model(d2q37_lattice* h, const d2q37_model* m) {
                 return fail(D2Q37_ERR_INVALID_ARGUMENT, "Hermite table entry (%d,%d) must be zero", i, k);
             h->mp.eq[i][k] = v;
         }
+    // The FAST kernels evaluate one Hermite row per (+-a, +-b) group and take
+    // the other rows' signs from the parity of each coefficient; require that
+    // symmetry (and equal weights within a group) to hold exactly.
+    for (int i = 0; i < kNpop; ++i)
+        for (int j = 0; j < kNpop; ++j) {
+            if (std::abs(cx_of(i)) != std::abs(cx_of(j)) || std::abs(cy_of(i)) != std::abs(cy_of(j))) continue;
+            if (m->w[i] != m->w[j]) return fail(D2Q37_ERR_INVALID_ARGUMENT, "weights %d and %d differ", i, j);
+            const bool fx = (cx_of(i) < 0) != (cx_of(j) < 0), fy = (cy_of(i) < 0) != (cy_of(j) < 0);
+            for (int k = 0; k < kNmom; ++k) {
+                const double s = ((fx && mom_has_cx(k)) != (fy && mom_has_cy(k))) ? -1.0 : 1.0;
+                if (m->eq[j * kNmom + k] != s * m->eq[i * kNmom + k])
+                    return fail(D2Q37_ERR_INVALID_ARGUMENT,
+                                "Hermite table rows %d and %d are not sign-symmetric at term %d", i, j, k);
+            }
+        }
     for (int i = 0; i < kNpop; ++i) h->mp.w[i] = m->w[i];
     h->mp.t0 = m->t0;
     return D2Q37_OK;

@@ -136,4 +136,148 @@ __device__ __forceinline__ bool collide_site(double (&f)[kNpop], double omega, c
     return bad;
 }
 
+// ---------------------------------------------------------------------------
+// FAST collide with the sign symmetry of the velocity set.
+//
+// Hermite coefficient k has a definite parity in cx and in cy (model.cpp:
+// 200-232), so for the four velocities (+-a, +-b) the table rows are the row
+// of (a, b) with signs flipped on the odd terms, exactly.  Per quadruple the
+// equilibrium sum splits into four partial sums over the parity classes
+//   EE = {2,4,9,11,13}  OE = {0,5,7}  EO = {1,6,8}  OO = {3,10,12}
+// and s(+-a, +-b) = EE +- OE +- EO + (sign) OO.  Axis velocities (a,0)/(0,b)
+// pair the same way.  221 FP64 ops instead of 436 for the equilibrium sums;
+// same result as the reference up to summation-order rounding (~1e-16).
+// d2q37_set_model verifies the table has the exact symmetry this relies on.
+
+D2Q37_HD constexpr int vel_index(int cx, int cy) {
+    for (int p = 0; p < kNpop; ++p)
+        if (cx_of(p) == cx && cy_of(p) == cy) return p;
+    return -1;
+}
+
+template <int K>
+__device__ __forceinline__ double hsum(double acc, const double* g, const double* mom) {
+    return fma(g[K], mom[K], acc);
+}
+
+template <int A, int B>
+__device__ __forceinline__ void eq_quad(double (&f)[kNpop], const double* mom, const ModelParams& mp, double rho,
+                                        double omega) {
+    constexpr int ipp = vel_index(A, B), imp = vel_index(-A, B), ipm = vel_index(A, -B), imm = vel_index(-A, -B);
+    const double* g = mp.eq[ipp];
+    double ee = fma(g[2], mom[2], 1.0);
+    ee = fma(g[4], mom[4], ee);
+    ee = fma(g[9], mom[9], ee);
+    ee = fma(g[11], mom[11], ee);
+    ee = fma(g[13], mom[13], ee);
+    double oe = g[0] * mom[0];
+    oe = fma(g[5], mom[5], oe);
+    oe = fma(g[7], mom[7], oe);
+    double eo = g[1] * mom[1];
+    eo = fma(g[6], mom[6], eo);
+    eo = fma(g[8], mom[8], eo);
+    double oo = g[3] * mom[3];
+    oo = fma(g[10], mom[10], oo);
+    oo = fma(g[12], mom[12], oo);
+    const double P = ee + oo, Q = ee - oo, S = oe + eo, T = oe - eo;
+    const double rw = rho * mp.w[ipp];
+    f[ipp] = fma(omega, fma(rw, P + S, -f[ipp]), f[ipp]);
+    f[imm] = fma(omega, fma(rw, P - S, -f[imm]), f[imm]);
+    f[ipm] = fma(omega, fma(rw, Q + T, -f[ipm]), f[ipm]);
+    f[imp] = fma(omega, fma(rw, Q - T, -f[imp]), f[imp]);
+}
+
+template <int A>
+__device__ __forceinline__ void eq_axis(double (&f)[kNpop], const double* mom, const ModelParams& mp, double rho,
+                                        double omega) {
+    // x-axis pair (+-A, 0) and y-axis pair (0, +-A) share a shell weight.
+    constexpr int xp = vel_index(A, 0), xm = vel_index(-A, 0), yp = vel_index(0, A), ym = vel_index(0, -A);
+    const double rw = rho * mp.w[xp];
+    {
+        const double* g = mp.eq[xp];
+        double ee = fma(g[2], mom[2], 1.0);
+        ee = fma(g[4], mom[4], ee);
+        ee = fma(g[9], mom[9], ee);
+        ee = fma(g[11], mom[11], ee);
+        ee = fma(g[13], mom[13], ee);
+        double o = g[0] * mom[0];
+        o = fma(g[5], mom[5], o);
+        o = fma(g[7], mom[7], o);
+        f[xp] = fma(omega, fma(rw, ee + o, -f[xp]), f[xp]);
+        f[xm] = fma(omega, fma(rw, ee - o, -f[xm]), f[xm]);
+    }
+    {
+        const double* g = mp.eq[yp];
+        double ee = fma(g[2], mom[2], 1.0);
+        ee = fma(g[4], mom[4], ee);
+        ee = fma(g[9], mom[9], ee);
+        ee = fma(g[11], mom[11], ee);
+        ee = fma(g[13], mom[13], ee);
+        double o = g[1] * mom[1];
+        o = fma(g[6], mom[6], o);
+        o = fma(g[8], mom[8], o);
+        f[yp] = fma(omega, fma(rw, ee + o, -f[yp]), f[yp]);
+        f[ym] = fma(omega, fma(rw, ee - o, -f[ym]), f[ym]);
+    }
+}
+
+__device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omega, const ModelParams& mp) {
+    double rho = 0.0;
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i) rho += f[i];
+    const bool bad = !(rho > 0.0);
+    double jx = 0.0, jy = 0.0, e2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cx_of(i) != 0) jx = fma((double)cx_of(i), f[i], jx);
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cy_of(i) != 0) jy = fma((double)cy_of(i), f[i], jy);
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cx_of(i) != 0 || cy_of(i) != 0)
+            e2 = fma((double)(cx_of(i) * cx_of(i) + cy_of(i) * cy_of(i)), f[i], e2);
+    const double inv_rho = 1.0 / rho;
+    const double ux = jx * inv_rho;
+    const double uy = jy * inv_rho;
+    const double temp = 0.5 * (e2 * inv_rho - (ux * ux + uy * uy));
+    const double dt = temp - mp.t0;
+    const double ux2 = ux * ux, uy2 = uy * uy, uxuy = ux * uy;
+    const double dt3 = 3.0 * dt, dt6 = 6.0 * dt, dt2 = dt * dt, dt2x3 = 3.0 * dt2;
+    double mom[kNmom];
+    mom[0] = ux;
+    mom[1] = uy;
+    mom[2] = ux2 + dt;
+    mom[3] = uxuy;
+    mom[4] = uy2 + dt;
+    mom[5] = ux * (ux2 + dt3);
+    mom[6] = uy * (ux2 + dt);
+    mom[7] = ux * (uy2 + dt);
+    mom[8] = uy * (uy2 + dt3);
+    mom[9] = ux2 * (ux2 + dt6) + dt2x3;
+    mom[10] = uxuy * (ux2 + dt3);
+    mom[11] = uxuy * uxuy + dt * (ux2 + uy2) + dt2;
+    mom[12] = uxuy * (uy2 + dt3);
+    mom[13] = uy2 * (uy2 + dt6) + dt2x3;
+    {  // rest velocity: even terms only
+        const double* g = mp.eq[0];
+        double ee = fma(g[2], mom[2], 1.0);
+        ee = fma(g[4], mom[4], ee);
+        ee = fma(g[9], mom[9], ee);
+        ee = fma(g[11], mom[11], ee);
+        ee = fma(g[13], mom[13], ee);
+        f[0] = fma(omega, fma(rho * mp.w[0], ee, -f[0]), f[0]);
+    }
+    eq_axis<1>(f, mom, mp, rho, omega);
+    eq_axis<2>(f, mom, mp, rho, omega);
+    eq_axis<3>(f, mom, mp, rho, omega);
+    eq_quad<1, 1>(f, mom, mp, rho, omega);
+    eq_quad<2, 1>(f, mom, mp, rho, omega);
+    eq_quad<1, 2>(f, mom, mp, rho, omega);
+    eq_quad<2, 2>(f, mom, mp, rho, omega);
+    eq_quad<3, 1>(f, mom, mp, rho, omega);
+    eq_quad<1, 3>(f, mom, mp, rho, omega);
+    return bad;
+}
+
 }  // namespace d2q37

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     double f[kNpop];
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + (SHIFT ? off.o[p] : p * g.plane));
-    const bool bad = collide_site<STRICT>(f, omega, mp);
+    const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);

@@ -1,0 +1,50 @@
+#!/usr/bin/env python3
+"""Small, ncu-friendly drivers of the three hot kernels (the commands the profiles/ captures come from).
+
+  --case step       4096x16384 SoA, RT init, wall bc, omega 0.8, fused steps   (bench workload)
+  --case unfused    same lattice, unfused steps (edge + propagate + collide)
+  --case csoa       same lattice, CSoA vl=32 fused steps
+  --case propagate  1024x8192 SoA Philox input, propagate prv->nxt            (BASELINE config 1)
+  --case collide    1024x8192 SoA c2 input, collide nxt->prv                  (BASELINE config 2)
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1804_01918_b200 as lbm  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="step", choices=["step", "unfused", "csoa", "propagate", "collide"])
+    ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--lx", type=int, default=4096)
+    ap.add_argument("--ly", type=int, default=16384)
+    a = ap.parse_args()
+    if a.case in ("step", "unfused", "csoa"):
+        layout, vl = ("csoa", 32) if a.case == "csoa" else ("soa", 1)
+        s = lbm.Simulation(layout, a.lx, a.ly, vl, bc="wall", variant="unfused" if a.case == "unfused" else "fused")
+        s.load(lbm.make_lattice("rt", a.lx, a.ly, 12345))
+        for _ in range(a.steps):
+            s.step(0.8, 1, sync=False)
+        s.sync()
+    elif a.case == "propagate":
+        s = lbm.Simulation("soa", 1024, 8192)
+        s.init_philox(12345)
+        s.bc("periodic")
+        for _ in range(a.steps):
+            s.propagate_only(sync=False)
+        s.sync()
+    else:
+        s = lbm.Simulation("soa", 1024, 8192)
+        s.load(lbm.make_lattice("c2", 1024, 8192, 12345), which=1)
+        for _ in range(a.steps):
+            s.collide(1.0, sync=False)
+        s.sync()
+    print(f"{a.case}: ok, {s.time_step} steps")
+
+
+if __name__ == "__main__":
+    main()
