@@ -4,7 +4,7 @@
 Workload (BASELINE configs 3/4): a 4096 x 16384 lattice per GPU (weak
 scaling; the global lattice is 4096 x 16384*N, split into y-slabs), config-0
 Rayleigh-Taylor-like init, periodic x, top/bottom specular walls, omega 0.8
-(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the SoA store.
+(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the CSoA (vl = 32) store.
 value = whole-job MLUPS over the K timed steps (max over ranks of the device
 time).  Inputs are larger than L2 (2 x 19.9 GB per GPU vs 126 MB), so no
 explicit flush is needed.
@@ -198,10 +198,10 @@ def host_mem_available() -> int:
 
 # --------------------------------------------------------------------------- sub-benchmarks (N=1)
 
-def bench_propagate(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
+def bench_propagate(lbm, warmup: int, reps: int, hbm_peak: float, layout: str = "soa", vl: int = 1) -> dict:
     """BASELINE config 1: 1024 x 8192 Philox input, repeated propagate prv -> nxt, 592 B/site."""
     lx, ly = 1024, 8192
-    sim = lbm.Simulation("soa", lx, ly, device=0)
+    sim = lbm.Simulation(layout, lx, ly, vl, device=0)
     sim.init_philox(SEED)
     sim.bc("periodic")
     for _ in range(warmup):
@@ -214,15 +214,16 @@ def bench_propagate(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
     t = kt[0] / kt[1] / 1e3
     gbs = lbm.propagate_gbps(lx, ly, 37, t, "nt")
     sim.close()
-    return {"config": "c1: 1024x8192 SoA, Philox U[0,1) input, periodic halo, propagate prv->nxt",
+    return {"config": f"c1: 1024x8192 {layout}{vl if vl > 1 else ''}, Philox U[0,1) input, periodic halo, "
+                      "propagate prv->nxt",
             "reps": reps, "ms_per_call": t * 1e3, "wall_ms_per_call": ms / reps, "GB_per_s": gbs,
             "frac_of_hbm": gbs / hbm_peak, "mlups": lbm.mlups(lx, ly, t)}
 
 
-def bench_collide(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
+def bench_collide(lbm, warmup: int, reps: int, hbm_peak: float, layout: str = "soa", vl: int = 1) -> dict:
     """BASELINE config 2: 1024 x 8192 perturbed equilibrium, collide nxt -> prv, 1522 FLOP/site."""
     lx, ly = 1024, 8192
-    sim = lbm.Simulation("soa", lx, ly, device=0)
+    sim = lbm.Simulation(layout, lx, ly, vl, device=0)
     sim.load(lbm.make_lattice("c2", lx, ly, SEED), which=1)
     for _ in range(warmup):
         sim.collide(1.0, sync=False)
@@ -235,11 +236,27 @@ def bench_collide(lbm, warmup: int, reps: int, hbm_peak: float) -> dict:
     gf = lbm.collide_gflops(lx, ly, FLOPS_PER_SITE, t)
     gbs = lx * ly * BYTES_PER_SITE / t / 1e9
     sim.close()
-    return {"config": "c2: 1024x8192 SoA, c2 perturbed equilibrium, collide nxt->prv, omega 1.0",
+    return {"config": f"c2: 1024x8192 {layout}{vl if vl > 1 else ''}, c2 perturbed equilibrium, collide nxt->prv, "
+                      "omega 1.0",
             "reps": reps, "ms_per_call": t * 1e3, "GFLOP_per_s": gf, "mlups": lbm.mlups(lx, ly, t),
             "frac_of_fp64_nominal": gf / (FP64_NOMINAL_TFLOPS * 1e3), "GB_per_s": gbs,
             "frac_of_hbm": gbs / hbm_peak,
             "frac_of_attainable": gf / min(FP64_NOMINAL_TFLOPS * 1e3, FLOPS_PER_SITE / BYTES_PER_SITE * hbm_peak)}
+
+
+def bench_config0(lbm, warmup: int) -> dict:
+    """BASELINE config 0: 256 x 1024 RT init, wall bc, 100 full steps (one timed call of step(0.8, 100))."""
+    lx, ly, n = 256, 1024, 100
+    canon = lbm.make_lattice("rt", lx, ly, SEED)
+    out = {}
+    for variant in ("fused", "unfused"):
+        sim = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant=variant)
+        sim.load(canon)
+        sim.step(OMEGA, warmup)
+        best = min(time_steps(sim, 1, lambda: sim.step(OMEGA, n, sync=False)) for _ in range(5))
+        out[variant] = {"ms_per_100_steps": best, "mlups": lx * ly * n / (best / 1e3) / 1e6}
+        sim.close()
+    return {"config": "c0: 256x1024 SoA, RT init, wall bc, omega 0.8, 100 steps per call (best of 5)", **out}
 
 
 def bench_variant(lbm, canon, layout, vl, variant, warmup, steps) -> dict:
@@ -385,9 +402,12 @@ def run_b200(args, dist: Dist):
         sim.close()
         del sim
         line["kernels"] = {"propagate_c1": bench_propagate(lbm, 5, 200, hbm_peak),
-                           "collide_c2": bench_collide(lbm, 5, 200, hbm_peak)}
+                           "propagate_c1_csoa32": bench_propagate(lbm, 5, 200, hbm_peak, "csoa", 32),
+                           "collide_c2": bench_collide(lbm, 5, 200, hbm_peak),
+                           "collide_c2_csoa32": bench_collide(lbm, 5, 200, hbm_peak, "csoa", 32),
+                           "step_c0": bench_config0(lbm, 5)}
         variants = {}
-        for lay, vl, var in (("soa", 1, "unfused"), ("csoa", 32, "fused"), ("csoa", 32, "unfused")):
+        for lay, vl, var in (("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"), ("csoa", 32, "unfused")):
             if (lay, var) == (args.layout, args.variant):
                 continue
             variants[f"{lay}{vl if lay == 'csoa' else ''}-{var}"] = bench_variant(lbm, canon, lay, vl, var, 3, 20)
@@ -453,7 +473,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--layout", choices=["soa", "csoa"], default="soa")
+    ap.add_argument("--layout", choices=["soa", "csoa"], default="csoa")
     ap.add_argument("--vl", type=int, default=32)
     ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU")

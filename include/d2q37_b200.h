@@ -166,7 +166,10 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed);
 int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]);
 /* Rank `rank` of `nranks` owns global rows [rank*ly/nranks, (rank+1)*ly/nranks)
  * of an lx x ly lattice; load/dump take that slab's canonical array (lx x ly/nranks).
- * Halo rows travel by ncclSend/ncclRecv between y neighbours each step. */
+ * Halo rows travel by ncclSend/ncclRecv between y neighbours each step.
+ * nranks = 1 with a non-NULL id builds a one-rank NCCL ring: the periodic y
+ * wrap goes through NCCL send/recv to self (the whole multi-GPU schedule on
+ * one GPU); with id = NULL it is a plain single-domain lattice. */
 int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
                       const unsigned char id[D2Q37_NCCL_ID_BYTES], d2q37_lattice** out);
 /* In-process emulation: nslabs slabs of one lx x ly lattice on one device whose

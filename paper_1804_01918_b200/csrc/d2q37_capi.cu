@@ -139,6 +139,8 @@ int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
     g->strip = ly / vl;
     g->sy = g->strip + 2 * kHalo;
     g->px = lx + 2 * kHalo;
+    g->lvl = 0;
+    while ((1 << g->lvl) < vl) ++g->lvl;
     // 256-byte alignment of every column's first physical element.
     const int per = 32 / std::gcd(vl, 32);
     g->pitch = (g->sy + per - 1) / per * per;
@@ -338,13 +340,18 @@ Segments all_sites(const DevGeo& g) {
     return s;
 }
 
+// A single rank with an NCCL communicator (d2q37_create_slab with nranks = 1
+// and an id) routes its periodic y wrap through NCCL to itself: the full
+// multi-GPU schedule on one GPU.
+bool local_only(const d2q37_lattice* h) { return h->nranks == 1 && h->transport != kTransportNccl; }
+
 int face_lo_of(const d2q37_lattice* h, int bc) {
-    if (h->nranks == 1) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
-    if (h->rank == 0 && bc == D2Q37_BC_WALL) return kFaceWall;
+    if (local_only(h)) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
+    if (h->rank == 0 && bc == D2Q37_BC_WALL) return kFaceWall;  // global low wall
     return kFaceRemote;
 }
 int face_hi_of(const d2q37_lattice* h, int bc) {
-    if (h->nranks == 1) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
+    if (local_only(h)) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
     if (h->rank == h->nranks - 1 && bc == D2Q37_BC_WALL) return kFaceWall;
     return kFaceRemote;
 }
@@ -364,8 +371,12 @@ int validate_bc(const d2q37_lattice* h, int bc) {
     return D2Q37_OK;
 }
 
-int edge(d2q37_lattice* h, int bc, int filter) {
+// lean = true inside steps: the stream kernels read inner lane rows directly,
+// so only the outer faces' ghost rows are needed; the bc verb fills all ghosts
+// (the reference's halo_exchange semantics).
+int edge(d2q37_lattice* h, int bc, int filter, bool lean = true) {
     EdgeParams ep = h->edge_base;
+    ep.lean = lean ? 1 : 0;
     ep.face_lo = face_lo_of(h, bc);
     ep.face_hi = face_hi_of(h, bc);
     ep.filter = filter;
@@ -713,18 +724,18 @@ int d2q37_bc(d2q37_lattice* h, int bc) {
     RET(check_handle(h));
     RET(validate_bc(h, bc));
     DeviceGuard dg(h->device);
-    if (h->nranks > 1 && remote_faces(h, bc)) {
+    if (!local_only(h) && remote_faces(h, bc)) {
         if (h->transport == kTransportGroup) {
             // every slab of the group packs, then halos move, then edges run
             for (d2q37_lattice* s : h->group) RET(exchange_begin(s, bc));
             RET(group_exchange(h->group, bc));
-            for (d2q37_lattice* s : h->group) RET(edge(s, bc, kEdgeAll));
+            for (d2q37_lattice* s : h->group) RET(edge(s, bc, kEdgeAll, false));
             return D2Q37_OK;
         }
         RET(exchange_begin(h, bc));
         RET(exchange_wait(h));
     }
-    return edge(h, bc, kEdgeAll);
+    return edge(h, bc, kEdgeAll, false);
 }
 
 int d2q37_propagate(d2q37_lattice* h) { return d2q37_propagate_corrupt(h, -1); }
@@ -757,7 +768,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         return d2q37_group_step(slabs, int(h->group.size()), omega, nsteps, variant, bc);
     }
     for (int s = 0; s < nsteps; ++s) {
-        if (h->nranks > 1 && remote_faces(h, bc)) {
+        if (!local_only(h) && remote_faces(h, bc)) {
             RET(exchange_begin(h, bc));
             RET(slab_phase1(h, omega, variant, bc));
             RET(slab_phase2(h, omega, variant, bc));
@@ -843,7 +854,7 @@ int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, 
                       const unsigned char id[D2Q37_NCCL_ID_BYTES], d2q37_lattice** out) {
     RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks));
     d2q37_lattice* h = *out;
-    if (nranks == 1) return D2Q37_OK;
+    if (nranks == 1 && !id) return D2Q37_OK;
     auto bail = [&](int rc) {
         d2q37_destroy(h);
         *out = nullptr;

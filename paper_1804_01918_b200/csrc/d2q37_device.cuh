@@ -27,7 +27,7 @@ struct DevGeo {
     int sy;         // strip + 6 (reference padded rows per lane)
     int pitch;      // device rows per padded column (>= sy)
     int px;         // lx + 6
-    int pad_;
+    int lvl;        // log2(vl)
     long long lead;   // element offset of population plane 0
     long long plane;  // elements per population plane
 };
@@ -153,11 +153,6 @@ D2Q37_HD constexpr int vel_index(int cx, int cy) {
     for (int p = 0; p < kNpop; ++p)
         if (cx_of(p) == cx && cy_of(p) == cy) return p;
     return -1;
-}
-
-template <int K>
-__device__ __forceinline__ double hsum(double acc, const double* g, const double* mom) {
-    return fma(g[K], mom[K], acc);
 }
 
 template <int A, int B>

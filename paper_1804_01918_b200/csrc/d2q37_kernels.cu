@@ -31,6 +31,24 @@ __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
 // ---------------------------------------------------------------------------
 
+// Pull offset of population P for the site in lane k, lane row `row`.  With
+// LANES (CSoA, vl > 1) a lane reads the rows beyond its strip ends straight
+// from the neighbouring lane (same cluster row range, lane k-1 / k+1) instead
+// of the lane-halo copies, so a step only needs lane 0's low and lane vl-1's
+// high ghost rows (k_edge "lean").  For vl >= 32 the test is warp-uniform.
+template <bool LANES>
+__device__ __forceinline__ long long pull_offset(const Offsets& off, const DevGeo& g, int p, int row, int k) {
+    long long o = off.o[p];
+    if (LANES) {
+        const int cy = cy_of(p);
+        const long long wrap = (long long)g.strip * g.vl - 1;
+        if (cy > 0 && row < cy && k > 0) o += wrap;
+        if (cy < 0 && row >= g.strip + cy && k < g.vl - 1) o -= wrap;
+    }
+    return o;
+}
+
+template <bool LANES>
 __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __restrict__ src,
                                                               double* __restrict__ dst, DevGeo g, Offsets off,
                                                               Segments seg) {
@@ -38,14 +56,15 @@ __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __re
     const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= seg.q0[z] + seg.nq) return;
     const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    const int row = q >> g.lvl, k = q & (g.vl - 1);
     double f[kNpop];
 #pragma unroll
-    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + off.o[p]);
+    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + pull_offset<LANES>(off, g, p, row, k));
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);
 }
 
-template <bool STRICT, bool SHIFT>
+template <bool STRICT, bool SHIFT, bool LANES>
 __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, ModelParams mp,
               double omega, Segments seg, int* __restrict__ flag) {
@@ -53,9 +72,11 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= seg.q0[z] + seg.nq) return;
     const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    const int row = q >> g.lvl, k = q & (g.vl - 1);
     double f[kNpop];
 #pragma unroll
-    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + (SHIFT ? off.o[p] : p * g.plane));
+    for (int p = 0; p < kNpop; ++p)
+        f[p] = ld_stream(src + e + (SHIFT ? pull_offset<LANES>(off, g, p, row, k) : p * g.plane));
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
 #pragma unroll
@@ -76,12 +97,14 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 
 __global__ void __launch_bounds__(256) k_edge(double* __restrict__ buf, DevGeo g, EdgeParams ep) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nrows = (long long)kNpop * g.px * 6 * g.vl;
+    // lean: only the outer faces' ghost rows (lane 0 low, lane vl-1 high)
+    const int nk = ep.lean ? 1 : g.vl;
+    const long long nrows = (long long)kNpop * g.px * 6 * nk;
     if (t < nrows) {
-        const int k = int(t % g.vl);
-        const int r = int((t / g.vl) % 6);
-        const int X = int((t / (6LL * g.vl)) % g.px);
-        const int p = int(t / (6LL * g.vl * g.px));
+        const int r = int((t / nk) % 6);
+        const int k = ep.lean ? (r < 3 ? 0 : g.vl - 1) : int(t % nk);
+        const int X = int((t / (6LL * nk)) % g.px);
+        const int p = int(t / (6LL * nk * g.px));
         const int xs = wrapi(X - kHalo, g.lx);
         const int Xs = xs + kHalo;
         int j, y, q = p;
@@ -251,7 +274,10 @@ cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, co
                              const Segments& seg, int nseg, cudaStream_t s) {
     if (seg.nq <= 0) return cudaSuccess;
     (void)cudaGetLastError();
-    k_propagate<<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
+    if (g.vl > 1)
+        k_propagate<true><<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
+    else
+        k_propagate<false><<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
     return cudaGetLastError();
 }
 
@@ -260,22 +286,32 @@ cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, cons
                            int nseg, int* flag, cudaStream_t s) {
     if (seg.nq <= 0) return cudaSuccess;
     const dim3 grid = stream_grid(g, seg, nseg);
-    if (strict) {
-        if (shift)
-            k_collide<true, true><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+    const bool lanes = g.vl > 1;
+#define D2Q37_COLLIDE(S, SH, L) \
+    k_collide<S, SH, L><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag)
+    (void)cudaGetLastError();
+    if (!shift) {
+        if (strict)
+            D2Q37_COLLIDE(true, false, false);
         else
-            k_collide<true, false><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+            D2Q37_COLLIDE(false, false, false);
+    } else if (strict) {
+        if (lanes)
+            D2Q37_COLLIDE(true, true, true);
+        else
+            D2Q37_COLLIDE(true, true, false);
     } else {
-        if (shift)
-            k_collide<false, true><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+        if (lanes)
+            D2Q37_COLLIDE(false, true, true);
         else
-            k_collide<false, false><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag);
+            D2Q37_COLLIDE(false, true, false);
     }
+#undef D2Q37_COLLIDE
     return cudaGetLastError();
 }
 
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s) {
-    long long total = (long long)kNpop * g.px * 6 * g.vl;
+    long long total = (long long)kNpop * g.px * 6 * (ep.lean ? 1 : g.vl);
     if (ep.filter & kEdgeLocal) total += (long long)kNpop * 6 * g.ly;
     const long long blocks = (total + 255) / 256;
     (void)cudaGetLastError();

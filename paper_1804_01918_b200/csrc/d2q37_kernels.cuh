@@ -27,7 +27,7 @@ struct EdgeParams {
     const double* recv_hi;  // [slot][x]: neighbour's rows d-1 for (d, p) with cy_p <= -d
     int face_lo, face_hi;
     int filter;
-    int pad_;
+    int lean;  // fill only lane 0's low / lane vl-1's high ghost rows (+ ghost columns)
     signed char lo_slot[kHalo][kNpop];  // (d-1, p) -> slot or -1
     signed char hi_slot[kHalo][kNpop];
     signed char ybar[kNpop];            // y-mirror (cx, -cy)

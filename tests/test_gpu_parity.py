@@ -356,3 +356,29 @@ def test_config3_size_conservation(gpu, lbm):
     assert abs(m1[0] - m0[0]) / m0[0] < 1e-11
     assert abs(m1[3] - m0[3]) / m0[3] < 1e-11
     assert abs(m1[1]) < 1e-6 * m0[0]
+
+
+@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("csoa", 8, "fused"), ("soa", 1, "unfused")])
+def test_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, variant):
+    """The real NCCL transport on one GPU: a 1-rank ring whose periodic y wrap goes
+    pack -> ncclSend/ncclRecv (self) -> remote edge, with the interior/boundary overlap."""
+    import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library binds to)
+
+    lx, ly = 16, 256
+    init = lbm.make_lattice("random", lx, ly, seed=33)
+    ref = sim_of(lbm, layout, lx, ly, vl, variant=variant)
+    ref.load(init)
+    ref.step(1.2, 6)
+    s = lbm.Simulation.slab(layout, lx, ly, vl, rank=0, nranks=1, nccl_id=lbm.nccl_unique_id(),
+                            bc="periodic", variant=variant)
+    s.load(init)
+    s.step(1.2, 6)
+    assert np.array_equal(s.dump(), ref.dump())
+    assert s.exposed_halo_ms() >= 0.0
+    # the bc verb through NCCL fills only the 26 planned ghost pop-rows, which is
+    # everything propagate reads: halo + propagate must still equal the single domain
+    s.bc("periodic")
+    s.propagate_only()
+    ref.bc("periodic")
+    ref.propagate_only()
+    assert np.array_equal(s.dump(which=1), ref.dump(which=1))
