@@ -259,9 +259,33 @@ def bench_config0(lbm, warmup: int) -> dict:
     return {"config": "c0: 256x1024 SoA, RT init, wall bc, omega 0.8, 100 steps per call (best of 5)", **out}
 
 
-def bench_variant(lbm, canon, layout, vl, variant, warmup, steps) -> dict:
-    sim = lbm.Simulation(layout, LX, canon.shape[2], vl, device=0, bc="wall", variant=variant)
-    sim.load(canon)
+def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
+    """The multi-GPU schedule on one GPU: a 1-rank NCCL ring (pack -> ncclSend/Recv to self ->
+    remote edge, interior/boundary split) vs the plain single-domain step, same lattice.
+    ly = 4096 is the per-GPU slab of the 8-GPU strong-scaling config (4096 x 32768 / 8)."""
+    import torch  # noqa: F401  (NCCL comes from torch's libnccl.so.2)
+    out = {}
+    for name in ("single_domain", "nccl_self_ring"):
+        if name == "single_domain":
+            sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="periodic")
+        else:
+            sim = lbm.Simulation.slab(layout, LX, ly, vl, device=0, rank=0, nranks=1,
+                                      nccl_id=lbm.nccl_unique_id(), bc="periodic")
+        sim.init_rt_device(SEED)
+        sim.step(OMEGA, warmup)
+        ms = time_steps(sim, steps, lambda: sim.step(OMEGA, 1, sync=False))
+        out[name] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6}
+        if name != "single_domain":
+            out[name]["exposed_halo_ms"] = sim.exposed_halo_ms()
+        sim.close()
+    out["schedule_overhead"] = out["nccl_self_ring"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
+    out["config"] = f"{LX}x{ly} {layout}{vl}, periodic y through NCCL to self vs local wrap, {steps} steps"
+    return out
+
+
+def bench_variant(lbm, ly, layout, vl, variant, warmup, steps) -> dict:
+    sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="wall", variant=variant)
+    sim.init_rt_device(SEED)
     sim.step(OMEGA, warmup)
     sim.set_profiling(True)
     sim.kernel_times()
@@ -269,7 +293,7 @@ def bench_variant(lbm, canon, layout, vl, variant, warmup, steps) -> dict:
     kt = sim.kernel_times()
     sim.set_profiling(False)
     sim.close()
-    sites = LX * canon.shape[2]
+    sites = LX * ly
     out = {"mlups": sites * steps / (ms / 1e3) / 1e6, "ms_per_step": ms / steps}
     for k, (tot, n) in kt.items():
         if n:
@@ -338,17 +362,14 @@ def run_b200(args, dist: Dist):
     sites_local = LX * ly_local
     rank = dist.rank
 
-    # ---- lattice + init (host canonical of this rank's slab: also the e2e input)
-    canon = np.empty((37, LX, ly_local), dtype=np.float64)
-    params = None if n == 1 else [float(ly_global), float(rank * ly_local)]
-    lbm.make_lattice("rt", LX, ly_local, SEED, params=params, out=canon)
+    # ---- lattice + init: each rank generates its slab of the RT state on the device
     if n == 1:
         sim = lbm.Simulation(args.layout, LX, ly_local, args.vl, device=dev, bc="wall", variant=args.variant)
     else:
         uid = dist.bcast_bytes(lbm.nccl_unique_id() if rank == 0 else None)
         sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
                                   nccl_id=uid, bc="wall", variant=args.variant)
-    sim.load(canon)
+    sim.init_rt_device(SEED)
 
     clocks = ClockSampler(dev)
     clocks.start()
@@ -375,7 +396,7 @@ def run_b200(args, dist: Dist):
     step_ms = ms_max / args.steps
     roofline = {"bound": "hbm", "kernel": "k_collide<FAST,SHIFT> (fused pull-gather + collide)",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak if achieved else None, "traffic": load_ncu_traffic(),
+                "frac": achieved / hbm_peak if achieved else None, "traffic": load_ncu_traffic(args.layout, ly_local),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms,
@@ -384,7 +405,7 @@ def run_b200(args, dist: Dist):
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(lbm, sim, canon, args, dist)
+        e2e = run_e2e(lbm, sim, args, dist)
 
     line = {"metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -410,8 +431,13 @@ def run_b200(args, dist: Dist):
         for lay, vl, var in (("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"), ("csoa", 32, "unfused")):
             if (lay, var) == (args.layout, args.variant):
                 continue
-            variants[f"{lay}{vl if lay == 'csoa' else ''}-{var}"] = bench_variant(lbm, canon, lay, vl, var, 3, 20)
+            variants[f"{lay}{vl if lay == 'csoa' else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20)
         line["variants_c3"] = variants
+        try:
+            line["slab_schedule"] = {"strong_8gpu_slab": bench_slab_schedule(lbm, "csoa", 32, 4096, 3, 50),
+                                     "weak_slab": bench_slab_schedule(lbm, "csoa", 32, LY_PER_GPU, 3, 20)}
+        except Exception as e:  # NCCL unavailable must not sink the line
+            line["slab_schedule"] = {"error": str(e)}
     if n == 1 and not args.no_cpu:
         try:
             v, med, workers = reference_step_rate()
@@ -426,45 +452,52 @@ def run_b200(args, dist: Dist):
         print(json.dumps(line), flush=True)
 
 
-def run_e2e(lbm, sim, canon, args, dist: Dist):
-    """load(host) -> step x n -> dump(host) through the public API, host buffers pinned."""
+def run_e2e(lbm, sim, args, dist: Dist):
+    """load(host) -> step x n -> dump(host) through the public API, one pinned host canonical per rank.
+
+    The rank's current state is dumped into the host buffer first; every call
+    then loads it, advances n steps and dumps the result back into it.
+    """
     nsteps = args.e2e_steps
-    need = canon.nbytes
-    if host_mem_available() < need * 1.5 and host_mem_available() > 0:
-        return {"value": None, "unit": "MLUPS", "skipped": "not enough host memory for a second buffer"}
-    out = np.empty_like(canon)
-    pinned = pin(canon) and pin(out)
-    sim.load(canon)
-    sim.step(OMEGA, nsteps)
-    sim.dump(out=out)
+    need = 37 * sim.lx * sim.ly * 8
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", dist.world))
+    avail = host_mem_available()
+    if avail and avail < need * local_ranks * 1.25:
+        return {"value": None, "unit": "MLUPS",
+                "skipped": f"{local_ranks} x {need / 1e9:.1f} GB host buffers exceed available host memory"}
+    canon = np.empty((37, sim.lx, sim.ly), dtype=np.float64)
+    pinned = pin(canon)
+    sim.dump(out=canon)
     times = []
-    for _ in range(args.e2e_iters):
+    for _ in range(1 + args.e2e_iters):  # first call warms the pinned path
         dist.barrier()
         t0 = time.perf_counter()
         sim.load(canon)
         sim.step(OMEGA, nsteps)
-        sim.dump(out=out)
+        sim.dump(out=canon)
         times.append(time.perf_counter() - t0)
     if pinned:
         unpin(canon)
-        unpin(out)
-    t = dist.max(min(times))
-    sites = LX * canon.shape[2] * dist.world
-    return {"value": sites * nsteps / t / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": canon.nbytes / nsteps,
-            "d2h_bytes_per_step": out.nbytes / nsteps, "steps_per_call": nsteps,
-            "h2d_bytes_per_call": canon.nbytes, "d2h_bytes_per_call": out.nbytes, "pinned": pinned,
+    t = dist.max(min(times[1:]))
+    sites = LX * sim.ly * dist.world
+    return {"value": sites * nsteps / t / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": need / nsteps,
+            "d2h_bytes_per_step": need / nsteps, "steps_per_call": nsteps,
+            "h2d_bytes_per_call": need, "d2h_bytes_per_call": need, "pinned": pinned,
             "seconds_per_call": t,
             "call": "Simulation.load(host canonical) + step(0.8, n, fused, wall) + dump(host canonical)"}
 
 
-def load_ncu_traffic():
-    """dram bytes/launch of the fused kernel from the committed ncu summary (profiles/), else None."""
+def load_ncu_traffic(layout: str, ly: int):
+    """DRAM bytes/launch of the fused kernel from the committed ncu capture (profiles/), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
+    key = "prof_fused_csoa" if layout == "csoa" else "prof_fused"
     try:
         with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            rec = json.load(f)[key]
     except Exception:
         return None
+    # the capture is of the 4096 x 16384 launch; scale per site for other slab heights
+    return rec["dram_bytes_per_launch"] * (LX * ly) / (4096 * 16384)
 
 
 def main():

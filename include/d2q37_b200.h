@@ -160,6 +160,12 @@ int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* pa
 /* Device-side D2Q37_INIT_PHILOX straight into one buffer (bit-identical to the host one). */
 int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed);
 
+/* Device-side config-0/3/4 RT init of the state buffer: the D2Q37_INIT_RT
+ * formulas with the per-site noise drawn from Philox (key = seed, counter = the
+ * global site index x*ly + y) instead of the sequential mt19937_64 stream, so
+ * every y-slab initialises itself; equilibrium in the reference's op order. */
+int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed);
+
 /* ---- Multi-GPU: 1-D y-slab decomposition (BASELINE config 4) ------------- */
 
 /* NCCL unique id for d2q37_create_slab (rank 0 creates, the caller broadcasts). */

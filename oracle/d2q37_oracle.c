@@ -648,6 +648,32 @@ void orc_rt_lattice(const orc_model* m, int lx, int ly, uint64_t seed, double* o
     }
 }
 
+static double philox_u01(uint64_t seed, uint64_t counter) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const uint32_t ctr[4] = {(uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u};
+    uint32_t r[4];
+    orc_philox4x32_10(ctr, key, r);
+    return (double)((((uint64_t)r[1] << 32) | r[0]) >> 11) * 0x1.0p-53;
+}
+
+void orc_rt_philox_lattice(const orc_model* m, int lx, int ly, int ly_global, int y0, uint64_t seed, double* out) {
+    double feq[ORC_NPOP], mac[4];
+    for (int x = 0; x < lx; ++x) {
+        const double yint = 0.5 * ly_global + 0.01 * ly_global * sin(2.0 * ORC_PI * x / lx);
+        for (int y = 0; y < ly; ++y) {
+            const int yg = y0 + y;
+            const double noise = -1e-3 + 2e-3 * philox_u01(seed, (uint64_t)x * (uint64_t)ly_global + (uint64_t)yg);
+            const double temp = ((double)yg < yint ? 1.5 : 0.5) + noise;
+            mac[0] = 1.0 / temp;
+            mac[1] = 0.0;
+            mac[2] = 0.0;
+            mac[3] = temp;
+            orc_equilibrium(m, mac, feq);
+            for (int p = 0; p < ORC_NPOP; ++p) out[cidx(lx, ly, p, x, y)] = feq[p];
+        }
+    }
+}
+
 void orc_c2_lattice(const orc_model* m, int lx, int ly, uint64_t seed, double* out) {
     orc_mt64 g;
     orc_mt64_seed(&g, seed);

@@ -99,6 +99,9 @@ void orc_equilibrium_lattice(const orc_model* m, int lx, int ly, const double ma
 void orc_shear_lattice(const orc_model* m, int lx, int ly, double amp, double temp, double* out);
 /* BASELINE config 0/3/4: Rayleigh-Taylor-like init (builder recipe). */
 void orc_rt_lattice(const orc_model* m, int lx, int ly, uint64_t seed, double* out);
+/* Same RT formulas with Philox noise keyed by the global site index x*ly_global + y_global,
+ * for rows [y0, y0+ly) of an lx x ly_global lattice (the product's device-side init). */
+void orc_rt_philox_lattice(const orc_model* m, int lx, int ly, int ly_global, int y0, uint64_t seed, double* out);
 /* BASELINE config 2 recipe. */
 void orc_c2_lattice(const orc_model* m, int lx, int ly, uint64_t seed, double* out);
 /* BASELINE config 1: i.i.d. U[0,1) from Philox keyed by seed, counter = site-major index. */

@@ -79,6 +79,7 @@ def orc() -> C.CDLL:
             "orc_shear_lattice": (None, [M, C.c_int, C.c_int, C.c_double, C.c_double, _dp]),
             "orc_rt_lattice": (None, [M, C.c_int, C.c_int, C.c_uint64, _dp]),
             "orc_c2_lattice": (None, [M, C.c_int, C.c_int, C.c_uint64, _dp]),
+            "orc_rt_philox_lattice": (None, [M, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]),
             "orc_philox_lattice": (None, [C.c_int, C.c_int, C.c_uint64, _dp]),
         }
         for name, (res, args) in sig.items():
@@ -305,6 +306,8 @@ def orc_lattice(kind, lx, ly, seed=12345, **kw):
         orc().orc_rt_lattice(M, lx, ly, seed, o)
     elif kind == "c2":
         orc().orc_c2_lattice(M, lx, ly, seed, o)
+    elif kind == "rt_philox":
+        orc().orc_rt_philox_lattice(M, lx, ly, kw.get("ly_global", ly), kw.get("y0", 0), seed, o)
     elif kind == "philox":
         orc().orc_philox_lattice(lx, ly, seed, o)
     else:

@@ -121,6 +121,7 @@ def _load():
         "d2q37_moments": (i, [vp, _dp]),
         "d2q37_make_lattice": (i, [i, i, i, C.c_uint64, vp, P(_Model), vp, sz, i]),
         "d2q37_fill_philox": (i, [vp, i, C.c_uint64]),
+        "d2q37_init_rt_device": (i, [vp, C.c_uint64]),
         "d2q37_nccl_unique_id": (i, [C.c_char_p]),
         "d2q37_create_slab": (i, [i, i, i, i, i, i, i, C.c_char_p, P(vp)]),
         "d2q37_create_group": (i, [i, i, i, i, i, i, P(vp)]),
@@ -451,6 +452,10 @@ class Simulation:
 
     def init_philox(self, seed: int, which: int = 0):
         _check(_load().d2q37_fill_philox(self._h, which, seed))
+
+    def init_rt_device(self, seed: int):
+        """Config-0/3/4 RT init generated on the device (Philox noise by global site)."""
+        _check(_load().d2q37_init_rt_device(self._h, seed))
 
     # kernels (kernels.hpp:29-46); each verb is synchronous like the reference's
     def bc(self, mode: str | None = None, sync: bool = True):

@@ -841,6 +841,14 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
     return D2Q37_OK;
 }
 
+int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed) {
+    RET(check_handle(h));
+    DeviceGuard dg(h->device);
+    CK(launch_init_rt(h->buf[h->cur], h->g, h->mp, seed, h->y0, h->ly_global, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return D2Q37_OK;
+}
+
 // ---- multi-GPU ------------------------------------------------------------
 
 int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]) {

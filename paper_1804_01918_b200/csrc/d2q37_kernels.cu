@@ -233,6 +233,37 @@ __global__ void k_philox(double* __restrict__ buf, DevGeo g, unsigned long long 
     for (int p = 0; p < kNpop; ++p) buf[e + p * g.plane] = philox_u01_dev(seed, site * kNpop + p);
 }
 
+// BASELINE config-0/3/4 Rayleigh-Taylor-like init on the device: T = 1.5 below
+// y_int(x) = ly_g/2 + 0.01 ly_g sin(2 pi x / lx), 0.5 above, plus U(-1e-3, 1e-3)
+// noise from Philox keyed by the global site index x*ly_g + y; rho = 1/T, u = 0;
+// f = equilibrium (model.cpp:259-291 operation order, DFMA-contracted).
+__global__ void k_init_rt(double* __restrict__ buf, DevGeo g, ModelParams mp, unsigned long long seed, int y0,
+                          int ly_global) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= g.ly) return;
+    const int x = blockIdx.y;
+    const int y = y0 + (q % g.vl) * g.strip + q / g.vl;
+    const double noise = -1e-3 + 2e-3 * philox_u01_dev(seed, (unsigned long long)x * ly_global + y);
+    const double yint = 0.5 * ly_global + 0.01 * ly_global * sin(2.0 * 3.14159265358979323846 * x / g.lx);
+    const double temp = ((double)y < yint ? 1.5 : 0.5) + noise;
+    const double rho = 1.0 / temp;
+    const double dt = temp - mp.t0, dt2 = dt * dt;
+    // u = 0: only the pure-temperature Hermite terms survive (mom 2, 4, 9, 11, 13)
+    const double m2 = dt, m9 = 3.0 * dt2, m11 = dt2;
+    const long long e = col_base(g, x + kHalo) + q;
+#pragma unroll 1
+    for (int p = 0; p < kNpop; ++p) {
+        const double* gp = mp.eq[p];
+        double s = 1.0;
+        s += gp[2] * m2;
+        s += gp[4] * m2;
+        s += gp[9] * m9;
+        s += gp[11] * m11;
+        s += gp[13] * m9;
+        buf[e + p * g.plane] = rho * mp.w[p] * s;
+    }
+}
+
 // Per-column sums {mass, jx, jy, sum |c|^2 f} in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) k_moments(const double* __restrict__ buf, DevGeo g, double* __restrict__ part) {
     __shared__ double red[4][256];
@@ -345,6 +376,13 @@ cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed,
                           cudaStream_t s) {
     (void)cudaGetLastError();
     k_philox<<<dim3((g.ly + 255) / 256, g.lx), 256, 0, s>>>(buf, g, seed, y0, ly_global);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, unsigned long long seed, int y0,
+                           int ly_global, cudaStream_t s) {
+    (void)cudaGetLastError();
+    k_init_rt<<<dim3((g.ly + 127) / 128, g.lx), 128, 0, s>>>(buf, g, mp, seed, y0, ly_global);
     return cudaGetLastError();
 }
 

@@ -54,6 +54,8 @@ cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_pla
 cudaError_t launch_gather(const double* buf, const DevGeo& g, double* canon_plane, int p, cudaStream_t s);
 cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed, int y0, int ly_global,
                           cudaStream_t s);
+cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, unsigned long long seed, int y0,
+                           int ly_global, cudaStream_t s);
 cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
 
 }  // namespace d2q37

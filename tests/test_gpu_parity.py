@@ -315,6 +315,20 @@ def test_step_no_nan_1000_steps(gpu, lbm):
 
 # --------------------------------------------------------------------------- full BASELINE sizes
 
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 32)])
+def test_device_rt_init_vs_oracle(gpu, lbm, po, layout, vl):
+    """init_rt_device == the oracle's Philox-noise RT recipe (<= 1e-14), per slab of a taller lattice."""
+    lx, ly = 32, 256
+    want = po.orc_lattice("rt_philox", lx, ly, seed=12345)
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.init_rt_device(12345)
+    assert max_rel(s.dump(), want) <= 1e-14
+    grp = lbm.SlabGroup(layout, lx, ly, 1 if layout == "soa" else 8, 4)
+    for sl in grp.slabs:
+        sl.init_rt_device(12345)
+    assert max_rel(grp.dump(), want) <= 1e-14
+
+
 @pytest.mark.slow
 def test_config1_full_size_propagate_bitwise(gpu, lbm):
     """Config 1 at full size (1024x8192): device Philox == host Philox, propagate == np.roll oracle."""
