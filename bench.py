@@ -4,7 +4,7 @@
 Workload (BASELINE configs 3/4): a 4096 x 16384 lattice per GPU (weak
 scaling; the global lattice is 4096 x 16384*N, split into y-slabs), config-0
 Rayleigh-Taylor-like init, periodic x, top/bottom specular walls, omega 0.8
-(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the CSoA (vl = 32) store.
+(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the CAoSoA (vl = 32) store.
 value = whole-job MLUPS over the K timed steps (max over ranks of the device
 time).  Inputs are larger than L2 (2 x 19.9 GB per GPU vs 126 MB), so no
 explicit flush is needed.
@@ -249,14 +249,15 @@ def bench_config0(lbm, warmup: int) -> dict:
     lx, ly, n = 256, 1024, 100
     canon = lbm.make_lattice("rt", lx, ly, SEED)
     out = {}
-    for variant in ("fused", "unfused"):
-        sim = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant=variant)
+    for layout, vl, variant in (("caosoa", 32, "fused"), ("soa", 1, "fused"), ("soa", 1, "unfused")):
+        sim = lbm.Simulation(layout, lx, ly, vl, device=0, bc="wall", variant=variant)
         sim.load(canon)
         sim.step(OMEGA, warmup)
         best = min(time_steps(sim, 1, lambda: sim.step(OMEGA, n, sync=False)) for _ in range(5))
-        out[variant] = {"ms_per_100_steps": best, "mlups": lx * ly * n / (best / 1e3) / 1e6}
+        out[f"{layout}{vl if vl > 1 else ''}-{variant}"] = {"ms_per_100_steps": best,
+                                                            "mlups": lx * ly * n / (best / 1e3) / 1e6}
         sim.close()
-    return {"config": "c0: 256x1024 SoA, RT init, wall bc, omega 0.8, 100 steps per call (best of 5)", **out}
+    return {"config": "c0: 256x1024, RT init, wall bc, omega 0.8, 100 steps per call (best of 5)", **out}
 
 
 def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
@@ -413,7 +414,7 @@ def run_b200(args, dist: Dist):
             "config": {"workload": f"c3/c4-weak: {LX}x{ly_local} per GPU (global {LX}x{ly_global}), RT init, "
                                    f"periodic x, top/bottom specular walls, omega {OMEGA}",
                        "lx": LX, "ly_per_gpu": ly_local, "ly_global": ly_global, "layout": args.layout,
-                       "vl": args.vl if args.layout == "csoa" else 1, "variant": args.variant,
+                       "vl": args.vl if args.layout in ("csoa", "caosoa") else 1, "variant": args.variant,
                        "l2": "inputs larger than L2 (2 x 19.9 GB lattice per GPU vs 126 MB L2): no flush needed",
                        "parallelism": f"y-slab x{n}" if n > 1 else "single GPU"},
             "roofline": roofline, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
@@ -422,20 +423,25 @@ def run_b200(args, dist: Dist):
     if n == 1 and not args.no_extras:
         sim.close()
         del sim
-        line["kernels"] = {"propagate_c1": bench_propagate(lbm, 5, 200, hbm_peak),
-                           "propagate_c1_csoa32": bench_propagate(lbm, 5, 200, hbm_peak, "csoa", 32),
-                           "collide_c2": bench_collide(lbm, 5, 200, hbm_peak),
-                           "collide_c2_csoa32": bench_collide(lbm, 5, 200, hbm_peak, "csoa", 32),
-                           "step_c0": bench_config0(lbm, 5)}
+        kernels = {}
+        for lay, vl in (("soa", 1), ("csoa", 32), ("caosoa", 32), ("aos", 1)):
+            tag = f"{lay}{vl if vl > 1 else ''}"
+            kernels[f"propagate_c1_{tag}"] = bench_propagate(lbm, 5, 200, hbm_peak, lay, vl)
+            kernels[f"collide_c2_{tag}"] = bench_collide(lbm, 5, 200, hbm_peak, lay, vl)
+        kernels["step_c0"] = bench_config0(lbm, 5)
+        line["kernels"] = kernels
         variants = {}
-        for lay, vl, var in (("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"), ("csoa", 32, "unfused")):
+        for lay, vl, var in (("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"),
+                             ("csoa", 32, "unfused"), ("aos", 1, "fused"), ("caosoa", 32, "fused"),
+                             ("caosoa", 32, "unfused")):
             if (lay, var) == (args.layout, args.variant):
                 continue
-            variants[f"{lay}{vl if lay == 'csoa' else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20)
+            variants[f"{lay}{vl if vl > 1 else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20)
         line["variants_c3"] = variants
         try:
-            line["slab_schedule"] = {"strong_8gpu_slab": bench_slab_schedule(lbm, "csoa", 32, 4096, 3, 50),
-                                     "weak_slab": bench_slab_schedule(lbm, "csoa", 32, LY_PER_GPU, 3, 20)}
+            line["slab_schedule"] = {
+                "strong_8gpu_slab": bench_slab_schedule(lbm, args.layout, args.vl, 4096, 3, 50),
+                "weak_slab": bench_slab_schedule(lbm, args.layout, args.vl, LY_PER_GPU, 3, 20)}
         except Exception as e:  # NCCL unavailable must not sink the line
             line["slab_schedule"] = {"error": str(e)}
     if n == 1 and not args.no_cpu:
@@ -490,7 +496,7 @@ def run_e2e(lbm, sim, args, dist: Dist):
 def load_ncu_traffic(layout: str, ly: int):
     """DRAM bytes/launch of the fused kernel from the committed ncu capture (profiles/), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
-    key = "prof_fused_csoa" if layout == "csoa" else "prof_fused"
+    key = {"csoa": "prof_fused_csoa", "caosoa": "prof_fused_caosoa"}.get(layout, "prof_fused")
     try:
         with open(path) as f:
             rec = json.load(f)[key]
@@ -506,7 +512,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--layout", choices=["soa", "csoa"], default="csoa")
+    ap.add_argument("--layout", choices=["aos", "soa", "csoa", "caosoa"], default="caosoa")
     ap.add_argument("--vl", type=int, default=32)
     ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU")

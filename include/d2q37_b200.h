@@ -44,8 +44,8 @@ enum {
     D2Q37_ERR_UNSUPPORTED = 5
 };
 
-/* LayoutKind numbering of layout.hpp:12 {AoS, SoA, CSoA, CAoSoA}.  SoA and CSoA
- * are device layouts here; AoS/CAoSoA return D2Q37_ERR_UNSUPPORTED. */
+/* LayoutKind numbering of layout.hpp:12 {AoS, SoA, CSoA, CAoSoA}; all four are
+ * device layouts (the reference's element order, with a device column pitch). */
 enum { D2Q37_AOS = 0, D2Q37_SOA = 1, D2Q37_CSOA = 2, D2Q37_CAOSOA = 3 };
 
 /* Boundary condition of the y faces.  PERIODIC is the reference

@@ -27,6 +27,7 @@ constexpr int kTransportNone = 0;
 constexpr int kTransportNccl = 1;
 constexpr int kTransportGroup = 2;
 constexpr int kEventRing = 64;
+constexpr int kGraphSteps = 10;  // even, so a replay leaves the state in the same buffer
 
 }  // namespace
 
@@ -76,6 +77,15 @@ struct d2q37_lattice {
     std::vector<ProfEntry> prof_pending;
     std::vector<cudaEvent_t> prof_free;
     std::vector<d2q37_lattice*> group;  // transport == group: all slabs, in rank order
+    // cached CUDA graph of kGraphSteps single-domain steps (d2q37_step)
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        double omega = 0.0;
+        int variant = -1, bc = -1, cur = -1, math = -1;
+        unsigned long model_gen = 0;
+        cudaStream_t stream = nullptr;
+    } graph;
+    unsigned long model_gen = 0;  // bumped by every set_model
 };
 
 namespace {
@@ -120,15 +130,15 @@ struct DeviceGuard {
 bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 // Geometry checks of layout.cpp:12-24 plus the device limits.
+bool clustered(int layout) { return layout == D2Q37_CSOA || layout == D2Q37_CAOSOA; }
+bool site_major(int layout) { return layout == D2Q37_AOS || layout == D2Q37_CAOSOA; }
+
 int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
-    if (layout == D2Q37_AOS || layout == D2Q37_CAOSOA)
-        return fail(D2Q37_ERR_UNSUPPORTED, "layout %d (AoS/CAoSoA) has no device implementation; use SoA or CSoA",
-                    layout);
-    if (layout != D2Q37_SOA && layout != D2Q37_CSOA) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown layout %d", layout);
+    if (layout < D2Q37_AOS || layout > D2Q37_CAOSOA) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown layout %d", layout);
     if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");
     if (lx > 65535) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lx > 65535 not supported");
-    if (layout == D2Q37_SOA) vl = 1;
-    if (layout == D2Q37_CSOA) {
+    if (!clustered(layout)) vl = 1;  // Descriptor::evl (layout.cpp:55)
+    if (clustered(layout)) {
         if (!is_pow2(vl)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "vl must be a power of two");
         if (ly % vl != 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "ly divisible by vl");
         if (ly / vl < kHalo) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lane strip shorter than its halo (ly/vl < hy)");
@@ -141,12 +151,15 @@ int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
     g->px = lx + 2 * kHalo;
     g->lvl = 0;
     while ((1 << g->lvl) < vl) ++g->lvl;
-    // 256-byte alignment of every column's first physical element.
-    const int per = 32 / std::gcd(vl, 32);
+    // 256-byte alignment of every column's first physical element: the column
+    // stride is a multiple of 32 doubles and lead puts (p=0, X=0, j=3, k=0) on
+    // a 32-double boundary.
+    g->rstride = site_major(layout) ? (long long)kNpop * vl : vl;
+    const int per = int(32 / std::gcd(g->rstride, 32LL));
     g->pitch = (g->sy + per - 1) / per * per;
-    g->lead = (32 - (kHalo * vl) % 32) % 32;
-    g->plane = (long long)g->px * g->pitch * vl;
-    g->plane = (g->plane + 31) / 32 * 32;
+    g->cstride = (long long)g->pitch * g->rstride;
+    g->lead = (32 - (kHalo * g->rstride) % 32) % 32;
+    g->pstride = site_major(layout) ? vl : (g->px * g->cstride + 31) / 32 * 32;
     return D2Q37_OK;
 }
 
@@ -154,7 +167,7 @@ void fill_offsets(d2q37_lattice* h, int corrupt = -1) {
     const DevGeo& g = h->g;
     for (int p = 0; p < kNpop; ++p) {
         // build_offset_table (kernels.cpp:180-195): pull from (x - cx, y - cy).
-        h->off_pull.o[p] = (long long)p * g.plane - ((long long)cx_of(p) * g.pitch + cy_of(p)) * g.vl;
+        h->off_pull.o[p] = (long long)p * g.pstride - (long long)cx_of(p) * g.cstride - (long long)cy_of(p) * g.rstride;
         if (p == corrupt) h->off_pull.o[p] += 1;
     }
 }
@@ -189,6 +202,7 @@ int upload_model(d2q37_lattice* h, const d2q37_model* m) {
         }
     for (int i = 0; i < kNpop; ++i) h->mp.w[i] = m->w[i];
     h->mp.t0 = m->t0;
+    ++h->model_gen;  // captured step graphs carry the old constants
     return D2Q37_OK;
 }
 
@@ -232,7 +246,7 @@ int new_stream(d2q37_lattice* h) {
 int alloc_lattice(d2q37_lattice* h) {
     DeviceGuard dg(h->device);
     const DevGeo& g = h->g;
-    h->buf_elems = size_t(g.lead + kNpop * g.plane + 32);
+    h->buf_elems = size_t(g.lead + (site_major(h->layout) ? g.px * g.cstride : kNpop * g.pstride) + 32);
     for (int b = 0; b < 2; ++b) {
         CK(cudaMalloc(&h->buf[b], h->buf_elems * sizeof(double)));
         CK(cudaMemset(h->buf[b], 0, h->buf_elems * sizeof(double)));  // AlignedBuffer is zeroed (layout.cpp:101)
@@ -286,6 +300,7 @@ void free_lattice(d2q37_lattice* h) {
         cudaEventDestroy(e.b);
     }
     for (cudaEvent_t e : h->prof_free) cudaEventDestroy(e);
+    if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
     if (h->comm) nccl_comm_destroy(h->comm);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     h->stream_owner.reset();
@@ -470,6 +485,55 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
     return D2Q37_OK;
 }
 
+void drop_step_graph(d2q37_lattice* h) {
+    if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
+    h->graph = d2q37_lattice::StepGraph{};
+}
+
+// Captures kGraphSteps single-domain steps (edge + fused, or edge + propagate +
+// collide) into one executable graph, keyed by everything the kernels bake in.
+// On any capture failure (e.g. a legacy default stream) graphs stay off and
+// d2q37_step launches directly.
+int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
+    auto& gr = h->graph;
+    if (gr.exec && gr.omega == omega && gr.variant == variant && gr.bc == bc && gr.cur == h->cur &&
+        gr.math == h->math && gr.model_gen == h->model_gen && gr.stream == h->stream)
+        return D2Q37_OK;
+    drop_step_graph(h);
+    const int cur0 = h->cur;
+    const long ts0 = h->time_step;
+    if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return D2Q37_OK;
+    }
+    int rc = D2Q37_OK;
+    for (int i = 0; i < kGraphSteps && rc == D2Q37_OK; ++i) rc = step_local(h, omega, variant, bc);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+    h->cur = cur0;  // capture only recorded the launches
+    h->time_step = ts0;
+    if (rc != D2Q37_OK || ec != cudaSuccess || !graph) {
+        if (graph) cudaGraphDestroy(graph);
+        (void)cudaGetLastError();
+        return rc;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&gr.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        gr.exec = nullptr;
+        (void)cudaGetLastError();
+        return D2Q37_OK;
+    }
+    gr.omega = omega;
+    gr.variant = variant;
+    gr.bc = bc;
+    gr.cur = h->cur;
+    gr.math = h->math;
+    gr.model_gen = h->model_gen;
+    gr.stream = h->stream;
+    return D2Q37_OK;
+}
+
 // Slab step, phase 1 (before the halos are needed): local ghosts + interior.
 int slab_phase1(d2q37_lattice* h, double omega, int variant, int bc) {
     RET(edge(h, bc, kEdgeLocal));
@@ -513,10 +577,10 @@ int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n
     const DevGeo& g = h->g;
     double* dst = h->buf[which == 0 ? h->cur : 1 - h->cur];
     const size_t plane_vals = size_t(g.lx) * g.ly;
-    if (g.vl == 1 && !src_device) {
+    if (h->layout == D2Q37_SOA && !src_device) {
         // SoA: one pitched copy per population straight from the host array.
         for (int p = 0; p < kNpop; ++p)
-            CK(cudaMemcpy2DAsync(dst + col_base(g, kHalo) + p * g.plane, size_t(g.pitch) * sizeof(double),
+            CK(cudaMemcpy2DAsync(dst + site_of(g, kHalo, 0) + p * g.pstride, size_t(g.cstride) * sizeof(double),
                                  src + p * plane_vals, size_t(g.ly) * sizeof(double), size_t(g.ly) * sizeof(double),
                                  size_t(g.lx), cudaMemcpyHostToDevice, h->stream));
     } else {
@@ -543,10 +607,11 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
     const DevGeo& g = h->g;
     const double* src = h->buf[which == 0 ? h->cur : 1 - h->cur];
     const size_t plane_vals = size_t(g.lx) * g.ly;
-    if (g.vl == 1 && !out_device) {
+    if (h->layout == D2Q37_SOA && !out_device) {
         for (int p = 0; p < kNpop; ++p)
-            CK(cudaMemcpy2DAsync(out + p * plane_vals, size_t(g.ly) * sizeof(double), src + col_base(g, kHalo) + p * g.plane,
-                                 size_t(g.pitch) * sizeof(double), size_t(g.ly) * sizeof(double), size_t(g.lx),
+            CK(cudaMemcpy2DAsync(out + p * plane_vals, size_t(g.ly) * sizeof(double),
+                                 src + site_of(g, kHalo, 0) + p * g.pstride, size_t(g.cstride) * sizeof(double),
+                                 size_t(g.ly) * sizeof(double), size_t(g.lx),
                                  cudaMemcpyDeviceToHost, h->stream));
     } else {
         if (!out_device && !h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
@@ -683,6 +748,14 @@ static size_t padded_count(const d2q37_lattice* h) {
     return size_t(kNpop) * h->g.px * h->g.sy * h->g.vl;
 }
 
+// Element index of the reference Descriptor for this layout (layout.hpp:67-79).
+static size_t ref_index(const d2q37_lattice* h, int p, int X, int j, int k) {
+    const DevGeo& g = h->g;
+    const size_t cluster = site_major(h->layout) ? (size_t(X) * g.sy + j) * kNpop + p
+                                                 : (size_t(p) * g.px + X) * g.sy + j;
+    return cluster * size_t(g.vl) + size_t(k);
+}
+
 int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
@@ -693,11 +766,10 @@ int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
     CK(cudaMemcpy(dev.data(), h->buf[which == 0 ? h->cur : 1 - h->cur], h->buf_elems * sizeof(double),
                   cudaMemcpyDeviceToHost));
     const DevGeo& g = h->g;
-    size_t i = 0;
     for (int p = 0; p < kNpop; ++p)
         for (int X = 0; X < g.px; ++X)
             for (int j = 0; j < g.sy; ++j)
-                for (int k = 0; k < g.vl; ++k) host[i++] = dev[size_t(elem_of(g, p, X, j, k))];
+                for (int k = 0; k < g.vl; ++k) host[ref_index(h, p, X, j, k)] = dev[size_t(elem_of(g, p, X, j, k))];
     return D2Q37_OK;
 }
 
@@ -711,11 +783,10 @@ int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaMemcpy(dev.data(), d, h->buf_elems * sizeof(double), cudaMemcpyDeviceToHost));
     const DevGeo& g = h->g;
-    size_t i = 0;
     for (int p = 0; p < kNpop; ++p)
         for (int X = 0; X < g.px; ++X)
             for (int j = 0; j < g.sy; ++j)
-                for (int k = 0; k < g.vl; ++k) dev[size_t(elem_of(g, p, X, j, k))] = host[i++];
+                for (int k = 0; k < g.vl; ++k) dev[size_t(elem_of(g, p, X, j, k))] = host[ref_index(h, p, X, j, k)];
     CK(cudaMemcpy(d, dev.data(), h->buf_elems * sizeof(double), cudaMemcpyHostToDevice));
     return D2Q37_OK;
 }
@@ -767,8 +838,20 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         d2q37_lattice** slabs = h->group.data();
         return d2q37_group_step(slabs, int(h->group.size()), omega, nsteps, variant, bc);
     }
-    for (int s = 0; s < nsteps; ++s) {
-        if (!local_only(h) && remote_faces(h, bc)) {
+    const bool slab = !local_only(h) && remote_faces(h, bc);
+    int s = 0;
+    if (!slab && !h->prof_on && nsteps >= kGraphSteps) {
+        // Launch-bound small lattices: replay kGraphSteps steps as one CUDA graph.
+        RET(ensure_step_graph(h, omega, variant, bc));
+        if (h->graph.exec) {
+            for (; s + kGraphSteps <= nsteps; s += kGraphSteps) {
+                CK(cudaGraphLaunch(h->graph.exec, h->stream));
+                h->time_step += kGraphSteps;  // kGraphSteps is even: cur is unchanged
+            }
+        }
+    }
+    for (; s < nsteps; ++s) {
+        if (slab) {
             RET(exchange_begin(h, bc));
             RET(slab_phase1(h, omega, variant, bc));
             RET(slab_phase2(h, omega, variant, bc));

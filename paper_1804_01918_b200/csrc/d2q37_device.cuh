@@ -1,18 +1,21 @@
 // d2q37_device.cuh -- device-side building blocks of the D2Q37 hot path (sm_100a).
 //
-// HBM layout: the reference's padded SoA / CSoA
-// storage (layout.hpp:46-98) generalised with a column pitch, so that one
-// code path serves both layouts (SoA is CSoA with vl = 1):
+// HBM layout: the reference's padded storage
+// (layout.hpp:46-98) for all four layouts, generalised with a column pitch
+// and expressed with three strides so one code path serves every layout:
 //
-//   elem(p, X, j, k) = lead + p*plane + (X*pitch + j)*vl + k
+//   elem(p, X, j, k) = lead + p*pstride + X*cstride + j*rstride + k
+//   SoA/CSoA:   pstride = plane, rstride = vl      (SoA: vl = 1)
+//   AoS/CAoSoA: pstride = vl,    rstride = 37*vl   (AoS: vl = 1)
 //
 //   X in [0, lx+6)        padded column (3 ghost columns each side)
 //   j in [0, strip+6)     padded row of a lane strip (3 halo rows each end)
 //   k in [0, vl)          lane; lattice y = k*strip + (j - 3)
 //
 // pitch >= sy = strip + 6 and lead are chosen so that every column's first
-// physical element (j = 3, k = 0) starts a 256-byte segment: one warp of
-// consecutive q = (j-3)*vl + k stores two whole 128-byte lines.
+// physical element (j = 3, k = 0, p = 0) starts a 256-byte segment: for the
+// SoA-type layouts one warp of consecutive q = (j-3)*vl + k stores two whole
+// 128-byte lines, for CAoSoA (vl = 32) every population cluster is one.
 #pragma once
 
 #include <cstdint>
@@ -28,16 +31,19 @@ struct DevGeo {
     int pitch;      // device rows per padded column (>= sy)
     int px;         // lx + 6
     int lvl;        // log2(vl)
-    long long lead;   // element offset of population plane 0
-    long long plane;  // elements per population plane
+    long long lead;     // element offset of (p, X, j, k) = (0, 0, 0, 0)
+    long long pstride;  // between populations of one site: plane (SoA/CSoA) or vl (AoS/CAoSoA)
+    long long rstride;  // between padded rows j of a lane: vl (SoA/CSoA) or 37*vl (AoS/CAoSoA)
+    long long cstride;  // between padded columns X: pitch * rstride
 };
 
+// Reference Descriptor::elem (layout.hpp:67-79) for all four layouts.
 __host__ __device__ __forceinline__ long long elem_of(const DevGeo& g, int p, int X, int j, int k) {
-    return g.lead + (long long)p * g.plane + ((long long)X * g.pitch + j) * g.vl + k;
+    return g.lead + (long long)p * g.pstride + (long long)X * g.cstride + (long long)j * g.rstride + k;
 }
-// Element of physical q (q = (j-3)*vl + k, 0 <= q < ly) of column X, population 0.
-__host__ __device__ __forceinline__ long long col_base(const DevGeo& g, int X) {
-    return g.lead + ((long long)X * g.pitch + kHalo) * g.vl;
+// Population-0 element of the site at memory position q = (j-3)*vl + k of column X.
+__host__ __device__ __forceinline__ long long site_of(const DevGeo& g, int X, int q) {
+    return g.lead + (long long)X * g.cstride + (long long)(kHalo + (q >> g.lvl)) * g.rstride + (q & (g.vl - 1));
 }
 
 // Model constants travel as kernel parameters (constant bank 0, broadcast to

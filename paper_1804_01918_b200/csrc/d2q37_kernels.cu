@@ -41,7 +41,7 @@ __device__ __forceinline__ long long pull_offset(const Offsets& off, const DevGe
     long long o = off.o[p];
     if (LANES) {
         const int cy = cy_of(p);
-        const long long wrap = (long long)g.strip * g.vl - 1;
+        const long long wrap = (long long)g.strip * g.rstride - 1;
         if (cy > 0 && row < cy && k > 0) o += wrap;
         if (cy < 0 && row >= g.strip + cy && k < g.vl - 1) o -= wrap;
     }
@@ -55,13 +55,13 @@ __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __re
     const int z = blockIdx.z;
     const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= seg.q0[z] + seg.nq) return;
-    const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    const long long e = site_of(g, blockIdx.y + kHalo, q);
     const int row = q >> g.lvl, k = q & (g.vl - 1);
     double f[kNpop];
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + pull_offset<LANES>(off, g, p, row, k));
 #pragma unroll
-    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);
+    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.pstride, f[p]);
 }
 
 template <bool STRICT, bool SHIFT, bool LANES>
@@ -71,16 +71,16 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     const int z = blockIdx.z;
     const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= seg.q0[z] + seg.nq) return;
-    const long long e = col_base(g, blockIdx.y + kHalo) + q;
+    const long long e = site_of(g, blockIdx.y + kHalo, q);
     const int row = q >> g.lvl, k = q & (g.vl - 1);
     double f[kNpop];
 #pragma unroll
     for (int p = 0; p < kNpop; ++p)
-        f[p] = ld_stream(src + e + (SHIFT ? pull_offset<LANES>(off, g, p, row, k) : p * g.plane));
+        f[p] = ld_stream(src + e + (SHIFT ? pull_offset<LANES>(off, g, p, row, k) : p * g.pstride));
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
 #pragma unroll
-    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.plane, f[p]);
+    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.pstride, f[p]);
 }
 
 // ---------------------------------------------------------------------------
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256) k_edge(double* __restrict__ buf, DevGeo g
     const int p = int(u / (6LL * g.ly));
     const int X = c < 3 ? c : g.lx + kHalo + (c - 3);
     const int Xs = wrapi(X - kHalo, g.lx) + kHalo;
-    buf[col_base(g, X) + p * g.plane + qq] = buf[col_base(g, Xs) + p * g.plane + qq];
+    buf[site_of(g, X, qq) + p * g.pstride] = buf[site_of(g, Xs, qq) + p * g.pstride];
 }
 
 // Slab boundary rows -> send buffers, [slot][x] contiguous.  send_hi carries
@@ -189,7 +189,7 @@ __global__ void k_scatter(double* __restrict__ buf, DevGeo g, const double* __re
     if (t >= (long long)g.lx * g.ly) return;
     const int x = int(t / g.ly), q = int(t % g.ly);
     const int y = (q % g.vl) * g.strip + q / g.vl;
-    buf[col_base(g, x + kHalo) + p * g.plane + q] = canon[(long long)x * g.ly + y];
+    buf[site_of(g, x + kHalo, q) + p * g.pstride] = canon[(long long)x * g.ly + y];
 }
 
 __global__ void k_gather(const double* __restrict__ buf, DevGeo g, double* __restrict__ canon, int p) {
@@ -197,7 +197,7 @@ __global__ void k_gather(const double* __restrict__ buf, DevGeo g, double* __res
     if (t >= (long long)g.lx * g.ly) return;
     const int x = int(t / g.ly), q = int(t % g.ly);
     const int y = (q % g.vl) * g.strip + q / g.vl;
-    canon[(long long)x * g.ly + y] = buf[col_base(g, x + kHalo) + p * g.plane + q];
+    canon[(long long)x * g.ly + y] = buf[site_of(g, x + kHalo, q) + p * g.pstride];
 }
 
 // Philox4x32-10, key = seed, counter = site-major index (x*ly_global + y)*37 + p.
@@ -228,9 +228,9 @@ __global__ void k_philox(double* __restrict__ buf, DevGeo g, unsigned long long 
     const int x = blockIdx.y;
     const int y = (q % g.vl) * g.strip + q / g.vl;
     const unsigned long long site = (unsigned long long)x * ly_global + (unsigned long long)(y0 + y);
-    const long long e = col_base(g, x + kHalo) + q;
+    const long long e = site_of(g, x + kHalo, q);
 #pragma unroll 1
-    for (int p = 0; p < kNpop; ++p) buf[e + p * g.plane] = philox_u01_dev(seed, site * kNpop + p);
+    for (int p = 0; p < kNpop; ++p) buf[e + p * g.pstride] = philox_u01_dev(seed, site * kNpop + p);
 }
 
 // BASELINE config-0/3/4 Rayleigh-Taylor-like init on the device: T = 1.5 below
@@ -250,7 +250,7 @@ __global__ void k_init_rt(double* __restrict__ buf, DevGeo g, ModelParams mp, un
     const double dt = temp - mp.t0, dt2 = dt * dt;
     // u = 0: only the pure-temperature Hermite terms survive (mom 2, 4, 9, 11, 13)
     const double m2 = dt, m9 = 3.0 * dt2, m11 = dt2;
-    const long long e = col_base(g, x + kHalo) + q;
+    const long long e = site_of(g, x + kHalo, q);
 #pragma unroll 1
     for (int p = 0; p < kNpop; ++p) {
         const double* gp = mp.eq[p];
@@ -260,7 +260,7 @@ __global__ void k_init_rt(double* __restrict__ buf, DevGeo g, ModelParams mp, un
         s += gp[9] * m9;
         s += gp[11] * m11;
         s += gp[13] * m9;
-        buf[e + p * g.plane] = rho * mp.w[p] * s;
+        buf[e + p * g.pstride] = rho * mp.w[p] * s;
     }
 }
 
@@ -270,10 +270,10 @@ __global__ void __launch_bounds__(256) k_moments(const double* __restrict__ buf,
     const int X = blockIdx.x + kHalo;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     for (int q = threadIdx.x; q < g.ly; q += blockDim.x) {
-        const long long e = col_base(g, X) + q;
+        const long long e = site_of(g, X, q);
 #pragma unroll
         for (int p = 0; p < kNpop; ++p) {
-            const double v = buf[e + p * g.plane];
+            const double v = buf[e + p * g.pstride];
             s[0] += v;
             s[1] += cx_of(p) * v;
             s[2] += cy_of(p) * v;

@@ -4,6 +4,7 @@
   --case step       4096x16384 SoA, RT init, wall bc, omega 0.8, fused steps   (bench workload)
   --case unfused    same lattice, unfused steps (edge + propagate + collide)
   --case csoa       same lattice, CSoA vl=32 fused steps
+  --case caosoa     same lattice, CAoSoA vl=32 fused steps                    (bench default)
   --case propagate  1024x8192 SoA Philox input, propagate prv->nxt            (BASELINE config 1)
   --case collide    1024x8192 SoA c2 input, collide nxt->prv                  (BASELINE config 2)
 """
@@ -18,13 +19,13 @@ import paper_1804_01918_b200 as lbm  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="step", choices=["step", "unfused", "csoa", "propagate", "collide"])
+    ap.add_argument("--case", default="step", choices=["step", "unfused", "csoa", "caosoa", "propagate", "collide"])
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--lx", type=int, default=4096)
     ap.add_argument("--ly", type=int, default=16384)
     a = ap.parse_args()
-    if a.case in ("step", "unfused", "csoa"):
-        layout, vl = ("csoa", 32) if a.case == "csoa" else ("soa", 1)
+    if a.case in ("step", "unfused", "csoa", "caosoa"):
+        layout, vl = (a.case, 32) if a.case in ("csoa", "caosoa") else ("soa", 1)
         s = lbm.Simulation(layout, a.lx, a.ly, vl, bc="wall", variant="unfused" if a.case == "unfused" else "fused")
         s.load(lbm.make_lattice("rt", a.lx, a.ly, 12345))
         for _ in range(a.steps):

@@ -33,7 +33,8 @@ def lattice_case(lx, ly, seed, name, steps=10, omega_step=1.0, omega_collide=1.2
     out = {"init": init, "lx": lx, "ly": ly, "seed": seed, "omega_step": omega_step,
            "omega_collide": omega_collide, "steps": steps, "vl_csoa": vl_csoa}
     # halo_exchange + propagate on the SoA and CSoA layouts (kernels.cpp:197-258)
-    for tag, layout, vl in (("soa", po.SOA, 1), ("csoa", po.CSOA, vl_csoa)):
+    for tag, layout, vl in (("aos", po.AOS, 1), ("soa", po.SOA, 1), ("csoa", po.CSOA, vl_csoa),
+                            ("caosoa", po.CAOSOA, vl_csoa)):
         s = po.RefSim(layout, lx, ly, vl, workers=2)
         s.load(init)
         s.halo_exchange()

@@ -15,7 +15,8 @@ from conftest import golden, macros_fields, max_rel
 pytestmark = pytest.mark.gpu
 
 GEOMS = [(16, 32), (64, 128)]
-LAYOUTS = [("soa", 1), ("csoa", 1), ("csoa", 2), ("csoa", 4), ("csoa", 8)]
+LAYOUTS = [("aos", 1), ("soa", 1), ("csoa", 1), ("csoa", 2), ("csoa", 4), ("csoa", 8), ("caosoa", 1),
+           ("caosoa", 2), ("caosoa", 4), ("caosoa", 8)]
 
 
 def sim_of(lbm, layout, lx, ly, vl=1, **kw):
@@ -37,8 +38,9 @@ def test_propagate_bitwise_vs_oracle(gpu, lbm, po, lx, ly, layout, vl):
     assert np.array_equal(s.dump(which=1), want)
 
 
-@pytest.mark.parametrize("layout,vl,lx,ly", [("csoa", 4, 5, 12), ("soa", 1, 5, 2), ("soa", 1, 1, 8),
-                                             ("csoa", 32, 8, 96)])
+@pytest.mark.parametrize("layout,vl,lx,ly", [("csoa", 4, 5, 12), ("caosoa", 4, 5, 12), ("soa", 1, 5, 2),
+                                             ("aos", 1, 5, 2), ("soa", 1, 1, 8), ("aos", 1, 1, 8),
+                                             ("csoa", 32, 8, 96), ("caosoa", 32, 8, 96)])
 def test_propagate_edge_geometries(gpu, lbm, po, layout, vl, lx, ly):
     """Strip == halo depth (test_kernels.cpp:171-189), ly=2 < halo (:191-209), lx=1, vl=32 warp-wide clusters."""
     init = lbm.make_lattice("random", lx, ly, seed=606)
@@ -49,19 +51,34 @@ def test_propagate_edge_geometries(gpu, lbm, po, layout, vl, lx, ly):
     assert np.array_equal(s.dump(which=1), po.orc_propagate(init, po.BC_PERIODIC))
 
 
-@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 4)])
-def test_golden_reference_propagate_and_halo(gpu, lbm, layout, vl):
-    """Against fixtures written by the reference itself (tests/golden/make_golden.py)."""
+@pytest.mark.parametrize("layout", ["aos", "soa", "csoa", "caosoa"])
+def test_golden_reference_propagate_and_halo(gpu, lbm, layout):
+    """Against fixtures written by the reference itself (tests/golden/make_golden.py): the whole
+    padded halo_exchange buffer in the reference's own element order, and propagate."""
     for name in ("ref_random_16x32.npz", "ref_random_5x12.npz"):
         g = golden(name)
         lx, ly = int(g["lx"]), int(g["ly"])
-        vl_ = 1 if layout == "soa" else int(g["vl_csoa"])
+        vl_ = 1 if layout in ("soa", "aos") else int(g["vl_csoa"])
         s = sim_of(lbm, layout, lx, ly, vl_)
         s.load(g["init"])
         s.bc("periodic")
         assert np.array_equal(s.read_padded(), g[f"padded_{layout}"]), "halo_exchange padded buffer differs"
         s.propagate_only()
         assert np.array_equal(s.dump(which=1), g[f"propagate_{layout}"])
+
+
+@pytest.mark.parametrize("layout,vl", [("aos", 1), ("caosoa", 4), ("caosoa", 32)])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_site_major_layouts_bc_propagate(gpu, lbm, po, layout, vl, bc):
+    """AoS / CAoSoA device layouts: bc + propagate bit-exact vs the oracle (periodic and wall)."""
+    lx, ly = 7, 96
+    init = lbm.make_lattice("random", lx, ly, seed=321)
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.load(init)
+    assert np.array_equal(s.dump(), init)
+    s.bc(bc)
+    s.propagate_only()
+    assert np.array_equal(s.dump(which=1), po.orc_propagate(init, po.BC_WALL if bc == "wall" else po.BC_PERIODIC))
 
 
 @pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 2), ("csoa", 8)])
@@ -266,7 +283,8 @@ def test_layouts_and_variants_bitwise_identical(gpu, lbm, bc):
     lx, ly = 24, 192
     init = lbm.make_lattice("random", lx, ly, seed=13)
     outs = []
-    for layout, vl in (("soa", 1), ("csoa", 2), ("csoa", 8), ("csoa", 32)):
+    for layout, vl in (("soa", 1), ("csoa", 2), ("csoa", 8), ("csoa", 32), ("aos", 1), ("caosoa", 8),
+                       ("caosoa", 32)):
         for variant in ("fused", "unfused"):
             s = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
             s.load(init)
@@ -278,7 +296,8 @@ def test_layouts_and_variants_bitwise_identical(gpu, lbm, bc):
 
 @pytest.mark.parametrize("nslabs", [2, 4])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
-@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 4, "fused")])
+@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 4, "fused"),
+                                               ("caosoa", 4, "fused"), ("aos", 1, "unfused")])
 def test_slab_group_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, vl, variant):
     """GPU-count invariance (test_kernels.cpp:361-381 analogue): y-slabs == one domain, bit for bit."""
     lx, ly = 16, 256
@@ -290,6 +309,27 @@ def test_slab_group_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, v
     grp.load(init)
     grp.step(1.1, 5)
     assert np.array_equal(grp.dump(), ref.dump())
+
+
+@pytest.mark.parametrize("variant", ["fused", "unfused"])
+def test_graph_replayed_steps_equal_single_steps(gpu, lbm, variant):
+    """step(n) replays a captured 10-step CUDA graph; it must equal n single steps bit for bit,
+    including after the model / omega / bc change that forces a recapture."""
+    lx, ly = 32, 96
+    init = lbm.make_lattice("random", lx, ly, seed=2)
+    a = sim_of(lbm, "csoa", lx, ly, 4, variant=variant, bc="wall")
+    b = sim_of(lbm, "csoa", lx, ly, 4, variant=variant, bc="wall")
+    a.load(init)
+    b.load(init)
+    a.step(1.1, 25)
+    for _ in range(25):
+        b.step(1.1, 1)
+    assert a.time_step == b.time_step == 25
+    assert np.array_equal(a.dump(), b.dump())
+    a.step(0.7, 20, bc="periodic")
+    for _ in range(20):
+        b.step(0.7, 1, bc="periodic")
+    assert np.array_equal(a.dump(), b.dump())
 
 
 def test_step_conserves_mass(gpu, lbm):

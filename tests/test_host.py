@@ -109,8 +109,8 @@ def test_host_model_helpers(lbm):
 
 
 @pytest.mark.parametrize("args,msg", [
-    (("aos", 8, 16, 1), "no device implementation"),
-    (("caosoa", 8, 16, 4), "no device implementation"),
+    (("caosoa", 8, 16, 3), "power of two"),
+    (("caosoa", 8, 18, 4), "divisible"),
     (("csoa", 8, 16, 3), "power of two"),
     (("csoa", 8, 18, 4), "divisible"),
     (("csoa", 8, 16, 8), "shorter than its halo"),
