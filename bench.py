@@ -278,6 +278,15 @@ def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
         out[name] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6}
         if name != "single_domain":
             out[name]["exposed_halo_ms"] = sim.exposed_halo_ms()
+        # per-kernel breakdown (separate, profiled pass)
+        sim.set_profiling(True)
+        sim.kernel_times()
+        for _ in range(10):
+            sim.step(OMEGA, 1, sync=False)
+        kt = sim.kernel_times()
+        sim.set_profiling(False)
+        out[name]["kernel_ms_per_step"] = {k: v[0] / 10 for k, v in kt.items() if v[1]}
+        out[name]["launches_per_step"] = {k: v[1] / 10 for k, v in kt.items() if v[1]}
         sim.close()
     out["schedule_overhead"] = out["nccl_self_ring"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
     out["config"] = f"{LX}x{ly} {layout}{vl}, periodic y through NCCL to self vs local wrap, {steps} steps"

@@ -197,9 +197,10 @@ int d2q37_slab_info(const d2q37_lattice* h, int out[4]);
 /* Per-kernel device timing (CUDA events recorded around each launch on the
  * handle's stream while profiling is on).  d2q37_kernel_times returns the
  * summed milliseconds and launch counts since the last call, per class:
- * 0 edge (bc), 1 propagate, 2 collide, 3 fused propagate+collide, 4 pack. */
+ * 0 edge (bc), 1 propagate, 2 collide, 3 fused propagate+collide, 4 pack,
+ * 5 fused boundary sites of a slab (after its halos arrived). */
 int d2q37_set_profiling(d2q37_lattice* h, int on);
-int d2q37_kernel_times(d2q37_lattice* h, double ms[5], long counts[5]);
+int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
 /* Average device time (ms) of the last step's halo phase that was not hidden
  * behind interior compute (0 for single-domain lattices); see DESIGN.md. */
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);

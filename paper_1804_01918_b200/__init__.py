@@ -498,15 +498,15 @@ class Simulation:
     def sync(self):
         _check(_load().d2q37_sync(self._h))
 
-    KERNEL_CLASSES = ("edge", "propagate", "collide", "fused", "pack")
+    KERNEL_CLASSES = ("edge", "propagate", "collide", "fused", "pack", "boundary")
 
     def set_profiling(self, on: bool = True):
         _check(_load().d2q37_set_profiling(self._h, int(bool(on))))
 
     def kernel_times(self) -> dict:
         """{class: (total_ms, launches)} since the last call (CUDA events on the lattice stream)."""
-        ms = np.zeros(5)
-        cnt = (C.c_long * 5)()
+        ms = np.zeros(6)
+        cnt = (C.c_long * 6)()
         _check(_load().d2q37_kernel_times(self._h, ms, cnt))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.KERNEL_CLASSES)}
 

@@ -345,13 +345,12 @@ struct ProfScope {
     }
 };
 
-enum { kProfEdge = 0, kProfPropagate = 1, kProfCollide = 2, kProfFused = 3, kProfPack = 4, kProfClasses = 5 };
+enum { kProfEdge = 0, kProfPropagate = 1, kProfCollide = 2, kProfFused = 3, kProfPack = 4, kProfBoundary = 5, kProfClasses = 6 };
 
 Segments all_sites(const DevGeo& g) {
-    Segments s;
-    s.q0[0] = 0;
-    s.q0[1] = 0;
+    Segments s{};
     s.nq = g.ly;
+    s.stride = 1;
     return s;
 }
 
@@ -442,44 +441,78 @@ int group_exchange(std::vector<d2q37_lattice*>& slabs, int bc) {
     return D2Q37_OK;
 }
 
-bool can_split(const d2q37_lattice* h) { return h->g.strip >= 2 * kHalo + 1; }
+bool can_split(const d2q37_lattice* h) { return h->g.strip >= 2 * kHalo; }
 
-// Sites whose pull stencil stays inside the slab's own rows: q in [3vl, ly-3vl).
-Segments interior(const DevGeo& g) {
-    Segments s;
-    s.q0[0] = kHalo * g.vl;
-    s.q0[1] = 0;
-    s.nq = g.ly - 2 * kHalo * g.vl;
-    return s;
-}
-Segments boundary(const DevGeo& g) {
-    Segments s;
-    s.q0[0] = 0;
-    s.q0[1] = g.ly - kHalo * g.vl;
-    s.nq = kHalo * g.vl;
+// Every site whose pull does not reach a remote face: all sites but lane 0's
+// first 3 rows (remote low face) and lane vl-1's last 3 rows (remote high face).
+Segments interior(const d2q37_lattice* h, int bc) {
+    Segments s = all_sites(h->g);
+    s.skip_lo = face_lo_of(h, bc) == kFaceRemote;
+    s.skip_hi = face_hi_of(h, bc) == kFaceRemote;
     return s;
 }
 
-int collide_launch(d2q37_lattice* h, int src, int dst, double omega, bool shift, const Segments& seg, int nseg) {
-    ProfScope ps(h, shift ? kProfFused : kProfCollide);
-    CK(launch_collide(h->buf[src], h->buf[dst], h->g, h->off_pull, h->mp, omega, h->math == D2Q37_MATH_STRICT, shift,
-                      seg, nseg, h->d_flag, h->stream));
+// The sites interior() skips, 3 per remote face and column; *nseg = 1 or 2.
+Segments boundary(const d2q37_lattice* h, int bc, int* nseg) {
+    const DevGeo& g = h->g;
+    Segments s{};
+    s.nq = kHalo;
+    s.stride = g.vl;
+    int n = 0;
+    if (face_lo_of(h, bc) == kFaceRemote) s.q0[n++] = 0;  // rows 0..2 of lane 0
+    if (face_hi_of(h, bc) == kFaceRemote) s.q0[n++] = (g.strip - kHalo) * g.vl + g.vl - 1;  // lane vl-1's last rows
+    *nseg = n;
+    s.dense = 1;  // 3 or 6 sites per column: one 1-D grid over all columns
+    s.nseg = n;
+    return s;
+}
+
+// Outer-face handling of the pull kernels for a step with boundary `bc`: local
+// faces (periodic wrap, wall) are resolved inside the kernel, faces shared with
+// another slab read the ghost rows k_edge fills from the receive buffers.
+Faces step_faces(const d2q37_lattice* h, int bc) {
+    Faces fc;
+    const int lo = face_lo_of(h, bc), hi = face_hi_of(h, bc);
+    fc.lo = lo == kFaceRemote ? kFaceGhost : lo;
+    fc.hi = hi == kFaceRemote ? kFaceGhost : hi;
+    std::memcpy(fc.ybar, h->edge_base.ybar, sizeof fc.ybar);
+    return fc;
+}
+
+// The propagate verb reads whatever the preceding bc verb left in the ghost rows
+// (kernels.hpp:33: "Requires halo_exchange(prv) first").
+Faces ghost_faces(const d2q37_lattice* h) {
+    Faces fc;
+    fc.lo = fc.hi = kFaceGhost;
+    std::memcpy(fc.ybar, h->edge_base.ybar, sizeof fc.ybar);
+    return fc;
+}
+
+int collide_launch(d2q37_lattice* h, int src, int dst, double omega, bool shift, const Segments& seg, int nseg,
+                   const Faces& fc) {
+    ProfScope ps(h, !shift ? kProfCollide : seg.dense ? kProfBoundary : kProfFused);
+    CK(launch_collide(h->buf[src], h->buf[dst], h->g, h->off_pull, fc, h->mp, omega, h->math == D2Q37_MATH_STRICT,
+                      shift, seg, nseg, h->d_flag, h->stream));
     return D2Q37_OK;
 }
 
-// One time step on a single domain: edge -> fused (or propagate + collide).
+int propagate_launch(d2q37_lattice* h, const Offsets& off, const Faces& fc) {
+    ProfScope ps(h, kProfPropagate);
+    CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, off, fc, all_sites(h->g), 1, h->stream));
+    return D2Q37_OK;
+}
+
+// One time step on a single domain: one fused kernel (or propagate + collide);
+// the boundary is resolved inside the pull, no bc pass.
 int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
-    RET(edge(h, bc, kEdgeAll));
+    const Faces fc = step_faces(h, bc);
     const Segments all = all_sites(h->g);
     if (variant == D2Q37_FUSED) {
-        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1));
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1, fc));
         h->cur = 1 - h->cur;
     } else {
-        {
-            ProfScope ps(h, kProfPropagate);
-            CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, all, 1, h->stream));
-        }
-        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1));
+        RET(propagate_launch(h, h->off_pull, fc));
+        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1, fc));
     }
     ++h->time_step;
     return D2Q37_OK;
@@ -534,17 +567,17 @@ int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     return D2Q37_OK;
 }
 
-// Slab step, phase 1 (before the halos are needed): local ghosts + interior.
+// Slab step, phase 1 (before the halos are needed): the interior rows, whose
+// pull stencil stays inside the slab (x wrap and lane shifts in-kernel).
 int slab_phase1(d2q37_lattice* h, double omega, int variant, int bc) {
-    RET(edge(h, bc, kEdgeLocal));
     if (variant == D2Q37_FUSED && can_split(h)) {
-        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, interior(h->g), 1));
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, interior(h, bc), 1, step_faces(h, bc)));
         if (h->transport == kTransportNccl) CK(cudaEventRecord(h->ev_int[h->ev_count % kEventRing], h->stream));
     }
     return D2Q37_OK;
 }
 
-// Slab step, phase 2 (after the halos landed): remote ghosts + boundary rows.
+// Slab step, phase 2 (after the halos landed): remote ghost rows + boundary rows.
 int slab_phase2(d2q37_lattice* h, double omega, int variant, int bc) {
     RET(exchange_wait(h));
     const bool split = variant == D2Q37_FUSED && can_split(h);
@@ -553,16 +586,19 @@ int slab_phase2(d2q37_lattice* h, double omega, int variant, int bc) {
         ++h->ev_count;
     }
     RET(edge(h, bc, kEdgeRemote));
+    const Faces fc = step_faces(h, bc);
     const Segments all = all_sites(h->g);
     if (variant == D2Q37_FUSED) {
+        int nseg = 0;
+        const Segments bnd = boundary(h, bc, &nseg);
         if (split)
-            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, boundary(h->g), 2));
+            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, bnd, nseg, fc));
         else
-            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1));
+            RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1, fc));
         h->cur = 1 - h->cur;
     } else {
-        CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, all, 1, h->stream));
-        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1));
+        RET(propagate_launch(h, h->off_pull, fc));
+        RET(collide_launch(h, 1 - h->cur, h->cur, omega, false, all, 1, fc));
     }
     ++h->time_step;
     return D2Q37_OK;
@@ -816,16 +852,14 @@ int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
     DeviceGuard dg(h->device);
     if (corrupt_population >= kNpop) return fail(D2Q37_ERR_INVALID_ARGUMENT, "corrupt_population out of range");
     Offsets off = h->off_pull;
-    if (corrupt_population >= 0) off.o[corrupt_population] += 1;
-    ProfScope ps(h, kProfPropagate);
-    CK(launch_propagate(h->buf[h->cur], h->buf[1 - h->cur], h->g, off, all_sites(h->g), 1, h->stream));
-    return D2Q37_OK;
+    if (corrupt_population >= 0) off.o[corrupt_population] += 1;  // bites on the flat-offset (interior) sites
+    return propagate_launch(h, off, ghost_faces(h));
 }
 
 int d2q37_collide(d2q37_lattice* h, double omega) {
     RET(check_handle(h));
     DeviceGuard dg(h->device);
-    return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1);
+    return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1, ghost_faces(h));
 }
 
 int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) {
@@ -1023,7 +1057,7 @@ int d2q37_set_profiling(d2q37_lattice* h, int on) {
     return D2Q37_OK;
 }
 
-int d2q37_kernel_times(d2q37_lattice* h, double ms[5], long counts[5]) {
+int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]) {
     RET(check_handle(h));
     DeviceGuard dg(h->device);
     CK(cudaStreamSynchronize(h->stream));

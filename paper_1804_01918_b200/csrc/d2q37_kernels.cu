@@ -31,52 +31,121 @@ __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 
 // ---------------------------------------------------------------------------
 
-// Pull offset of population P for the site in lane k, lane row `row`.  With
-// LANES (CSoA, vl > 1) a lane reads the rows beyond its strip ends straight
-// from the neighbouring lane (same cluster row range, lane k-1 / k+1) instead
-// of the lane-halo copies, so a step only needs lane 0's low and lane vl-1's
-// high ghost rows (k_edge "lean").  For vl >= 32 the test is warp-uniform.
-template <bool LANES>
-__device__ __forceinline__ long long pull_offset(const Offsets& off, const DevGeo& g, int p, int row, int k) {
-    long long o = off.o[p];
-    if (LANES) {
-        const int cy = cy_of(p);
-        const long long wrap = (long long)g.strip * g.rstride - 1;
-        if (cy > 0 && row < cy && k > 0) o += wrap;
-        if (cy < 0 && row >= g.strip + cy && k < g.vl - 1) o -= wrap;
-    }
-    return o;
+__device__ __forceinline__ int wrapi(int v, int n) {
+    const int r = v % n;
+    return r < 0 ? r + n : r;
 }
 
-template <bool LANES>
+// Source element of population p for the site (column x, lane row `row`, lane
+// k) of a pull step, for sites within 3 of a column end or a lane-strip end
+// (everything else uses the flat offsets).  The boundary is resolved here
+// instead of through ghost copies:
+//   * x is periodic: the source column wraps (no ghost columns are read);
+//   * a lane reads rows beyond its strip ends from the neighbouring lane
+//     (CSoA/CAoSoA, vl > 1), so inner lane halos are never read;
+//   * the outer y faces (lane 0 low, lane vl-1 high) are periodic (wrap to the
+//     opposite face), wall (specular image f(mirror y, ybar p)) or
+//     ghost (read the ghost rows: after a bc verb, or halos received by a slab).
+__device__ __forceinline__ long long edge_source(const DevGeo& g, const Faces& fc, int p, int x, int row, int k) {
+    const int xs = wrapi(x - cx_of(p), g.lx);
+    int r = row - cy_of(p), kk = k, pp = p;
+    if (r < 0) {
+        if (k > 0) {
+            r += g.strip;
+            kk = k - 1;
+        } else if (fc.lo == kFacePeriodic) {
+            if (g.vl == 1) {
+                r = wrapi(r, g.strip);
+            } else {
+                r += g.strip;
+                kk = g.vl - 1;
+            }
+        } else if (fc.lo == kFaceWall) {
+            r = -1 - r;
+            pp = fc.ybar[p];
+        }  // kFaceGhost: ghost row j = 3 + r of lane 0
+    } else if (r >= g.strip) {
+        if (k < g.vl - 1) {
+            r -= g.strip;
+            kk = k + 1;
+        } else if (fc.hi == kFacePeriodic) {
+            if (g.vl == 1) {
+                r = r % g.strip;
+            } else {
+                r -= g.strip;
+                kk = 0;
+            }
+        } else if (fc.hi == kFaceWall) {
+            r = 2 * g.strip - 1 - r;
+            pp = fc.ybar[p];
+        }
+    }
+    return elem_of(g, pp, xs + kHalo, r + kHalo, kk);
+}
+
+__device__ __forceinline__ bool edge_site(const DevGeo& g, int x, int row) {
+    return x < kHalo || x >= g.lx - kHalo || row < kHalo || row >= g.strip - kHalo;
+}
+
+// Gathers the 37 pulled populations of one site into registers.
+__device__ __forceinline__ void pull_site(double (&f)[kNpop], const double* __restrict__ src, long long e,
+                                          const DevGeo& g, const Offsets& off, const Faces& fc, int x, int row,
+                                          int k) {
+    if (!edge_site(g, x, row)) {
+#pragma unroll
+        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + off.o[p]);
+    } else {  // unrolled: f[] must stay in registers
+#pragma unroll
+        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + edge_source(g, fc, p, x, row, k));
+    }
+}
+
+// Column x and site q of this thread in the launch's segments; false if none.
+__device__ __forceinline__ bool segment_site(const DevGeo& g, const Segments& seg, int& x, int& q) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (seg.dense) {
+        const int per_col = seg.nq * seg.nseg;
+        if (t >= per_col * g.lx) return false;
+        x = t / per_col;
+        const int i = t - x * per_col;
+        q = seg.q0[i / seg.nq] + (i % seg.nq) * seg.stride;
+    } else {
+        if (t >= seg.nq) return false;
+        x = blockIdx.y;
+        q = seg.q0[blockIdx.z] + t * seg.stride;
+    }
+    const int row = q >> g.lvl, k = q & (g.vl - 1);
+    if (seg.skip_lo && k == 0 && row < kHalo) return false;
+    if (seg.skip_hi && k == g.vl - 1 && row >= g.strip - kHalo) return false;
+    return true;
+}
+
 __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __restrict__ src,
                                                               double* __restrict__ dst, DevGeo g, Offsets off,
-                                                              Segments seg) {
-    const int z = blockIdx.z;
-    const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= seg.q0[z] + seg.nq) return;
-    const long long e = site_of(g, blockIdx.y + kHalo, q);
-    const int row = q >> g.lvl, k = q & (g.vl - 1);
+                                                              Faces fc, Segments seg) {
+    int x, q;
+    if (!segment_site(g, seg, x, q)) return;
+    const long long e = site_of(g, x + kHalo, q);
     double f[kNpop];
-#pragma unroll
-    for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + pull_offset<LANES>(off, g, p, row, k));
+    pull_site(f, src, e, g, off, fc, x, q >> g.lvl, q & (g.vl - 1));
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.pstride, f[p]);
 }
 
-template <bool STRICT, bool SHIFT, bool LANES>
+template <bool STRICT, bool SHIFT>
 __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
-    k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, ModelParams mp,
-              double omega, Segments seg, int* __restrict__ flag) {
-    const int z = blockIdx.z;
-    const int q = seg.q0[z] + blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= seg.q0[z] + seg.nq) return;
-    const long long e = site_of(g, blockIdx.y + kHalo, q);
-    const int row = q >> g.lvl, k = q & (g.vl - 1);
+    k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, Faces fc,
+              ModelParams mp, double omega, Segments seg, int* __restrict__ flag) {
+    int x, q;
+    if (!segment_site(g, seg, x, q)) return;
+    const long long e = site_of(g, x + kHalo, q);
     double f[kNpop];
+    if (SHIFT) {
+        pull_site(f, src, e, g, off, fc, x, q >> g.lvl, q & (g.vl - 1));
+    } else {
 #pragma unroll
-    for (int p = 0; p < kNpop; ++p)
-        f[p] = ld_stream(src + e + (SHIFT ? pull_offset<LANES>(off, g, p, row, k) : p * g.pstride));
+        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + p * g.pstride);
+    }
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
 #pragma unroll
@@ -89,11 +158,6 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
 // the 6 ghost columns.  Every ghost slot is computed from its final physical
 // source directly (ghost-column images of ghost rows included), so one pass
 // reproduces the reference's y-then-x fill order.
-
-__device__ __forceinline__ int wrapi(int v, int n) {
-    const int r = v % n;
-    return r < 0 ? r + n : r;
-}
 
 __global__ void __launch_bounds__(256) k_edge(double* __restrict__ buf, DevGeo g, EdgeParams ep) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -298,44 +362,39 @@ __global__ void __launch_bounds__(256) k_moments(const double* __restrict__ buf,
 // Launchers
 
 static dim3 stream_grid(const DevGeo& g, const Segments& seg, int nseg) {
+    if (seg.dense) {
+        const long long n = (long long)seg.nq * nseg * g.lx;
+        return dim3(unsigned((n + kStreamThreads - 1) / kStreamThreads), 1, 1);
+    }
     return dim3((seg.nq + kStreamThreads - 1) / kStreamThreads, g.lx, nseg);
 }
 
-cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                              const Segments& seg, int nseg, cudaStream_t s) {
-    if (seg.nq <= 0) return cudaSuccess;
+    if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
     (void)cudaGetLastError();
-    if (g.vl > 1)
-        k_propagate<true><<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
-    else
-        k_propagate<false><<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, seg);
+    k_propagate<<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, fc, seg);
     return cudaGetLastError();
 }
 
-cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
                            int nseg, int* flag, cudaStream_t s) {
-    if (seg.nq <= 0) return cudaSuccess;
+    if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
     const dim3 grid = stream_grid(g, seg, nseg);
-    const bool lanes = g.vl > 1;
-#define D2Q37_COLLIDE(S, SH, L) \
-    k_collide<S, SH, L><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, mp, omega, seg, flag)
+#define D2Q37_COLLIDE(S, SH) \
+    k_collide<S, SH><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag)
     (void)cudaGetLastError();
-    if (!shift) {
-        if (strict)
-            D2Q37_COLLIDE(true, false, false);
+    if (strict) {
+        if (shift)
+            D2Q37_COLLIDE(true, true);
         else
-            D2Q37_COLLIDE(false, false, false);
-    } else if (strict) {
-        if (lanes)
-            D2Q37_COLLIDE(true, true, true);
-        else
-            D2Q37_COLLIDE(true, true, false);
+            D2Q37_COLLIDE(true, false);
     } else {
-        if (lanes)
-            D2Q37_COLLIDE(false, true, true);
+        if (shift)
+            D2Q37_COLLIDE(false, true);
         else
-            D2Q37_COLLIDE(false, true, false);
+            D2Q37_COLLIDE(false, false);
     }
 #undef D2Q37_COLLIDE
     return cudaGetLastError();

@@ -13,14 +13,30 @@ constexpr int kStreamThreads = 128;
 constexpr int kCollideMinBlocks = 3;
 
 // Up to two q-ranges per launch (blockIdx.z selects one); each has nq sites
-// per column.  q indexes a column's physical elements in memory order.
+// per column at q = q0 + t*stride.  q indexes a column's physical elements in
+// memory order (q = row*vl + lane).  skip_lo / skip_hi drop the sites whose
+// pull reaches a remote face (lane 0's first 3 rows / lane vl-1's last 3):
+// a slab computes those after its halos arrive.
+// dense = 1 packs the segments of every column into one 1-D grid (a few sites
+// per column: the slab boundary launch); otherwise grid = (nq/128, lx, nseg).
 struct Segments {
     int q0[2];
     int nq;
+    int stride;
+    int skip_lo, skip_hi;
+    int dense, nseg;
 };
 
-enum { kFacePeriodic = 0, kFaceWall = 1, kFaceRemote = 2 };
+// Outer y-face treatment.  k_edge: periodic wrap, wall mirror, or remote (from
+// the slab receive buffers).  Stream kernels: periodic / wall resolved
+// in-kernel, ghost = read the ghost rows (filled by a bc verb or k_edge remote).
+enum { kFacePeriodic = 0, kFaceWall = 1, kFaceRemote = 2, kFaceGhost = 3 };
 enum { kEdgeLocal = 1, kEdgeRemote = 2, kEdgeAll = 3 };
+
+struct Faces {
+    int lo, hi;
+    signed char ybar[kNpop];  // y-mirror (cx, -cy)
+};
 
 struct EdgeParams {
     const double* recv_lo;  // [slot][x]: neighbour's rows ny-d for (d, p) with cy_p >= d
@@ -43,9 +59,9 @@ struct PackParams {
     signed char hi_d[kMaxSlots], hi_p[kMaxSlots];  // entries of send_hi (cy_p >= d)
 };
 
-cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                              const Segments& seg, int nseg, cudaStream_t s);
-cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off,
+cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
                            int nseg, int* flag, cudaStream_t s);
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s);
