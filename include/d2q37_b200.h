@@ -160,6 +160,14 @@ int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* pa
 /* Device-side D2Q37_INIT_PHILOX straight into one buffer (bit-identical to the host one). */
 int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed);
 
+/* save_dump / load_dump (dump.hpp:31-34, dump.cpp:44-70) of the state buffer:
+ * "LBDUMP01", u64 lx, ly, npop, then the canonical values as little-endian
+ * f64, streamed plane by plane through two 64 MB pinned chunks (no full host
+ * copy of the lattice).  Errors as the reference: unopenable / short / not a
+ * dump / truncated -> INVALID_ARGUMENT with the reference's message. */
+int d2q37_save_dump(d2q37_lattice* h, const char* path);
+int d2q37_load_dump(d2q37_lattice* h, const char* path);
+
 /* Device-side config-0/3/4 RT init of the state buffer: the D2Q37_INIT_RT
  * formulas with the per-site noise drawn from Philox (key = seed, counter = the
  * global site index x*ly + y) instead of the sequential mt19937_64 stream, so

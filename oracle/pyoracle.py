@@ -127,6 +127,8 @@ def ref() -> C.CDLL:
             "ref_sim_time": (C.c_int, [vp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
             "ref_hardware_concurrency": (C.c_int, []),
+            "ref_save_dump": (C.c_int, [C.c_int, C.c_int, _dp, C.c_char_p]),
+            "ref_load_dump": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.c_void_p, C.c_size_t]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -346,6 +348,22 @@ def ref_oracle_collide(a, omega):
     out = _canon(lx, ly)
     fa, _ = _flat(a)
     _ref_check(ref().ref_oracle_collide(lx, ly, float(omega), fa, out.reshape(-1)))
+    return out
+
+
+def ref_save_dump(a, path):
+    """The reference's save_dump (dump.cpp:44-58)."""
+    _, lx, ly = a.shape
+    fa, _ = _flat(a)
+    _ref_check(ref().ref_save_dump(lx, ly, fa, os.fsencode(path)))
+
+
+def ref_load_dump(path):
+    """The reference's load_dump (dump.cpp:60-70) -> canonical (37, lx, ly)."""
+    dims = (C.c_int * 3)()
+    _ref_check(ref().ref_load_dump(os.fsencode(path), dims, None, 0))
+    out = np.empty((dims[2], dims[0], dims[1]))
+    _ref_check(ref().ref_load_dump(os.fsencode(path), dims, out.ctypes.data, out.size))
     return out
 
 

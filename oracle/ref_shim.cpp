@@ -280,4 +280,23 @@ int ref_sim_time(void* h, int kernel, double omega, int iterations, int warmup, 
 
 int ref_hardware_concurrency() { return int(std::thread::hardware_concurrency()); }
 
+// dump.cpp:44-70 (LBDUMP01 files)
+int ref_save_dump(int lx, int ly, const double* canon, const char* path) {
+    return guard([&] { save_dump(path, canon_from(lx, ly, canon)); });
+}
+
+// dims: {lx, ly, npop}; out may be null to query the dims only.
+int ref_load_dump(const char* path, int* dims, double* out, std::size_t n) {
+    return guard([&] {
+        const CanonicalLattice c = load_dump(path);
+        dims[0] = c.lx;
+        dims[1] = c.ly;
+        dims[2] = c.npop;
+        if (out) {
+            if (n != c.values.size()) throw std::invalid_argument("ref_load_dump: buffer size mismatch");
+            std::memcpy(out, c.values.data(), n * sizeof(double));
+        }
+    });
+}
+
 }  // extern "C"

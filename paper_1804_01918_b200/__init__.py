@@ -122,6 +122,8 @@ def _load():
         "d2q37_make_lattice": (i, [i, i, i, C.c_uint64, vp, P(_Model), vp, sz, i]),
         "d2q37_fill_philox": (i, [vp, i, C.c_uint64]),
         "d2q37_init_rt_device": (i, [vp, C.c_uint64]),
+        "d2q37_save_dump": (i, [vp, C.c_char_p]),
+        "d2q37_load_dump": (i, [vp, C.c_char_p]),
         "d2q37_nccl_unique_id": (i, [C.c_char_p]),
         "d2q37_create_slab": (i, [i, i, i, i, i, i, i, C.c_char_p, P(vp)]),
         "d2q37_create_group": (i, [i, i, i, i, i, i, P(vp)]),
@@ -452,6 +454,14 @@ class Simulation:
 
     def init_philox(self, seed: int, which: int = 0):
         _check(_load().d2q37_fill_philox(self._h, which, seed))
+
+    def save_dump(self, path: str):
+        """save_dump (dump.cpp:44-58): LBDUMP01 file of the state, streamed from the device."""
+        _check(_load().d2q37_save_dump(self._h, os.fsencode(path)))
+
+    def load_dump(self, path: str):
+        """load_dump + LatticeState::load (dump.cpp:60-70), streamed to the device."""
+        _check(_load().d2q37_load_dump(self._h, os.fsencode(path)))
 
     def init_rt_device(self, seed: int):
         """Config-0/3/4 RT init generated on the device (Philox noise by global site)."""

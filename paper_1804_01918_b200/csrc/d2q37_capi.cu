@@ -966,6 +966,123 @@ int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed) {
     return D2Q37_OK;
 }
 
+// ---- LBDUMP01 snapshots streamed from / to device memory (dump.cpp:44-70) ----
+
+namespace {
+
+constexpr char kDumpMagic[8] = {'L', 'B', 'D', 'U', 'M', 'P', '0', '1'};
+constexpr size_t kDumpChunk = size_t(1) << 23;  // doubles per pinned staging chunk (64 MB)
+
+struct FileCloser {
+    void operator()(std::FILE* f) const {
+        if (f) std::fclose(f);
+    }
+};
+
+// Two pinned chunks so file I/O of one overlaps the copy of the other.
+struct PinnedPair {
+    double* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~PinnedPair() {
+        for (int i = 0; i < 2; ++i) {
+            if (buf[i]) cudaFreeHost(buf[i]);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+    }
+    int init(size_t n) {
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaMallocHost(&buf[i], n * sizeof(double)));
+            CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+        return D2Q37_OK;
+    }
+};
+
+}  // namespace
+
+int d2q37_save_dump(d2q37_lattice* h, const char* path) {
+    RET(check_handle(h));
+    if (!path) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null path");
+    DeviceGuard dg(h->device);
+    std::unique_ptr<std::FILE, FileCloser> f(std::fopen(path, "wb"));
+    if (!f) return fail(D2Q37_ERR_INVALID_ARGUMENT, "cannot open dump file for writing: %s", path);
+    const DevGeo& g = h->g;
+    const uint64_t dims[3] = {uint64_t(g.lx), uint64_t(g.ly), uint64_t(kNpop)};
+    if (std::fwrite(kDumpMagic, 1, 8, f.get()) != 8 || std::fwrite(dims, 8, 3, f.get()) != 3)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "short write to dump file: %s", path);
+    const size_t plane = size_t(g.lx) * g.ly;
+    if (!h->stage) CK(cudaMalloc(&h->stage, plane * sizeof(double)));
+    PinnedPair pin;
+    const size_t chunk = std::min(plane, kDumpChunk);
+    RET(pin.init(chunk));
+    CK(cudaStreamSynchronize(h->stream));
+    int slot = 0;
+    bool pending[2] = {false, false};
+    size_t pending_n[2] = {0, 0};
+    auto drain = [&](int s) -> int {
+        if (!pending[s]) return D2Q37_OK;
+        CK(cudaEventSynchronize(pin.ev[s]));
+        if (std::fwrite(pin.buf[s], sizeof(double), pending_n[s], f.get()) != pending_n[s])
+            return fail(D2Q37_ERR_INVALID_ARGUMENT, "short write to dump file: %s", path);
+        pending[s] = false;
+        return D2Q37_OK;
+    };
+    for (int p = 0; p < kNpop; ++p) {
+        CK(launch_gather(h->buf[h->cur], g, h->stage, p, h->stream));
+        for (size_t off = 0; off < plane; off += chunk) {
+            const size_t n = std::min(chunk, plane - off);
+            RET(drain(slot));  // the chunk we are about to overwrite is on disk
+            CK(cudaMemcpyAsync(pin.buf[slot], h->stage + off, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaEventRecord(pin.ev[slot], h->stream));
+            pending[slot] = true;
+            pending_n[slot] = n;
+            slot ^= 1;
+        }
+    }
+    RET(drain(slot));
+    RET(drain(slot ^ 1));
+    return D2Q37_OK;
+}
+
+int d2q37_load_dump(d2q37_lattice* h, const char* path) {
+    RET(check_handle(h));
+    if (!path) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null path");
+    DeviceGuard dg(h->device);
+    std::unique_ptr<std::FILE, FileCloser> f(std::fopen(path, "rb"));
+    if (!f) return fail(D2Q37_ERR_INVALID_ARGUMENT, "cannot open dump file: %s", path);
+    char magic[8];
+    uint64_t dims[3];
+    if (std::fread(magic, 1, 8, f.get()) != 8 || std::fread(dims, 8, 3, f.get()) != 3 ||
+        std::memcmp(magic, kDumpMagic, 8) != 0)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "not a lattice dump: %s", path);
+    const DevGeo& g = h->g;
+    if (dims[0] != uint64_t(g.lx) || dims[1] != uint64_t(g.ly) || dims[2] != uint64_t(kNpop))
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "from_canonical: dimension mismatch (dump %llu x %llu x %llu)",
+                    (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2]);
+    const size_t plane = size_t(g.lx) * g.ly;
+    if (!h->stage) CK(cudaMalloc(&h->stage, plane * sizeof(double)));
+    PinnedPair pin;
+    const size_t chunk = std::min(plane, kDumpChunk);
+    RET(pin.init(chunk));
+    CK(cudaStreamSynchronize(h->stream));
+    double* dst = h->buf[h->cur];
+    int slot = 0;
+    for (int p = 0; p < kNpop; ++p) {
+        for (size_t off = 0; off < plane; off += chunk) {
+            const size_t n = std::min(chunk, plane - off);
+            CK(cudaEventSynchronize(pin.ev[slot]));  // previous copy out of this chunk finished
+            if (std::fread(pin.buf[slot], sizeof(double), n, f.get()) != n)
+                return fail(D2Q37_ERR_INVALID_ARGUMENT, "truncated dump file: %s", path);
+            CK(cudaMemcpyAsync(h->stage + off, pin.buf[slot], n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaEventRecord(pin.ev[slot], h->stream));
+            slot ^= 1;
+        }
+        CK(launch_scatter(dst, g, h->stage, p, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return D2Q37_OK;
+}
+
 // ---- multi-GPU ------------------------------------------------------------
 
 int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]) {

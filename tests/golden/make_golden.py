@@ -61,6 +61,8 @@ def main():
     model()
     lattice_case(16, 32, 2024, "ref_random_16x32")
     lattice_case(5, 12, 606, "ref_random_5x12", steps=5, omega_step=1.3, vl_csoa=4)  # strip == halo
+    # an LBDUMP01 file written by the reference's save_dump (dump.cpp:44-58)
+    po.ref_save_dump(po.ref_random_lattice(5, 12, 606), os.path.join(HERE, "ref_dump_5x12.lbd"))
     print("golden fixtures written to", HERE)
 
 

@@ -355,6 +355,54 @@ def test_step_no_nan_1000_steps(gpu, lbm):
 
 # --------------------------------------------------------------------------- full BASELINE sizes
 
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("caosoa", 4), ("aos", 1)])
+def test_lbdump01_save_load_reference_format(gpu, lbm, layout, vl, tmp_path):
+    """save_dump / load_dump (dump.cpp:44-70): byte-identical files to the reference's writer,
+    and a file written by the reference itself loads bit-exactly."""
+    import os
+    from conftest import GOLDEN
+    from oracle import pyoracle as po
+    g = golden("ref_random_5x12.npz")
+    s = sim_of(lbm, layout, 5, 12, vl)
+    s.load_dump(os.path.join(GOLDEN, "ref_dump_5x12.lbd"))
+    assert np.array_equal(s.dump(), g["init"])
+    path = str(tmp_path / "gpu.lbd")
+    s.save_dump(path)
+    assert open(path, "rb").read() == open(os.path.join(GOLDEN, "ref_dump_5x12.lbd"), "rb").read()
+    if po.ref_available():
+        assert np.array_equal(po.ref_load_dump(path), g["init"])
+
+
+def test_lbdump01_errors(gpu, lbm, tmp_path):
+    s = sim_of(lbm, "soa", 5, 12)
+    bad = tmp_path / "bad.lbd"
+    bad.write_bytes(b"NOTADUMP" + bytes(24))
+    with pytest.raises(ValueError, match="not a lattice dump"):
+        s.load_dump(str(bad))
+    other = sim_of(lbm, "soa", 6, 12)
+    other.save_dump(str(tmp_path / "other.lbd"))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        s.load_dump(str(tmp_path / "other.lbd"))
+    trunc = tmp_path / "trunc.lbd"
+    trunc.write_bytes((tmp_path / "other.lbd").read_bytes()[:-8])
+    with pytest.raises(ValueError, match="truncated"):
+        other.load_dump(str(trunc))
+    with pytest.raises(ValueError, match="cannot open"):
+        s.save_dump(str(tmp_path / "no" / "such" / "dir.lbd"))
+
+
+@pytest.mark.slow
+def test_lbdump01_streaming_multi_chunk(gpu, lbm, tmp_path):
+    """Config-1 size (8.4 M sites per plane > one 64 MB chunk): streamed save/load round trip."""
+    a = sim_of(lbm, "caosoa", 1024, 8192, 32)
+    a.init_philox(7)
+    path = str(tmp_path / "big.lbd")
+    a.save_dump(path)
+    b = sim_of(lbm, "soa", 1024, 8192)
+    b.load_dump(path)
+    assert np.array_equal(b.dump(), a.dump())
+
+
 @pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 32)])
 def test_device_rt_init_vs_oracle(gpu, lbm, po, layout, vl):
     """init_rt_device == the oracle's Philox-noise RT recipe (<= 1e-14), per slab of a taller lattice."""
