@@ -142,6 +142,23 @@ def time_kernel(sim, body, iterations: int, warmup: int):
     return statistics.median(samples), min(samples), samples
 
 
+def energy_per_iteration(sim, body, provider: NvmlEnergy, t_iter_s: float, window_s: float = 1.0) -> dict:
+    """Joules per call over a window of >= window_s: the NVML energy counter updates
+    every few tens of ms, so the timed iterations alone are too short to read it."""
+    import time
+
+    reps = max(1, int(window_s / max(t_iter_s, 1e-6)))
+    sim.sync()
+    before, t0 = provider.read_mj(), time.perf_counter()
+    for _ in range(reps):
+        body()
+    sim.sync()
+    wall = time.perf_counter() - t0
+    joules = (provider.read_mj() - before) / 1e3 / reps
+    return {"joules_package": joules, "joules_total": joules, "avg_power_w": joules * reps / wall,
+            "window_s": wall, "calls": reps}
+
+
 def run_bench_matrix(lx: int, ly: int, layouts=LAYOUTS, vls=(8,), iterations: int = 50, warmup: int = 5,
                      omega: float = 1.0, energy: bool = False, csv=sys.stdout, log=sys.stderr, device: int = 0):
     """bench_matrix.cpp:34-115 for the device lattice; returns the BenchReports."""
@@ -176,12 +193,9 @@ def run_bench_matrix(lx: int, ly: int, layouts=LAYOUTS, vls=(8,), iterations: in
                     for _ in range(warmup):
                         bodies[r.kernel]()
                     sim.sync()
-                    before = provider.read_mj() if energy_columns else None
                     r.t_iter_s, r.t_min_s, r.samples_s = time_kernel(sim, bodies[r.kernel], iterations, 0)
                     if energy_columns:
-                        joules = (provider.read_mj() - before) / 1e3 / iterations
-                        r.energy = {"joules_package": joules, "joules_total": joules,
-                                    "avg_power_w": joules / r.t_iter_s if r.t_iter_s > 0 else 0.0}
+                        r.energy = energy_per_iteration(sim, bodies[r.kernel], provider, r.t_iter_s)
                     finalize_metrics(r)
                 except Exception as e:
                     r.status = f"error: {e}"
