@@ -1,0 +1,231 @@
+// parity_main.cpp -- C++ drop-in parity program (TEST INFRASTRUCTURE).
+//
+// Links the UNMODIFIED reference library (oracle/_ref/liblbmref.so, built from
+// /root/reference/proj/src by oracle/Makefile) and drives the B200 path through
+// the reference-shaped C++ API (include/lbm_b200/lbm_b200.hpp), criterion by
+// criterion like the reference's own acceptance suite (proj/tests/
+// acceptance.cpp): one PASS/FAIL line each, exit status = number of failures.
+//
+//   G1  model constants: device model == VelocityModel::d2q37()      (C1, C2)
+//   G2  halo_exchange + propagate bitwise == oracle_propagate, 4 layouts x vl (C3)
+//   G3  collide <= 1e-12 vs oracle_collide with the reference's own table;
+//       100 steps conserve mass, momentum, energy to 1e-11               (C4)
+//   G4  identical dumps after 10 steps across the four layouts          (C5)
+//   G5  10 steps <= 1e-12 vs the reference lbm::step                     (validation.cpp)
+//   G6  metric formulas reproduce Table 1                                (C6)
+//   G7  errors: invalid geometry -> std::invalid_argument,
+//       rho <= 0 -> NonPhysicalError                                     (test_kernels.cpp:424-433)
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#define private public  // read the reference's Hermite table (model.hpp:97), test-only
+#include "lbm/model.hpp"
+#undef private
+#include "lbm/kernels.hpp"
+#include "lbm/lattice.hpp"
+#include "lbm/validation.hpp"
+#include "lbm_b200/lbm_b200.hpp"
+
+namespace {
+
+using B = lbm_b200::LayoutKind;
+const std::array<B, 4> kLayouts = {B::AoS, B::SoA, B::CSoA, B::CAoSoA};
+
+lbm_b200::CanonicalLattice to_gpu(const lbm::CanonicalLattice& c) {
+    lbm_b200::CanonicalLattice g = lbm_b200::make_canonical(c.lx, c.ly);
+    g.values = c.values;
+    return g;
+}
+
+lbm::CanonicalLattice oracle_run(const lbm::CanonicalLattice& init, const std::function<void(lbm::OracleLattice&, lbm::OracleLattice&)>& f) {
+    lbm::OracleLattice a(init.lx, init.ly), b(init.lx, init.ly);
+    lbm::oracle_from_canonical(init, a);
+    f(a, b);
+    return lbm::oracle_to_canonical(b);
+}
+
+double max_rel(const std::vector<double>& got, const std::vector<double>& want) {
+    double m = 0.0;
+    for (size_t i = 0; i < want.size(); ++i) m = std::max(m, std::abs(got[i] - want[i]) / std::abs(want[i]));
+    return m;
+}
+
+// The reference model's own constants (the device gets the table
+// of the binary it is compared with).
+lbm_b200::VelocityModel reference_model() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    d2q37_model raw{};
+    for (int i = 0; i < 37; ++i) {
+        raw.cx[i] = m.velocities()[i].x;
+        raw.cy[i] = m.velocities()[i].y;
+        raw.w[i] = m.weights()[i];
+        for (int k = 0; k < 14; ++k) raw.eq[i * 14 + k] = m.eq_table_[i][k];
+    }
+    raw.t0 = m.t0();
+    return lbm_b200::VelocityModel::from_raw(raw);
+}
+
+bool g1() {
+    const lbm::VelocityModel& r = lbm::VelocityModel::d2q37();
+    const lbm_b200::VelocityModel& d = lbm_b200::VelocityModel::d2q37();
+    if (d.t0() != r.t0()) return false;
+    for (int i = 0; i < 37; ++i) {
+        if (d.velocity(i).x != r.velocities()[i].x || d.velocity(i).y != r.velocities()[i].y) return false;
+        // the reference build contracts into FMA: weights agree to a few ulp
+        if (std::abs(d.weight(i) - r.weights()[i]) > 1e-14 * r.weights()[i]) return false;
+    }
+    return true;
+}
+
+bool g2() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    for (const auto& [lx, ly] : {std::pair{16, 32}, std::pair{64, 128}}) {
+        const lbm::CanonicalLattice init = lbm::make_random_lattice(lx, ly, 1001 + lx);
+        const lbm::CanonicalLattice want =
+            oracle_run(init, [&](auto& a, auto& b) { lbm::oracle_propagate(a, b, m.velocities()); });
+        for (const B kind : kLayouts)
+            for (const int vl : {1, 2, 4, 8}) {
+                lbm_b200::LatticeState s(kind, lbm_b200::Geometry{lx, ly, 3, 3, vl});
+                s.load(to_gpu(init));
+                lbm_b200::halo_exchange(s);
+                lbm_b200::propagate(s);
+                if (s.dump_from(1).values != want.values) return false;
+            }
+    }
+    return true;
+}
+
+bool g3() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm_b200::VelocityModel dm = reference_model();
+    const int lx = 64, ly = 128;
+    const double omega = 1.3;
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(lx, ly, 2002);
+    const lbm::CanonicalLattice want =
+        oracle_run(init, [&](auto& a, auto& b) { lbm::oracle_collide(a, b, m, omega); });
+    for (const B kind : kLayouts) {
+        lbm_b200::LatticeState s(kind, lbm_b200::Geometry{lx, ly, 3, 3, 4});
+        s.load_into(1, to_gpu(init));
+        lbm_b200::collide(s, dm, omega);
+        if (!(max_rel(s.dump().values, want.values) <= 1e-12)) return false;
+    }
+    auto totals = [&](const lbm_b200::CanonicalLattice& c) {
+        std::array<double, 4> t{};
+        for (int p = 0; p < 37; ++p)
+            for (int x = 0; x < c.lx; ++x)
+                for (int y = 0; y < c.ly; ++y) {
+                    const double f = c.at(x, y, p);
+                    const auto v = m.velocities()[p];
+                    t[0] += f;
+                    t[1] += v.x * f;
+                    t[2] += v.y * f;
+                    t[3] += (v.x * v.x + v.y * v.y) * f;
+                }
+        return t;
+    };
+    lbm_b200::LatticeState s(B::CAoSoA, lbm_b200::Geometry{lx, ly, 3, 3, 4});
+    s.load(to_gpu(init));
+    const auto t0 = totals(s.dump());
+    for (int n = 0; n < 100; ++n) {
+        lbm_b200::step(s, dm, omega);
+        const auto t = totals(s.dump());
+        if (!(std::abs(t[0] - t0[0]) / t0[0] < 1e-11)) return false;
+        if (!(std::abs(t[1] - t0[1]) / t0[0] < 1e-11)) return false;
+        if (!(std::abs(t[2] - t0[2]) / t0[0] < 1e-11)) return false;
+        if (!(std::abs(t[3] - t0[3]) / t0[3] < 1e-11)) return false;
+    }
+    return true;
+}
+
+bool g4() {
+    const lbm_b200::VelocityModel& m = lbm_b200::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(64, 128, 3003);
+    std::vector<double> reference;
+    for (const B kind : kLayouts)
+        for (const auto variant : {lbm_b200::StepVariant::Fused, lbm_b200::StepVariant::Unfused}) {
+            lbm_b200::LatticeState s(kind, lbm_b200::Geometry{64, 128, 3, 3, 4});
+            s.load(to_gpu(init));
+            lbm_b200::step(s, m, 1.1, 10, variant);
+            const auto out = s.dump();
+            if (reference.empty())
+                reference = out.values;
+            else if (out.values != reference)
+                return false;
+        }
+    return true;
+}
+
+bool g5() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(32, 64, 88);
+    lbm::LatticeState ref{lbm::Descriptor(lbm::LayoutKind::CSoA, [] {
+        lbm::Geometry g{32, 64};
+        g.vl = 4;
+        return g;
+    }())};
+    ref.load(init);
+    lbm::ThreadPool pool(4);
+    for (int n = 0; n < 10; ++n) lbm::step(ref, m, 0.9, pool);
+    lbm_b200::LatticeState s(B::CAoSoA, lbm_b200::Geometry{32, 64, 3, 3, 32});
+    s.load(to_gpu(init));
+    lbm_b200::step(s, reference_model(), 0.9, 10);
+    return s.time_step() == ref.time_step && max_rel(s.dump().values, ref.dump().values) <= 1e-12;
+}
+
+bool g6() {
+    auto within = [](double got, double want, double tol) { return std::abs(got - want) / want <= tol; };
+    return within(lbm_b200::propagate_gbps(1024, 8192, 37, 0.0125), 398.0, 0.01) &&
+           within(lbm_b200::collide_gflops(1024, 8192, 6600.0, 0.0503), 1100.0, 0.01) &&
+           within(lbm_b200::mlups(1024, 8192, 0.0503), 166.0, 0.01) &&
+           within(lbm_b200::mlups(4608, 12288, 0.55025), 103.0, 0.01);
+}
+
+bool g7() {
+    try {
+        lbm_b200::LatticeState bad(B::CSoA, lbm_b200::Geometry{8, 16, 3, 3, 8});  // strip 2 < halo
+        return false;
+    } catch (const std::invalid_argument&) {
+    }
+    lbm_b200::LatticeState s(B::SoA, lbm_b200::Geometry{8, 16, 3, 3, 1});
+    lbm_b200::CanonicalLattice neg = lbm_b200::make_canonical(8, 16);
+    for (double& v : neg.values) v = -1.0;
+    s.load_into(1, neg);
+    try {
+        lbm_b200::collide(s, lbm_b200::VelocityModel::d2q37(), 1.0);
+        return false;
+    } catch (const lbm_b200::NonPhysicalError&) {
+    }
+    return true;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const std::array<std::pair<const char*, bool (*)()>, 7> all = {{{"G1", g1},
+                                                                     {"G2", g2},
+                                                                     {"G3", g3},
+                                                                     {"G4", g4},
+                                                                     {"G5", g5},
+                                                                     {"G6", g6},
+                                                                     {"G7", g7}}};
+    int failures = 0;
+    for (const auto& [name, fn] : all) {
+        if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;
+        bool ok = false;
+        try {
+            ok = fn();
+        } catch (const std::exception& e) {
+            std::printf("%s exception: %s\n", name, e.what());
+        }
+        std::printf("%s %s\n", name, ok ? "PASS" : "FAIL");
+        failures += ok ? 0 : 1;
+    }
+    return failures;
+}
