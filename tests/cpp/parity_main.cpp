@@ -173,7 +173,7 @@ bool g5() {
     ref.load(init);
     lbm::ThreadPool pool(4);
     for (int n = 0; n < 10; ++n) lbm::step(ref, m, 0.9, pool);
-    lbm_b200::LatticeState s(B::CAoSoA, lbm_b200::Geometry{32, 64, 3, 3, 32});
+    lbm_b200::LatticeState s(B::CAoSoA, lbm_b200::Geometry{32, 64, 3, 3, 16});
     s.load(to_gpu(init));
     lbm_b200::step(s, reference_model(), 0.9, 10);
     return s.time_step() == ref.time_step && max_rel(s.dump().values, ref.dump().values) <= 1e-12;
