@@ -448,6 +448,23 @@ def test_config2_full_size_collide(gpu, lbm, po):
 
 
 @pytest.mark.slow
+def test_config3_full_size_one_step_vs_oracle(gpu, lbm, po):
+    """Config 3 at full size (4096 x 16384, 67 M sites): one fused CAoSoA32 wall step (the bench
+    step) within 1e-12 of the oracle's step on every population of every site."""
+    lx, ly = 4096, 16384
+    init = lbm.make_lattice("rt", lx, ly, seed=12345)
+    s = sim_of(lbm, "caosoa", lx, ly, 32, bc="wall")
+    s.load(init)
+    s.step(0.8, 1)
+    got = s.dump()
+    s.close()
+    want, bad = po.orc_step(init, 0.8, 1, po.BC_WALL)
+    assert not bad
+    del init
+    assert max_rel(got, want) <= 1e-12
+
+
+@pytest.mark.slow
 def test_config3_size_conservation(gpu, lbm):
     """4096x16384 RT, wall, 20 fused steps: mass / energy conserved, momentum stays ~0 (size-independent)."""
     s = sim_of(lbm, "soa", 4096, 16384, bc="wall")
