@@ -63,6 +63,10 @@ struct d2q37_lattice {
     double* recv_hi = nullptr;
     void* comm = nullptr;
     cudaStream_t comm_stream = nullptr;
+    // NCCL slabs: pack / unpack / boundary sites run on a high-priority stream
+    // concurrently with the interior kernel (disjoint sites), joined per step.
+    cudaStream_t halo_stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_bnd = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
     cudaEvent_t ev_int[kEventRing] = {}, ev_wait[kEventRing] = {};
     int ev_count = 0;
@@ -285,6 +289,7 @@ void free_lattice(d2q37_lattice* h) {
     DeviceGuard dg(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+    if (h->halo_stream) cudaStreamSynchronize(h->halo_stream);
     for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->send_lo, h->send_hi, h->recv_lo, h->recv_hi})
         if (p) cudaFree(p);
     if (h->d_flag) cudaFree(h->d_flag);
@@ -303,6 +308,9 @@ void free_lattice(d2q37_lattice* h) {
     if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
     if (h->comm) nccl_comm_destroy(h->comm);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->halo_stream) cudaStreamDestroy(h->halo_stream);
+    if (h->ev_start) cudaEventDestroy(h->ev_start);
+    if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     h->stream_owner.reset();
     (void)cudaGetLastError();  // teardown errors must not leak into later launches
 }
@@ -564,6 +572,47 @@ int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     gr.math = h->math;
     gr.model_gen = h->model_gen;
     gr.stream = h->stream;
+    return D2Q37_OK;
+}
+
+// Launches in scope go to `s` (the kernels and ProfScope use h->stream).
+struct OnStream {
+    d2q37_lattice* h;
+    cudaStream_t saved;
+    OnStream(d2q37_lattice* h_, cudaStream_t s) : h(h_), saved(h_->stream) { h->stream = s; }
+    ~OnStream() { h->stream = saved; }
+};
+
+// One fused slab step with the halo work hidden behind the interior:
+//   compute stream:  interior sites (everything whose pull stays local) ... join
+//   halo stream (high priority): pack -> | wait halos -> remote ghost rows -> boundary sites
+//   comm stream:                          NCCL send/recv
+// The interior and the boundary write disjoint sites of the next buffer; the
+// interior reads no ghost row the halo stream writes.
+int slab_step_overlapped(d2q37_lattice* h, double omega, int bc) {
+    CK(cudaEventRecord(h->ev_start, h->stream));
+    CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
+    {
+        OnStream on(h, h->halo_stream);
+        RET(exchange_begin(h, bc));  // pack on the halo stream, NCCL on the comm stream
+    }
+    RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, interior(h, bc), 1, step_faces(h, bc)));
+    const int ring = h->ev_count % kEventRing;
+    CK(cudaEventRecord(h->ev_int[ring], h->stream));
+    {
+        OnStream on(h, h->halo_stream);
+        RET(exchange_wait(h));
+        RET(edge(h, bc, kEdgeRemote));
+        int nseg = 0;
+        const Segments bnd = boundary(h, bc, &nseg);
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, bnd, nseg, step_faces(h, bc)));
+        CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
+    }
+    CK(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
+    CK(cudaEventRecord(h->ev_wait[ring], h->stream));  // exposed halo: interior done -> boundary done
+    ++h->ev_count;
+    h->cur = 1 - h->cur;
+    ++h->time_step;
     return D2Q37_OK;
 }
 
@@ -885,7 +934,9 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
     }
     for (; s < nsteps; ++s) {
-        if (slab) {
+        if (slab && h->halo_stream && variant == D2Q37_FUSED && can_split(h)) {
+            RET(slab_step_overlapped(h, omega, bc));
+        } else if (slab) {
             RET(exchange_begin(h, bc));
             RET(slab_phase1(h, omega, variant, bc));
             RET(slab_phase2(h, omega, variant, bc));
@@ -908,6 +959,7 @@ int d2q37_sync(d2q37_lattice* h) {
     CK(cudaMemcpyAsync(h->h_flag, h->d_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (h->comm_stream) CK(cudaStreamSynchronize(h->comm_stream));
+    if (h->halo_stream) CK(cudaStreamSynchronize(h->halo_stream));
     if (*h->h_flag) {
         *h->h_flag = 0;
         CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
@@ -1107,8 +1159,16 @@ int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, 
     if (rc != D2Q37_OK) return bail(rc);
     {
         DeviceGuard dg(device);
-        if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+        // Both side streams get the highest priority: NCCL's kernels and the
+        // boundary work must get SMs while the interior kernel is running.
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        if (cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
             return bail(fail(D2Q37_ERR_CUDA, "comm stream creation failed"));
+        if (cudaStreamCreateWithPriority(&h->halo_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess)
+            return bail(fail(D2Q37_ERR_CUDA, "halo stream creation failed"));
         std::string why;
         rc = nccl_comm_init(&h->comm, nranks, id, rank, &why);
         if (rc != D2Q37_OK) return bail(fail(rc, "%s", why.c_str()));
