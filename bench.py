@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 LX, LY_PER_GPU = 4096, 16384
+STRONG_LY = 32768  # BASELINE config 4, strong scaling: 4096 x 32768 in total
 OMEGA = 0.8
 SEED = 12345
 BYTES_PER_SITE = 592  # 37 x 8 B read + 37 x 8 B write (BASELINE north_star)
@@ -367,7 +368,8 @@ def run_b200(args, dist: Dist):
     torch.cuda.set_device(dev)
     hbm_peak, peak_src = peaks()
     n = dist.world
-    ly_local = args.ly
+    # weak (default): 4096 x 16384 per GPU; strong: BASELINE config 4's 4096 x 32768 split over N
+    ly_local = args.ly if args.scaling == "weak" else STRONG_LY // dist.world
     ly_global = ly_local * n
     sites_local = LX * ly_local
     rank = dist.rank
@@ -418,9 +420,9 @@ def run_b200(args, dist: Dist):
         e2e = run_e2e(lbm, sim, args, dist)
 
     line = {"metric": METRIC, "value": value, "unit": "MLUPS", "n_gpus": n, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"c3/c4-weak: {LX}x{ly_local} per GPU (global {LX}x{ly_global}), RT init, "
+            "config": {"workload": f"c3/c4-{args.scaling}: {LX}x{ly_local} per GPU (global {LX}x{ly_global}), RT init, "
                                    f"periodic x, top/bottom specular walls, omega {OMEGA}",
                        "lx": LX, "ly_per_gpu": ly_local, "ly_global": ly_global, "layout": args.layout,
                        "vl": args.vl if args.layout in ("csoa", "caosoa") else 1, "variant": args.variant,
@@ -524,7 +526,9 @@ def main():
     ap.add_argument("--layout", choices=["aos", "soa", "csoa", "caosoa"], default="caosoa")
     ap.add_argument("--vl", type=int, default=32)
     ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
-    ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU")
+    ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU (weak scaling)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: --ly rows per GPU; strong: 4096 x 32768 split over the GPUs (config 4)")
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--e2e-iters", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
