@@ -171,9 +171,11 @@ void fill_offsets(d2q37_lattice* h, int corrupt = -1) {
     const DevGeo& g = h->g;
     for (int p = 0; p < kNpop; ++p) {
         // build_offset_table (kernels.cpp:180-195): pull from (x - cx, y - cy).
-        h->off_pull.o[p] = (long long)p * g.pstride - (long long)cx_of(p) * g.cstride - (long long)cy_of(p) * g.rstride;
+        const int sx = g.tr ? scx<true>(p) : scx<false>(p), sy = g.tr ? scy<true>(p) : scy<false>(p);
+        h->off_pull.o[p] = (long long)p * g.pstride - (long long)sx * g.cstride - (long long)sy * g.rstride;
         if (p == corrupt) h->off_pull.o[p] += 1;
     }
+    finish_offsets(h->off_pull, g.pstride, corrupt < 0);
 }
 
 int upload_model(d2q37_lattice* h, const d2q37_model* m) {
@@ -319,6 +321,14 @@ size_t canon_count(const d2q37_lattice* h) { return size_t(kNpop) * h->g.lx * h-
 
 int check_handle(const d2q37_lattice* h) {
     if (!h) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null lattice handle");
+    return D2Q37_OK;
+}
+
+// The padded-buffer verbs (halo_exchange, propagate-after-halo, Field::data())
+// speak the reference's x-major element order; y-major slab storage has none.
+int padded_verbs_ok(const d2q37_lattice* h, const char* verb) {
+    if (h->g.tr)
+        return fail(D2Q37_ERR_UNSUPPORTED, "%s: not available on y-major slab storage (use step / load / dump)", verb);
     return D2Q37_OK;
 }
 
@@ -478,27 +488,39 @@ Segments boundary(const d2q37_lattice* h, int bc, int* nseg) {
 // Outer-face handling of the pull kernels for a step with boundary `bc`: local
 // faces (periodic wrap, wall) are resolved inside the kernel, faces shared with
 // another slab read the ghost rows k_edge fills from the receive buffers.
+// In y-major storage the y faces are the storage-column faces and the storage
+// rows (lattice x) are periodic.
 Faces step_faces(const d2q37_lattice* h, int bc) {
     Faces fc;
     const int lo = face_lo_of(h, bc), hi = face_hi_of(h, bc);
-    fc.lo = lo == kFaceRemote ? kFaceGhost : lo;
-    fc.hi = hi == kFaceRemote ? kFaceGhost : hi;
+    const int ylo = lo == kFaceRemote ? kFaceGhost : lo;
+    const int yhi = hi == kFaceRemote ? kFaceGhost : hi;
+    if (h->g.tr) {
+        fc.lo = fc.hi = kFacePeriodic;
+        fc.col_lo = ylo;
+        fc.col_hi = yhi;
+    } else {
+        fc.lo = ylo;
+        fc.hi = yhi;
+        fc.col_lo = fc.col_hi = kFacePeriodic;
+    }
     std::memcpy(fc.ybar, h->edge_base.ybar, sizeof fc.ybar);
     return fc;
 }
 
 // The propagate verb reads whatever the preceding bc verb left in the ghost rows
-// (kernels.hpp:33: "Requires halo_exchange(prv) first").
+// (kernels.hpp:33: "Requires halo_exchange(prv) first"); x is always periodic.
 Faces ghost_faces(const d2q37_lattice* h) {
     Faces fc;
     fc.lo = fc.hi = kFaceGhost;
+    fc.col_lo = fc.col_hi = kFacePeriodic;
     std::memcpy(fc.ybar, h->edge_base.ybar, sizeof fc.ybar);
     return fc;
 }
 
 int collide_launch(d2q37_lattice* h, int src, int dst, double omega, bool shift, const Segments& seg, int nseg,
-                   const Faces& fc) {
-    ProfScope ps(h, !shift ? kProfCollide : seg.dense ? kProfBoundary : kProfFused);
+                   const Faces& fc, bool boundary = false) {
+    ProfScope ps(h, !shift ? kProfCollide : (boundary || seg.dense) ? kProfBoundary : kProfFused);
     CK(launch_collide(h->buf[src], h->buf[dst], h->g, h->off_pull, fc, h->mp, omega, h->math == D2Q37_MATH_STRICT,
                       shift, seg, nseg, h->d_flag, h->stream));
     return D2Q37_OK;
@@ -616,6 +638,95 @@ int slab_step_overlapped(d2q37_lattice* h, double omega, int bc) {
     return D2Q37_OK;
 }
 
+// ---- y-major slabs: the slab faces are whole storage columns ---------------
+//
+// A neighbour needs our 3 physical columns next to the shared face; they
+// arrive in our 3 ghost columns.  Both are contiguous runs of the state buffer
+// (site-major layouts keep a column's 37 populations together), so NCCL sends
+// and receives straight from / into the lattice: no pack, no unpack.
+
+double* ycols(d2q37_lattice* h, int X) { return h->buf[h->cur] + h->g.lead + (long long)X * h->g.cstride; }
+size_t ycols_count(const d2q37_lattice* h) { return size_t(kHalo) * size_t(h->g.cstride); }
+
+int ymajor_exchange_nccl(d2q37_lattice* h, int bc) {
+    const int lx = h->g.lx;
+    std::string why;
+    const int rc = nccl_exchange(h->comm, h->comm_stream, ycols(h, kHalo), ycols(h, 0), lo_peer_of(h, bc),
+                                 ycols(h, lx), ycols(h, lx + kHalo), hi_peer_of(h, bc), ycols_count(h), &why);
+    if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+    CK(cudaEventRecord(h->ev_recv, h->comm_stream));
+    return D2Q37_OK;
+}
+
+int ymajor_group_exchange(std::vector<d2q37_lattice*>& slabs, int bc) {
+    for (d2q37_lattice* h : slabs) {
+        const size_t bytes = ycols_count(h) * sizeof(double);
+        const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+        if (lo >= 0)
+            CK(cudaMemcpyAsync(ycols(h, 0), ycols(slabs[lo], slabs[lo]->g.lx), bytes, cudaMemcpyDeviceToDevice,
+                               h->stream));
+        if (hi >= 0)
+            CK(cudaMemcpyAsync(ycols(h, h->g.lx + kHalo), ycols(slabs[hi], kHalo), bytes, cudaMemcpyDeviceToDevice,
+                               h->stream));
+    }
+    return D2Q37_OK;
+}
+
+// Columns whose pull stays inside the slab: all but the 3 next to a remote face.
+Segments ycols_interior(const d2q37_lattice* h, int bc) {
+    Segments s = all_sites(h->g);
+    const bool lo = face_lo_of(h, bc) == kFaceRemote, hi = face_hi_of(h, bc) == kFaceRemote;
+    s.x0[0] = lo ? kHalo : 0;
+    s.nx = h->g.lx - (lo ? kHalo : 0) - (hi ? kHalo : 0);
+    return s;
+}
+
+Segments ycols_boundary(const d2q37_lattice* h, int bc, int* nseg) {
+    Segments s = all_sites(h->g);
+    int n = 0;
+    if (face_lo_of(h, bc) == kFaceRemote) s.x0[n++] = 0;
+    if (face_hi_of(h, bc) == kFaceRemote) s.x0[n++] = h->g.lx - kHalo;
+    s.nx = kHalo;
+    *nseg = n;
+    return s;
+}
+
+// Fused y-major slab step over NCCL: the interior columns on the compute
+// stream while the halo columns travel, the 3 + 3 boundary columns on the
+// high-priority halo stream once they landed.
+int ymajor_step_nccl(d2q37_lattice* h, double omega, int bc) {
+    CK(cudaEventRecord(h->ev_start, h->stream));
+    CK(cudaStreamWaitEvent(h->comm_stream, h->ev_start, 0));
+    RET(ymajor_exchange_nccl(h, bc));
+    const Faces fc = step_faces(h, bc);
+    RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, ycols_interior(h, bc), 1, fc));
+    const int ring = h->ev_count % kEventRing;
+    CK(cudaEventRecord(h->ev_int[ring], h->stream));
+    {
+        OnStream on(h, h->halo_stream);
+        CK(cudaStreamWaitEvent(h->halo_stream, h->ev_recv, 0));
+        int nseg = 0;
+        const Segments bnd = ycols_boundary(h, bc, &nseg);
+        RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, bnd, nseg, fc, true));
+        CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
+    }
+    CK(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
+    CK(cudaEventRecord(h->ev_wait[ring], h->stream));
+    ++h->ev_count;
+    h->cur = 1 - h->cur;
+    ++h->time_step;
+    return D2Q37_OK;
+}
+
+// Unfused y-major slab step over NCCL: exchange, then propagate + collide.
+int ymajor_step_nccl_unfused(d2q37_lattice* h, double omega, int bc) {
+    CK(cudaEventRecord(h->ev_start, h->stream));
+    CK(cudaStreamWaitEvent(h->comm_stream, h->ev_start, 0));
+    RET(ymajor_exchange_nccl(h, bc));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_recv, 0));
+    return step_local(h, omega, D2Q37_UNFUSED, bc);
+}
+
 // Slab step, phase 1 (before the halos are needed): the interior rows, whose
 // pull stencil stays inside the slab (x wrap and lane shifts in-kernel).
 int slab_phase1(d2q37_lattice* h, double omega, int variant, int bc) {
@@ -712,14 +823,25 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
     return D2Q37_OK;
 }
 
-int create_impl(int layout, int lx, int ly, int vl, int device, d2q37_lattice** out, int rank, int nranks) {
+// ymajor: store the lattice transposed (storage columns along y, rows along x)
+// -- the y-slab layout of the site-major layouts, whose slab faces are then
+// whole contiguous storage columns.
+int create_impl(int layout, int lx, int ly, int vl, int device, d2q37_lattice** out, int rank, int nranks,
+                bool ymajor = false) {
     if (!out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null output handle");
     *out = nullptr;
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad rank %d / %d", rank, nranks);
     if (ly % nranks != 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "ly=%d not divisible by %d slabs", ly, nranks);
     std::unique_ptr<d2q37_lattice> h(new (std::nothrow) d2q37_lattice());
     if (!h) return fail(D2Q37_ERR_CUDA, "out of host memory");
-    RET(make_geometry(layout, lx, ly / nranks, vl, &h->g));
+    if (ymajor) {
+        if (ly / nranks < 2 * kHalo + 1)
+            return fail(D2Q37_ERR_INVALID_ARGUMENT, "y-major slab needs at least 7 rows per slab");
+        RET(make_geometry(layout, ly / nranks, lx, vl, &h->g));
+        h->g.tr = 1;
+    } else {
+        RET(make_geometry(layout, lx, ly / nranks, vl, &h->g));
+    }
     h->layout = layout;
     h->device = device;
     h->rank = rank;
@@ -796,8 +918,8 @@ void* d2q37_get_stream(d2q37_lattice* h) { return h ? static_cast<void*>(h->stre
 
 int d2q37_geometry(const d2q37_lattice* h, int out[6]) {
     RET(check_handle(h));
-    out[0] = h->g.lx;
-    out[1] = h->g.ly;
+    out[0] = h->g.tr ? h->g.ly : h->g.lx;  // lattice extents (y-major storage is transposed)
+    out[1] = h->g.tr ? h->g.lx : h->g.ly;
     out[2] = h->g.vl;
     out[3] = h->g.strip;
     out[4] = h->g.sy;
@@ -843,6 +965,7 @@ static size_t ref_index(const d2q37_lattice* h, int p, int X, int j, int k) {
 
 int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
     RET(check_handle(h));
+    RET(padded_verbs_ok(h, "read_padded"));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
     if (n != padded_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "padded size mismatch (want %zu)", padded_count(h));
     DeviceGuard dg(h->device);
@@ -860,6 +983,7 @@ int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
 
 int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n) {
     RET(check_handle(h));
+    RET(padded_verbs_ok(h, "write_padded"));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
     if (n != padded_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "padded size mismatch (want %zu)", padded_count(h));
     DeviceGuard dg(h->device);
@@ -878,6 +1002,7 @@ int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n
 
 int d2q37_bc(d2q37_lattice* h, int bc) {
     RET(check_handle(h));
+    RET(padded_verbs_ok(h, "bc"));
     RET(validate_bc(h, bc));
     DeviceGuard dg(h->device);
     if (!local_only(h) && remote_faces(h, bc)) {
@@ -898,10 +1023,12 @@ int d2q37_propagate(d2q37_lattice* h) { return d2q37_propagate_corrupt(h, -1); }
 
 int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
     RET(check_handle(h));
+    RET(padded_verbs_ok(h, "propagate"));
     DeviceGuard dg(h->device);
     if (corrupt_population >= kNpop) return fail(D2Q37_ERR_INVALID_ARGUMENT, "corrupt_population out of range");
     Offsets off = h->off_pull;
     if (corrupt_population >= 0) off.o[corrupt_population] += 1;  // bites on the flat-offset (interior) sites
+    finish_offsets(off, h->g.pstride, corrupt_population < 0);
     return propagate_launch(h, off, ghost_faces(h));
 }
 
@@ -934,7 +1061,9 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
     }
     for (; s < nsteps; ++s) {
-        if (slab && h->halo_stream && variant == D2Q37_FUSED && can_split(h)) {
+        if (slab && h->g.tr) {
+            RET(variant == D2Q37_FUSED ? ymajor_step_nccl(h, omega, bc) : ymajor_step_nccl_unfused(h, omega, bc));
+        } else if (slab && h->halo_stream && variant == D2Q37_FUSED && can_split(h)) {
             RET(slab_step_overlapped(h, omega, bc));
         } else if (slab) {
             RET(exchange_begin(h, bc));
@@ -1146,7 +1275,9 @@ int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]) {
 
 int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
                       const unsigned char id[D2Q37_NCCL_ID_BYTES], d2q37_lattice** out) {
-    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks));
+    // site-major layouts (AoS, CAoSoA) slab in y-major storage: faces = contiguous columns
+    const bool ymajor = site_major(layout) && (nranks > 1 || id != nullptr);
+    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks, ymajor));
     d2q37_lattice* h = *out;
     if (nranks == 1 && !id) return D2Q37_OK;
     auto bail = [&](int rc) {
@@ -1185,7 +1316,7 @@ int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslab
         return rc;
     };
     for (int r = 0; r < nslabs; ++r) {
-        int rc = create_impl(layout, lx, ly, vl, device, &slabs[r], r, nslabs);
+        int rc = create_impl(layout, lx, ly, vl, device, &slabs[r], r, nslabs, site_major(layout) && nslabs > 1);
         if (rc != D2Q37_OK) return bail(rc);
         if (nslabs > 1) {
             rc = alloc_exchange(slabs[r]);
@@ -1217,6 +1348,11 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
     DeviceGuard dg(slabs[0]->device);
     for (int s = 0; s < nsteps; ++s) {
         if (nslabs == 1 || !remote_faces(slabs[0], bc)) {
+            for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
+            continue;
+        }
+        if (slabs[0]->g.tr) {  // y-major: ghost columns <- neighbours' columns, then local steps
+            RET(ymajor_group_exchange(slabs, bc));
             for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
             continue;
         }
@@ -1285,7 +1421,7 @@ int d2q37_slab_info(const d2q37_lattice* h, int out[4]) {
     out[0] = h->rank;
     out[1] = h->nranks;
     out[2] = h->y0;
-    out[3] = h->g.ly;
+    out[3] = h->g.tr ? h->g.lx : h->g.ly;  // y-major: lattice y runs along the storage columns
     return D2Q37_OK;
 }
 

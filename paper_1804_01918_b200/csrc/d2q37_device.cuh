@@ -31,6 +31,8 @@ struct DevGeo {
     int pitch;      // device rows per padded column (>= sy)
     int px;         // lx + 6
     int lvl;        // log2(vl)
+    int tr;         // 1: y-major storage (storage column = lattice y, storage row = lattice x)
+    int pad_;
     long long lead;     // element offset of (p, X, j, k) = (0, 0, 0, 0)
     long long pstride;  // between populations of one site: plane (SoA/CSoA) or vl (AoS/CAoSoA)
     long long rstride;  // between padded rows j of a lane: vl (SoA/CSoA) or 37*vl (AoS/CAoSoA)
@@ -46,6 +48,18 @@ __host__ __device__ __forceinline__ long long site_of(const DevGeo& g, int X, in
     return g.lead + (long long)X * g.cstride + (long long)(kHalo + (q >> g.lvl)) * g.rstride + (q & (g.vl - 1));
 }
 
+// Storage velocity components: y-major storage (g.tr) swaps the lattice axes.
+template <bool TR>
+__host__ __device__ __forceinline__ constexpr int scx(int p) { return TR ? cy_of(p) : cx_of(p); }
+template <bool TR>
+__host__ __device__ __forceinline__ constexpr int scy(int p) { return TR ? cx_of(p) : cy_of(p); }
+
+// Index in a canonical population plane ((x*ly + y), dump.hpp:19-21) of the
+// storage site (column xs, storage y ys = lane*strip + row).
+__host__ __device__ __forceinline__ long long canon_index(const DevGeo& g, int xs, int ys) {
+    return g.tr ? (long long)ys * g.lx + xs : (long long)xs * g.ly + ys;
+}
+
 // Model constants travel as kernel parameters (constant bank 0, broadcast to
 // every lane), so lattices with different models never race on __constant__.
 struct ModelParams {
@@ -56,7 +70,24 @@ struct ModelParams {
 
 struct Offsets {
     long long o[kNpop];
+    int o32[kNpop];  // o as 32-bit (valid when w32)
+    int ps32;        // pstride as 32-bit (valid when w32)
+    int w32;         // every o and 36 * pstride fit in int32: one IMAD.WIDE per address
+    int canonical;   // o are the pull offsets of the geometry (no corrupt_population hook)
 };
+
+// Fills o32 / ps32 / w32 from o and pstride (call after every change of o).
+inline void finish_offsets(Offsets& off, long long pstride, bool canonical) {
+    off.canonical = canonical ? 1 : 0;
+    const long long lim = 0x7fffffffLL;
+    bool fits = 36 * pstride <= lim;
+    for (int p = 0; p < kNpop; ++p) {
+        fits = fits && off.o[p] <= lim && off.o[p] >= -lim;
+        off.o32[p] = int(off.o[p]);
+    }
+    off.ps32 = int(pstride);
+    off.w32 = fits ? 1 : 0;
+}
 
 // FP helpers: FAST lets nvcc contract a*b+c into DFMA; STRICT rounds every op.
 template <bool STRICT>

@@ -46,21 +46,52 @@ __device__ __forceinline__ int wrapi(int v, int n) {
 //   * the outer y faces (lane 0 low, lane vl-1 high) are periodic (wrap to the
 //     opposite face), wall (specular image f(mirror y, ybar p)) or
 //     ghost (read the ghost rows: after a bc verb, or halos received by a slab).
+//   * in y-major storage (TR) the roles swap: rows are periodic lattice x and the
+//     storage columns carry the y faces (periodic wrap, wall mirror, or ghost
+//     columns received from a slab neighbour).
+// Periodic wrap of an index at most one period outside [0, n) (the modulo
+// only runs for degenerate extents n < 3).
+__device__ __forceinline__ int wrap_near(int v, int n) {
+    if (v < 0) v += n;
+    else if (v >= n) v -= n;
+    return (v < 0 || v >= n) ? wrapi(v, n) : v;
+}
+
+template <bool TR>
 __device__ __forceinline__ long long edge_source(const DevGeo& g, const Faces& fc, int p, int x, int row, int k) {
-    const int xs = wrapi(x - cx_of(p), g.lx);
-    int r = row - cy_of(p), kk = k, pp = p;
+    int xs = x - scx<TR>(p), pp = p;
+    if (!TR) {  // normal storage: the columns are lattice x, always periodic
+        xs = wrap_near(xs, g.lx);
+    } else if (xs < 0) {
+        if (fc.col_lo == kFacePeriodic)
+            xs = wrap_near(xs, g.lx);
+        else if (fc.col_lo == kFaceWall) {
+            xs = -1 - xs;
+            pp = fc.ybar[p];
+        }  // kFaceGhost: ghost column X = 3 + xs
+    } else if (xs >= g.lx) {
+        if (fc.col_hi == kFacePeriodic)
+            xs = wrap_near(xs, g.lx);
+        else if (fc.col_hi == kFaceWall) {
+            xs = 2 * g.lx - 1 - xs;
+            pp = fc.ybar[p];
+        }
+    }
+    // y-major storage: the rows are lattice x, periodic (lane 0 low <-> lane vl-1 high)
+    const int face_lo = TR ? int(kFacePeriodic) : fc.lo, face_hi = TR ? int(kFacePeriodic) : fc.hi;
+    int r = row - scy<TR>(p), kk = k;
     if (r < 0) {
         if (k > 0) {
             r += g.strip;
             kk = k - 1;
-        } else if (fc.lo == kFacePeriodic) {
+        } else if (face_lo == kFacePeriodic) {
             if (g.vl == 1) {
-                r = wrapi(r, g.strip);
+                r = wrap_near(r, g.strip);
             } else {
                 r += g.strip;
                 kk = g.vl - 1;
             }
-        } else if (fc.lo == kFaceWall) {
+        } else if (face_lo == kFaceWall) {
             r = -1 - r;
             pp = fc.ybar[p];
         }  // kFaceGhost: ghost row j = 3 + r of lane 0
@@ -68,36 +99,19 @@ __device__ __forceinline__ long long edge_source(const DevGeo& g, const Faces& f
         if (k < g.vl - 1) {
             r -= g.strip;
             kk = k + 1;
-        } else if (fc.hi == kFacePeriodic) {
+        } else if (face_hi == kFacePeriodic) {
             if (g.vl == 1) {
-                r = r % g.strip;
+                r = wrap_near(r, g.strip);
             } else {
                 r -= g.strip;
                 kk = 0;
             }
-        } else if (fc.hi == kFaceWall) {
+        } else if (face_hi == kFaceWall) {
             r = 2 * g.strip - 1 - r;
             pp = fc.ybar[p];
         }
     }
     return elem_of(g, pp, xs + kHalo, r + kHalo, kk);
-}
-
-__device__ __forceinline__ bool edge_site(const DevGeo& g, int x, int row) {
-    return x < kHalo || x >= g.lx - kHalo || row < kHalo || row >= g.strip - kHalo;
-}
-
-// Gathers the 37 pulled populations of one site into registers.
-__device__ __forceinline__ void pull_site(double (&f)[kNpop], const double* __restrict__ src, long long e,
-                                          const DevGeo& g, const Offsets& off, const Faces& fc, int x, int row,
-                                          int k) {
-    if (!edge_site(g, x, row)) {
-#pragma unroll
-        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + off.o[p]);
-    } else {  // unrolled: f[] must stay in registers
-#pragma unroll
-        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + edge_source(g, fc, p, x, row, k));
-    }
 }
 
 // Column x and site q of this thread in the launch's segments; false if none.
@@ -109,6 +123,10 @@ __device__ __forceinline__ bool segment_site(const DevGeo& g, const Segments& se
         x = t / per_col;
         const int i = t - x * per_col;
         q = seg.q0[i / seg.nq] + (i % seg.nq) * seg.stride;
+    } else if (seg.nx > 0) {  // segment z: columns x0[z] .. +nx, sites q0[z] .. +nq
+        if (t >= seg.nq) return false;
+        x = seg.x0[blockIdx.z] + blockIdx.y;
+        q = seg.q0[blockIdx.z] + t * seg.stride;
     } else {
         if (t >= seg.nq) return false;
         x = blockIdx.y;
@@ -120,36 +138,120 @@ __device__ __forceinline__ bool segment_site(const DevGeo& g, const Segments& se
     return true;
 }
 
+// True if the site is within 3 of a column end or a lane-strip end, i.e. its
+// pull needs the in-kernel boundary (edge_source).  Per thread: a per-CTA test
+// sends whole CTAs of flat sites down the slower edge path (measured -2 %).
+__device__ __forceinline__ bool edge_site(const DevGeo& g, const Segments& seg, int x, int q) {
+    if (seg.dense) return true;
+    const int row = q >> g.lvl;
+    return x < kHalo || x >= g.lx - kHalo || row < kHalo || row >= g.strip - kHalo;
+}
+
+enum { kPullNone = 0, kPullFlat = 1, kPullEdge = 2 };
+
+// Hides how a pointer was formed, so nvcc adds each offset to it (one IMAD.WIDE)
+// instead of re-associating base + (e + o) * 8 per population.
+template <typename T>
+__device__ __forceinline__ T* opaque(T* p) {
+    asm("" : "+l"(p));
+    return p;
+}
+
+// Address modes of the flat (edge-free) site paths:
+//   kAddr64: 64-bit offsets (any geometry);
+//   kAddr32: 32-bit offsets, one IMAD.WIDE per address off the site pointer;
+//   VL > 0:  site-major store (AoS / CAoSoA) with vl = VL known at compile time:
+//            7 column base pointers, every load / store an immediate offset.
+enum { kAddr64 = -1, kAddr32 = 0 };
+
+// Gathers the 37 populations of site e: from itself (collide), from the flat
+// pull offsets, or through edge_source (in-kernel boundary).
+template <int PULL, bool TR, int AM>
+__device__ __forceinline__ void gather_site(double (&f)[kNpop], const double* __restrict__ src, long long e,
+                                            const DevGeo& g, const Offsets& off, const Faces& fc, int x, int q) {
+    const double* __restrict__ s = opaque(src + e);
+    if (PULL == kPullNone) {
+#pragma unroll
+        for (int p = 0; p < kNpop; ++p)
+            f[p] = ld_stream(AM > 0 ? s + p * AM : AM == kAddr32 ? s + p * off.ps32 : s + p * g.pstride);
+    } else if (PULL == kPullFlat) {
+        if (AM > 0) {
+            // pull offset p*vl - sx*cstride - sy*37*vl (fill_offsets): a base per source column
+            const double* b[2 * kHalo + 1];
+#pragma unroll
+            for (int c = -kHalo; c <= kHalo; ++c) b[c + kHalo] = opaque(s - (long long)c * g.cstride);
+#pragma unroll
+            for (int p = 0; p < kNpop; ++p)
+                f[p] = ld_stream(b[scx<TR>(p) + kHalo] + (p * AM - scy<TR>(p) * kNpop * AM));
+        } else {
+#pragma unroll
+            for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(AM == kAddr32 ? s + off.o32[p] : s + off.o[p]);
+        }
+    } else {  // unrolled: f[] must stay in registers (a rolled address loop costs 16 %)
+        const int row = q >> g.lvl, k = q & (g.vl - 1);
+#pragma unroll
+        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + edge_source<TR>(g, fc, p, x, row, k));
+    }
+}
+
+template <int AM>
+__device__ __forceinline__ void store_site(double* __restrict__ dst, long long e, const DevGeo& g, const Offsets& off,
+                                           const double (&f)[kNpop]) {
+    double* __restrict__ d = opaque(dst + e);
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p)
+        st_stream(AM > 0 ? d + p * AM : AM == kAddr32 ? d + p * off.ps32 : d + p * g.pstride, f[p]);
+}
+
+template <int PULL, bool TR, int AM>
+__device__ __forceinline__ void propagate_site(const double* __restrict__ src, double* __restrict__ dst, long long e,
+                                               const DevGeo& g, const Offsets& off, const Faces& fc, int x, int q) {
+    double f[kNpop];
+    gather_site<PULL, TR, AM>(f, src, e, g, off, fc, x, q);
+    store_site<AM>(dst, e, g, off, f);
+}
+
+template <int PULL, bool STRICT, bool TR, int AM>
+__device__ __forceinline__ void collide_site_at(const double* __restrict__ src, double* __restrict__ dst, long long e,
+                                                const DevGeo& g, const Offsets& off, const Faces& fc,
+                                                const ModelParams& mp, double omega, int x, int q,
+                                                int* __restrict__ flag) {
+    double f[kNpop];
+    gather_site<PULL, TR, AM>(f, src, e, g, off, fc, x, q);
+    const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
+    if (bad) *flag = 1;
+    store_site<AM>(dst, e, g, off, f);
+}
+
+// The flat and edge paths are separate, complete site updates, so the flat
+// path's load burst is scheduled as in an edge-free kernel.  The edge path
+// always uses 64-bit addressing.
+template <bool TR, int AM>
 __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __restrict__ src,
                                                               double* __restrict__ dst, DevGeo g, Offsets off,
                                                               Faces fc, Segments seg) {
     int x, q;
     if (!segment_site(g, seg, x, q)) return;
     const long long e = site_of(g, x + kHalo, q);
-    double f[kNpop];
-    pull_site(f, src, e, g, off, fc, x, q >> g.lvl, q & (g.vl - 1));
-#pragma unroll
-    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.pstride, f[p]);
+    if (edge_site(g, seg, x, q))
+        propagate_site<kPullEdge, TR, kAddr64>(src, dst, e, g, off, fc, x, q);
+    else
+        propagate_site<kPullFlat, TR, AM>(src, dst, e, g, off, fc, x, q);
 }
 
-template <bool STRICT, bool SHIFT>
+template <bool STRICT, bool SHIFT, bool TR, int AM>
 __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, Faces fc,
               ModelParams mp, double omega, Segments seg, int* __restrict__ flag) {
     int x, q;
     if (!segment_site(g, seg, x, q)) return;
     const long long e = site_of(g, x + kHalo, q);
-    double f[kNpop];
-    if (SHIFT) {
-        pull_site(f, src, e, g, off, fc, x, q >> g.lvl, q & (g.vl - 1));
-    } else {
-#pragma unroll
-        for (int p = 0; p < kNpop; ++p) f[p] = ld_stream(src + e + p * g.pstride);
-    }
-    const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
-    if (bad) *flag = 1;
-#pragma unroll
-    for (int p = 0; p < kNpop; ++p) st_stream(dst + e + p * g.pstride, f[p]);
+    if (!SHIFT)
+        collide_site_at<kPullNone, STRICT, TR, AM>(src, dst, e, g, off, fc, mp, omega, x, q, flag);
+    else if (edge_site(g, seg, x, q))
+        collide_site_at<kPullEdge, STRICT, TR, kAddr64>(src, dst, e, g, off, fc, mp, omega, x, q, flag);
+    else
+        collide_site_at<kPullFlat, STRICT, TR, AM>(src, dst, e, g, off, fc, mp, omega, x, q, flag);
 }
 
 // ---------------------------------------------------------------------------
@@ -253,7 +355,7 @@ __global__ void k_scatter(double* __restrict__ buf, DevGeo g, const double* __re
     if (t >= (long long)g.lx * g.ly) return;
     const int x = int(t / g.ly), q = int(t % g.ly);
     const int y = (q % g.vl) * g.strip + q / g.vl;
-    buf[site_of(g, x + kHalo, q) + p * g.pstride] = canon[(long long)x * g.ly + y];
+    buf[site_of(g, x + kHalo, q) + p * g.pstride] = canon[canon_index(g, x, y)];
 }
 
 __global__ void k_gather(const double* __restrict__ buf, DevGeo g, double* __restrict__ canon, int p) {
@@ -261,7 +363,13 @@ __global__ void k_gather(const double* __restrict__ buf, DevGeo g, double* __res
     if (t >= (long long)g.lx * g.ly) return;
     const int x = int(t / g.ly), q = int(t % g.ly);
     const int y = (q % g.vl) * g.strip + q / g.vl;
-    canon[(long long)x * g.ly + y] = buf[site_of(g, x + kHalo, q) + p * g.pstride];
+    canon[canon_index(g, x, y)] = buf[site_of(g, x + kHalo, q) + p * g.pstride];
+}
+
+// Lattice (x, y_local) of the storage site (column xs, storage y ys).
+__device__ __forceinline__ void lattice_xy(const DevGeo& g, int xs, int ys, int& x, int& y) {
+    x = g.tr ? ys : xs;
+    y = g.tr ? xs : ys;
 }
 
 // Philox4x32-10, key = seed, counter = site-major index (x*ly_global + y)*37 + p.
@@ -289,10 +397,11 @@ __device__ __forceinline__ double philox_u01_dev(unsigned long long seed, unsign
 __global__ void k_philox(double* __restrict__ buf, DevGeo g, unsigned long long seed, int y0, int ly_global) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= g.ly) return;
-    const int x = blockIdx.y;
-    const int y = (q % g.vl) * g.strip + q / g.vl;
+    const int xs = blockIdx.y;
+    int x, y;
+    lattice_xy(g, xs, (q % g.vl) * g.strip + q / g.vl, x, y);
     const unsigned long long site = (unsigned long long)x * ly_global + (unsigned long long)(y0 + y);
-    const long long e = site_of(g, x + kHalo, q);
+    const long long e = site_of(g, xs + kHalo, q);
 #pragma unroll 1
     for (int p = 0; p < kNpop; ++p) buf[e + p * g.pstride] = philox_u01_dev(seed, site * kNpop + p);
 }
@@ -305,16 +414,19 @@ __global__ void k_init_rt(double* __restrict__ buf, DevGeo g, ModelParams mp, un
                           int ly_global) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= g.ly) return;
-    const int x = blockIdx.y;
-    const int y = y0 + (q % g.vl) * g.strip + q / g.vl;
+    const int xs = blockIdx.y;
+    int x, y;
+    lattice_xy(g, xs, (q % g.vl) * g.strip + q / g.vl, x, y);
+    y += y0;
+    const int lx = g.tr ? g.ly : g.lx;
     const double noise = -1e-3 + 2e-3 * philox_u01_dev(seed, (unsigned long long)x * ly_global + y);
-    const double yint = 0.5 * ly_global + 0.01 * ly_global * sin(2.0 * 3.14159265358979323846 * x / g.lx);
+    const double yint = 0.5 * ly_global + 0.01 * ly_global * sin(2.0 * 3.14159265358979323846 * x / lx);
     const double temp = ((double)y < yint ? 1.5 : 0.5) + noise;
     const double rho = 1.0 / temp;
     const double dt = temp - mp.t0, dt2 = dt * dt;
     // u = 0: only the pure-temperature Hermite terms survive (mom 2, 4, 9, 11, 13)
     const double m2 = dt, m9 = 3.0 * dt2, m11 = dt2;
-    const long long e = site_of(g, x + kHalo, q);
+    const long long e = site_of(g, xs + kHalo, q);
 #pragma unroll 1
     for (int p = 0; p < kNpop; ++p) {
         const double* gp = mp.eq[p];
@@ -366,39 +478,83 @@ static dim3 stream_grid(const DevGeo& g, const Segments& seg, int nseg) {
         const long long n = (long long)seg.nq * nseg * g.lx;
         return dim3(unsigned((n + kStreamThreads - 1) / kStreamThreads), 1, 1);
     }
-    return dim3((seg.nq + kStreamThreads - 1) / kStreamThreads, g.lx, nseg);
+    return dim3((seg.nq + kStreamThreads - 1) / kStreamThreads, seg.nx > 0 ? seg.nx : g.lx, nseg);
 }
+
+// Address mode of a launch (see gather_site): the compile-time site-major
+// store for the canonical pull offsets at vl = 32 / 16 / 1 (CAoSoA, AoS), else
+// 32-bit or 64-bit offsets.
+int addr_mode(const DevGeo& g, const Offsets& off) {
+    if (off.canonical && g.pstride == g.vl && g.rstride == (long long)kNpop * g.vl && off.w32 &&
+        (g.vl == 32 || g.vl == 16 || g.vl == 1))
+        return g.vl;
+    return off.w32 ? kAddr32 : kAddr64;
+}
+
+#define D2Q37_BY_ADDR(am, LAUNCH)             \
+    switch (am) {                             \
+        case 32: LAUNCH(32); break;           \
+        case 16: LAUNCH(16); break;           \
+        case 1: LAUNCH(1); break;             \
+        case kAddr32: LAUNCH(kAddr32); break; \
+        default: LAUNCH(kAddr64); break;      \
+    }
 
 cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                              const Segments& seg, int nseg, cudaStream_t s) {
     if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
+    const dim3 grid = stream_grid(g, seg, nseg);
     (void)cudaGetLastError();
-    k_propagate<<<stream_grid(g, seg, nseg), kStreamThreads, 0, s>>>(src, dst, g, off, fc, seg);
+#define D2Q37_PROP_T(AM) k_propagate<true, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, seg)
+#define D2Q37_PROP_N(AM) k_propagate<false, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, seg)
+    if (g.tr) {
+        D2Q37_BY_ADDR(addr_mode(g, off), D2Q37_PROP_T)
+    } else {
+        D2Q37_BY_ADDR(addr_mode(g, off), D2Q37_PROP_N)
+    }
+#undef D2Q37_PROP_T
+#undef D2Q37_PROP_N
     return cudaGetLastError();
 }
+
+namespace {
+template <bool S, bool SH, bool TR>
+void collide_am(dim3 grid, cudaStream_t s, const double* src, double* dst, const DevGeo& g, const Offsets& off,
+                const Faces& fc, const ModelParams& mp, double omega, const Segments& seg, int* flag) {
+#define D2Q37_COLL(AM) \
+    k_collide<S, SH, TR, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag)
+    D2Q37_BY_ADDR(addr_mode(g, off), D2Q37_COLL)
+#undef D2Q37_COLL
+}
+}  // namespace
 
 cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
                            int nseg, int* flag, cudaStream_t s) {
     if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
     const dim3 grid = stream_grid(g, seg, nseg);
-#define D2Q37_COLLIDE(S, SH) \
-    k_collide<S, SH><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag)
+#define D2Q37_COLLIDE(S, SH, TR) collide_am<S, SH, TR>(grid, s, src, dst, g, off, fc, mp, omega, seg, flag)
     (void)cudaGetLastError();
-    if (strict) {
-        if (shift)
-            D2Q37_COLLIDE(true, true);
+    if (!shift) {  // no pull: the storage orientation does not matter
+        if (strict)
+            D2Q37_COLLIDE(true, false, false);
         else
-            D2Q37_COLLIDE(true, false);
+            D2Q37_COLLIDE(false, false, false);
+    } else if (strict) {
+        if (g.tr)
+            D2Q37_COLLIDE(true, true, true);
+        else
+            D2Q37_COLLIDE(true, true, false);
     } else {
-        if (shift)
-            D2Q37_COLLIDE(false, true);
+        if (g.tr)
+            D2Q37_COLLIDE(false, true, true);
         else
-            D2Q37_COLLIDE(false, false);
+            D2Q37_COLLIDE(false, true, false);
     }
 #undef D2Q37_COLLIDE
     return cudaGetLastError();
 }
+#undef D2Q37_BY_ADDR
 
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s) {
     long long total = (long long)kNpop * g.px * 6 * (ep.lean ? 1 : g.vl);

@@ -19,12 +19,16 @@ constexpr int kCollideMinBlocks = 3;
 // a slab computes those after its halos arrive.
 // dense = 1 packs the segments of every column into one 1-D grid (a few sites
 // per column: the slab boundary launch); otherwise grid = (nq/128, lx, nseg).
+// nx > 0 makes segment z the box of storage columns x0[z] .. x0[z]+nx-1 by
+// sites q0[z] + t*stride: the y-major slab's interior / boundary columns.
 struct Segments {
     int q0[2];
     int nq;
     int stride;
     int skip_lo, skip_hi;
     int dense, nseg;
+    int x0[2];
+    int nx;
 };
 
 // Outer y-face treatment.  k_edge: periodic wrap, wall mirror, or remote (from
@@ -33,8 +37,12 @@ struct Segments {
 enum { kFacePeriodic = 0, kFaceWall = 1, kFaceRemote = 2, kFaceGhost = 3 };
 enum { kEdgeLocal = 1, kEdgeRemote = 2, kEdgeAll = 3 };
 
+// lo / hi: the storage-row faces (lane 0 low, lane vl-1 high); col_lo / col_hi:
+// the storage-column faces (periodic x in the normal storage; the lattice y
+// faces in y-major storage, where walls and slab neighbours sit).
 struct Faces {
     int lo, hi;
+    int col_lo, col_hi;
     signed char ybar[kNpop];  // y-mirror (cx, -cy)
 };
 

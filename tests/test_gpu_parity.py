@@ -284,7 +284,7 @@ def test_layouts_and_variants_bitwise_identical(gpu, lbm, bc):
     init = lbm.make_lattice("random", lx, ly, seed=13)
     outs = []
     for layout, vl in (("soa", 1), ("csoa", 2), ("csoa", 8), ("csoa", 32), ("aos", 1), ("caosoa", 8),
-                       ("caosoa", 32)):
+                       ("caosoa", 16), ("caosoa", 32)):
         for variant in ("fused", "unfused"):
             s = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
             s.load(init)
@@ -297,10 +297,11 @@ def test_layouts_and_variants_bitwise_identical(gpu, lbm, bc):
 @pytest.mark.parametrize("nslabs", [2, 4])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 @pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 4, "fused"),
-                                               ("caosoa", 4, "fused"), ("aos", 1, "unfused")])
+                                               ("caosoa", 4, "fused"), ("caosoa", 8, "unfused"), ("aos", 1, "unfused")])
 def test_slab_group_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, vl, variant):
-    """GPU-count invariance (test_kernels.cpp:361-381 analogue): y-slabs == one domain, bit for bit."""
-    lx, ly = 16, 256
+    """GPU-count invariance (test_kernels.cpp:361-381 analogue): y-slabs == one domain, bit for bit.
+    Site-major slabs (AoS, CAoSoA) run in y-major storage: lanes along x need lx/vl >= 3."""
+    lx, ly = 32, 256
     init = lbm.make_lattice("random", lx, ly, seed=21)
     ref = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
     ref.load(init)
@@ -403,9 +404,10 @@ def test_lbdump01_streaming_multi_chunk(gpu, lbm, tmp_path):
     assert np.array_equal(b.dump(), a.dump())
 
 
-@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 32)])
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 32), ("caosoa", 32)])
 def test_device_rt_init_vs_oracle(gpu, lbm, po, layout, vl):
-    """init_rt_device == the oracle's Philox-noise RT recipe (<= 1e-14), per slab of a taller lattice."""
+    """init_rt_device == the oracle's Philox-noise RT recipe (<= 1e-14), per slab of a taller lattice
+    (CAoSoA slabs use y-major storage: the init maps storage to lattice coordinates)."""
     lx, ly = 32, 256
     want = po.orc_lattice("rt_philox", lx, ly, seed=12345)
     s = sim_of(lbm, layout, lx, ly, vl)
@@ -465,6 +467,26 @@ def test_config3_full_size_one_step_vs_oracle(gpu, lbm, po):
 
 
 @pytest.mark.slow
+def test_config3_full_size_address_modes_bitwise(gpu, lbm):
+    """Every address mode of the flat site path at the bench size (4096 x 16384): 64-bit offsets
+    (SoA / CSoA: 36 planes exceed int32), compile-time site-major vl = 32 / 16 / 1 (CAoSoA, AoS)
+    and 32-bit offsets (CAoSoA 8) give bit-identical lattices after 3 fused wall steps."""
+    lx, ly = 4096, 16384
+    ref = None
+    for layout, vl in (("caosoa", 32), ("soa", 1), ("csoa", 8), ("caosoa", 16), ("aos", 1), ("caosoa", 8)):
+        s = sim_of(lbm, layout, lx, ly, vl, bc="wall")
+        s.init_rt_device(777)
+        s.step(0.8, 3)
+        got = s.dump()
+        s.close()
+        if ref is None:
+            ref = got
+        else:
+            assert np.array_equal(got, ref), (layout, vl)
+        del got
+
+
+@pytest.mark.slow
 def test_config3_size_conservation(gpu, lbm):
     """4096x16384 RT, wall, 20 fused steps: mass / energy conserved, momentum stays ~0 (size-independent)."""
     s = sim_of(lbm, "soa", 4096, 16384, bc="wall")
@@ -477,13 +499,15 @@ def test_config3_size_conservation(gpu, lbm):
     assert abs(m1[1]) < 1e-6 * m0[0]
 
 
-@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("csoa", 8, "fused"), ("soa", 1, "unfused")])
+@pytest.mark.parametrize("layout,vl,variant", [("soa", 1, "fused"), ("csoa", 8, "fused"), ("soa", 1, "unfused"),
+                                               ("caosoa", 8, "fused"), ("caosoa", 4, "unfused"), ("aos", 1, "fused")])
 def test_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, variant):
     """The real NCCL transport on one GPU: a 1-rank ring whose periodic y wrap goes
-    pack -> ncclSend/ncclRecv (self) -> remote edge, with the interior/boundary overlap."""
+    through ncclSend/ncclRecv to self, with the interior/boundary overlap.  Plane-major
+    layouts pack 26 pop-rows; site-major layouts (y-major slab storage) send whole columns."""
     import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library binds to)
 
-    lx, ly = 16, 256
+    lx, ly = 32, 256
     init = lbm.make_lattice("random", lx, ly, seed=33)
     ref = sim_of(lbm, layout, lx, ly, vl, variant=variant)
     ref.load(init)
@@ -494,6 +518,10 @@ def test_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, varia
     s.step(1.2, 6)
     assert np.array_equal(s.dump(), ref.dump())
     assert s.exposed_halo_ms() >= 0.0
+    if layout in ("aos", "caosoa"):  # y-major storage: no padded-buffer verbs
+        with pytest.raises(ValueError, match="y-major"):
+            s.bc("periodic")
+        return
     # the bc verb through NCCL fills only the 26 planned ghost pop-rows, which is
     # everything propagate reads: halo + propagate must still equal the single domain
     s.bc("periodic")
