@@ -1,6 +1,6 @@
 """A/B timing of the single-domain step through the bare C-ABI (works with any
 build of libd2q37_b200.so, old or new): 4096 x 16384 RT init, wall bc.
-usage: python tools/ab_step.py LIB [layout vl variant steps]"""
+usage: python tools/ab_step.py LIB [layout vl variant steps lx ly]"""
 import ctypes as C
 import statistics
 import sys
@@ -12,7 +12,8 @@ layout = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}[sys.argv[2] if len(sys.arg
 vl = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 variant = {"unfused": 0, "fused": 1}[sys.argv[4] if len(sys.argv) > 4 else "fused"]
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 200
-lx, ly = 4096, 16384
+lx = int(sys.argv[6]) if len(sys.argv) > 6 else 4096
+ly = int(sys.argv[7]) if len(sys.argv) > 7 else 16384
 lib.d2q37_step.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int]
 lib.d2q37_sync.argtypes = [C.c_void_p]
 lib.d2q37_init_rt_device.argtypes = [C.c_void_p, C.c_uint64]
