@@ -67,6 +67,61 @@ def test_golden_reference_propagate_and_halo(gpu, lbm, layout):
         assert np.array_equal(s.dump(which=1), g[f"propagate_{layout}"])
 
 
+def ghost_mask(layout, lx, ly, vl):
+    """True at the ghost slots (halo rows / columns) of a read_padded() buffer, in the
+    reference element order of each layout (layout.hpp:67-79)."""
+    strip = ly // vl
+    px, sy = lx + 6, strip + 6
+    X = np.arange(px)[:, None]
+    j = np.arange(sy)[None, :]
+    ghost_xj = (X < 3) | (X >= lx + 3) | (j < 3) | (j >= strip + 3)  # (px, sy)
+    if layout in ("soa", "csoa"):  # ((p*px + X)*sy + j)*vl + k
+        m = np.broadcast_to(ghost_xj[None, :, :, None], (37, px, sy, vl))
+    else:  # AoS / CAoSoA: ((X*sy + j)*37 + p)*vl + k
+        m = np.broadcast_to(ghost_xj[:, :, None, None], (px, sy, 37, vl))
+    return np.ascontiguousarray(m).ravel()
+
+
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("csoa", 4), ("aos", 1), ("caosoa", 8), ("caosoa", 32)])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+@pytest.mark.parametrize("variant", ["fused", "unfused"])
+def test_steps_never_read_ghosts(gpu, lbm, layout, vl, bc, variant):
+    """The in-kernel boundary claim: a step reads physical sites only.  Every ghost slot of
+    both buffers is poisoned with NaN; the steps must still match the unpoisoned run bit for
+    bit (a single ghost read would spread NaN)."""
+    lx, ly = 24, 192
+    init = lbm.make_lattice("random", lx, ly, seed=29)
+    clean = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
+    clean.load(init)
+    clean.step(1.3, 3)
+    want = clean.dump()
+    s = sim_of(lbm, layout, lx, ly, vl, bc=bc, variant=variant)
+    s.load(init)
+    mask = ghost_mask(layout, lx, ly, vl)
+    for which in (0, 1):
+        buf = s.read_padded(which)
+        assert buf.size == mask.size
+        buf[mask] = np.nan
+        s.write_padded(buf, which)
+    s.step(1.3, 3)
+    got = s.dump()
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("layout,vl", [("soa", 1), ("caosoa", 8)])
+def test_ghost_poison_is_detectable(gpu, lbm, layout, vl):
+    """Control for test_steps_never_read_ghosts: the propagate verb does read the ghost rows
+    (kernels.hpp:33, after a bc), so the same poisoning must show up as NaN there."""
+    lx, ly = 24, 192
+    s = sim_of(lbm, layout, lx, ly, vl)
+    s.load(lbm.make_lattice("random", lx, ly, seed=29))
+    buf = s.read_padded(0)
+    buf[ghost_mask(layout, lx, ly, vl)] = np.nan
+    s.write_padded(buf, 0)
+    s.propagate_only()
+    assert np.isnan(s.dump(which=1)).any()
+
+
 @pytest.mark.parametrize("layout,vl", [("aos", 1), ("caosoa", 4), ("caosoa", 32)])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 def test_site_major_layouts_bc_propagate(gpu, lbm, po, layout, vl, bc):
