@@ -148,6 +148,21 @@ int d2q37_swap_buffers(d2q37_lattice* h);
  * any collide since the last sync saw !(rho > 0) (model.cpp:245). */
 int d2q37_sync(d2q37_lattice* h);
 
+/* convert(src, to) (layout.hpp:148, layout.cpp:105-116): copy the
+ * physical sites of src's state buffer into dst's state buffer, any layouts
+ * and vl, same lx x ly, same device (dst is "Field dst(to)" of the reference,
+ * created by the caller).  Ghost slots of dst are left as they were. */
+int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst);
+
+/* Scalar device reference of run_validation (validation.hpp:15-42,
+ * validation.cpp:13-38 OracleLattice / oracle_propagate / oracle_collide):
+ * nsteps of propagate then collide, periodic in x and y, on a halo-free
+ * canonical array (dump.hpp:19-21 order) with explicit modulo indexing and no
+ * layout machinery.  n = 37*lx*ly; m = NULL uses VelocityModel::d2q37();
+ * math selects the collide arithmetic (compare like with like). */
+int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_in, double* host_out, size_t n,
+                       double omega, int nsteps, int math, int device);
+
 /* Global sums over the physical sites of the state buffer (prv):
  * out = {mass, x-momentum, y-momentum, energy sum |c|^2 f}; deterministic
  * for a given geometry.  Conservation checks at full size. */

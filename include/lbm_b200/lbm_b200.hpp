@@ -185,6 +185,26 @@ class LatticeState {
     Geometry geom_;
 };
 
+/// convert(src, to) (layout.hpp:148, layout.cpp:105-116): a new device lattice
+/// with layout `kind` / geometry `to` holding src's physical sites.
+inline LatticeState convert(const LatticeState& src, LayoutKind kind, Geometry to, int device = 0) {
+    if (to.lx != src.geom().lx || to.ly != src.geom().ly || to.hx != src.geom().hx || to.hy != src.geom().hy)
+        throw std::invalid_argument("convert: geometry mismatch");
+    LatticeState dst(kind, to, device);
+    check(d2q37_convert(src.handle(), dst.handle()));
+    return dst;
+}
+
+/// The scalar device reference of run_validation (validation.hpp:36-42):
+/// nsteps of propagate then collide on a halo-free canonical array, periodic.
+inline CanonicalLattice scalar_steps(const VelocityModel& m, const CanonicalLattice& in, double omega, int nsteps,
+                                     Math math = Math::Fast, int device = 0) {
+    CanonicalLattice out = make_canonical(in.lx, in.ly);
+    check(d2q37_scalar_steps(&m.raw(), in.lx, in.ly, in.values.data(), out.values.data(), in.values.size(), omega,
+                             nsteps, int(math), device));
+    return out;
+}
+
 inline void halo_exchange(LatticeState& s, Boundary bc = Boundary::Periodic) {
     check(d2q37_bc(s.handle(), int(bc)));
     s.sync();

@@ -34,7 +34,7 @@ import numpy as np
 __all__ = [
     "NPOP", "Model", "Simulation", "SlabGroup", "NonPhysicalError", "model", "mlups",
     "propagate_gbps", "collide_gflops", "make_lattice", "library_path", "nccl_unique_id",
-    "COLLIDE_FLOPS_PER_SITE", "__version__",
+    "COLLIDE_FLOPS_PER_SITE", "__version__", "convert", "scalar_steps",
 ]
 __version__ = "0.1.0"
 
@@ -134,6 +134,8 @@ def _load():
         "d2q37_exposed_halo_ms": (d, [vp]),
         "d2q37_set_profiling": (i, [vp, i]),
         "d2q37_kernel_times": (i, [vp, _dp, P(C.c_long)]),
+        "d2q37_convert": (i, [vp, vp]),
+        "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -291,6 +293,30 @@ def make_lattice(kind: str, lx: int, ly: int, seed: int = 12345, params=None, md
     return out
 
 
+def scalar_steps(canon, omega: float, nsteps: int, math: str = "fast", mdl: Model | None = None,
+                 device: int = 0) -> np.ndarray:
+    """The scalar device reference of run_validation (validation.cpp:13-38): ``nsteps`` of
+    propagate then collide, periodic in x and y, on a halo-free canonical array with explicit
+    modulo indexing (d2q37_scalar_steps).  Returns a new (37, lx, ly) array."""
+    a = np.ascontiguousarray(canon, dtype=np.float64)
+    if a.ndim != 3 or a.shape[0] != NPOP:
+        raise ValueError("canonical array must have shape (37, lx, ly)")
+    out = np.empty_like(a)
+    m = (mdl or model())._s
+    _check(_load().d2q37_scalar_steps(C.byref(m), a.shape[1], a.shape[2], _ptr(a), _ptr(out), a.size,
+                                      float(omega), int(nsteps), MATHS[math], device))
+    return out
+
+
+def convert(src: "Simulation", layout: str, vl: int = 1) -> "Simulation":
+    """convert(src, to) (layout.hpp:148, layout.cpp:105-116): a new lattice with ``layout``/``vl``
+    holding the physical sites of ``src``'s state buffer, on the same device."""
+    dst = Simulation(layout, src.lx, src.ly, vl, device=src.device, bc=src.bc_mode, variant=src.variant,
+                     math=src.math, mdl=src.model)
+    _check(_load().d2q37_convert(src._h, dst._h))
+    return dst
+
+
 def halo_plan():
     """(lo_entries, hi_entries): lists of (d, p) of the slab halo messages (d2q37_halo_plan)."""
     arrs = [(C.c_int * 32)() for _ in range(4)]
@@ -337,6 +363,7 @@ class Simulation:
         if workers < 1:
             raise ValueError("worker count must be >= 1")
         self.layout, self.bc_mode, self.variant = layout, bc, variant
+        self.device, self.math = device, math
         if _handle is None:
             h = C.c_void_p()
             _check(lib.d2q37_create(LAYOUTS[layout], lx, ly, vl, device, C.byref(h)))
@@ -384,6 +411,7 @@ class Simulation:
     # configuration
     def set_math(self, math: str):
         _check(_load().d2q37_set_math(self._h, MATHS[math]))
+        self.math = math
 
     def set_model(self, mdl: Model):
         self.model = mdl

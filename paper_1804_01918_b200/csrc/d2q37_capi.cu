@@ -178,7 +178,9 @@ void fill_offsets(d2q37_lattice* h, int corrupt = -1) {
     finish_offsets(h->off_pull, g.pstride, corrupt < 0);
 }
 
-int upload_model(d2q37_lattice* h, const d2q37_model* m) {
+// Validates a host model against the device velocity set and the symmetry the
+// FAST kernels rely on, and packs it into kernel parameters.
+int model_params(const d2q37_model* m, ModelParams* mp) {
     for (int p = 0; p < kNpop; ++p)
         if (m->cx[p] != cx_of(p) || m->cy[p] != cy_of(p))
             return fail(D2Q37_ERR_INVALID_ARGUMENT,
@@ -189,7 +191,7 @@ int upload_model(d2q37_lattice* h, const d2q37_model* m) {
             const double v = m->eq[i * kNmom + k];
             if (eq_structural_zero(i, k) && v != 0.0)
                 return fail(D2Q37_ERR_INVALID_ARGUMENT, "Hermite table entry (%d,%d) must be zero", i, k);
-            h->mp.eq[i][k] = v;
+            mp->eq[i][k] = v;
         }
     // The FAST kernels evaluate one Hermite row per (+-a, +-b) group and take
     // the other rows' signs from the parity of each coefficient; require that
@@ -206,8 +208,15 @@ int upload_model(d2q37_lattice* h, const d2q37_model* m) {
                                 "Hermite table rows %d and %d are not sign-symmetric at term %d", i, j, k);
             }
         }
-    for (int i = 0; i < kNpop; ++i) h->mp.w[i] = m->w[i];
-    h->mp.t0 = m->t0;
+    for (int i = 0; i < kNpop; ++i) mp->w[i] = m->w[i];
+    mp->t0 = m->t0;
+    return D2Q37_OK;
+}
+
+int upload_model(d2q37_lattice* h, const d2q37_model* m) {
+    ModelParams mp{};
+    RET(model_params(m, &mp));
+    h->mp = mp;
     ++h->model_gen;  // captured step graphs carry the old constants
     return D2Q37_OK;
 }
@@ -1108,6 +1117,78 @@ int d2q37_moments(d2q37_lattice* h, double out[4]) {
     for (int i = 0; i < 4; ++i) out[i] = 0.0;
     for (int x = 0; x < h->g.lx; ++x)
         for (int i = 0; i < 4; ++i) out[i] += part[size_t(x) * 4 + i];
+    return D2Q37_OK;
+}
+
+int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_in, double* host_out, size_t n,
+                       double omega, int nsteps, int math, int device) {
+    if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");
+    if (!host_in || !host_out || n != size_t(kNpop) * lx * ly)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "canonical array size mismatch");
+    if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+    if (math != D2Q37_MATH_FAST && math != D2Q37_MATH_STRICT)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown math mode");
+    d2q37_model local;
+    if (!m) {
+        build_model(&local);
+        m = &local;
+    }
+    ModelParams mp{};
+    RET(model_params(m, &mp));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(D2Q37_ERR_INVALID_ARGUMENT, "no CUDA device %d", device);
+    DeviceGuard dg(device);
+    const size_t bytes = n * sizeof(double);
+    double *a = nullptr, *b = nullptr;
+    int* flag = nullptr;
+    int rc = D2Q37_OK;
+    cudaStream_t st = nullptr;
+    auto run = [&]() -> int {
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaMalloc(&a, bytes));
+        CK(cudaMalloc(&b, bytes));
+        CK(cudaMalloc(&flag, sizeof(int)));
+        CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+        CK(cudaMemcpyAsync(a, host_in, bytes, cudaMemcpyHostToDevice, st));
+        for (int i = 0; i < nsteps; ++i)  // a -> b (propagate) -> a (collide)
+            CK(launch_scalar_step(a, b, a, lx, ly, mp, omega, math == D2Q37_MATH_STRICT, flag, st));
+        int hflag = 0;
+        CK(cudaMemcpyAsync(host_out, a, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hflag) return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
+        return D2Q37_OK;
+    };
+    rc = run();
+    if (a) cudaFree(a);
+    if (b) cudaFree(b);
+    if (flag) cudaFree(flag);
+    if (st) cudaStreamDestroy(st);
+    return rc;
+}
+
+int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst) {
+    RET(check_handle(src));
+    RET(check_handle(dst));
+    if (src == dst) return fail(D2Q37_ERR_INVALID_ARGUMENT, "convert: source and destination alias");
+    int gs[6], gd[6];
+    RET(d2q37_geometry(src, gs));
+    RET(d2q37_geometry(dst, gd));
+    if (gs[0] != gd[0] || gs[1] != gd[1]) return fail(D2Q37_ERR_INVALID_ARGUMENT, "convert: geometry mismatch");
+    if (src->device != dst->device) return fail(D2Q37_ERR_INVALID_ARGUMENT, "convert: lattices on different devices");
+    DeviceGuard dg(src->device);
+    const size_t plane = size_t(src->g.lx) * src->g.ly;
+    double* tmp = nullptr;
+    CK(cudaStreamSynchronize(dst->stream));
+    CK(cudaMallocAsync(&tmp, plane * sizeof(double), src->stream));
+    for (int p = 0; p < kNpop; ++p) {
+        CK(launch_gather(src->buf[src->cur], src->g, tmp, p, src->stream));
+        CK(launch_scatter(dst->buf[dst->cur], dst->g, tmp, p, src->stream));
+    }
+    CK(cudaFreeAsync(tmp, src->stream));
+    CK(cudaStreamSynchronize(src->stream));
+    dst->time_step = src->time_step;
     return D2Q37_OK;
 }
 

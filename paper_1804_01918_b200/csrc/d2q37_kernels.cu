@@ -248,6 +248,41 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
 }
 
 // ---------------------------------------------------------------------------
+// Scalar device reference (validation.hpp:15-42, validation.cpp:13-38): a
+// halo-free canonical array ((p*lx + x)*ly + y, dump.hpp:19-21) stepped with
+// explicit modulo indexing and no layout machinery, so that run_validation
+// can point a divergence at a layout or offset bug.  One thread per site.
+
+__global__ void __launch_bounds__(256) k_scalar_propagate(const double* __restrict__ in, double* __restrict__ out,
+                                                          int lx, int ly) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)lx * ly) return;
+    const int x = int(t / ly), y = int(t - (long long)x * ly);
+    const long long plane = (long long)lx * ly;
+    for (int p = 0; p < kNpop; ++p) {
+        const int xs = ((x - cx_of(p)) % lx + lx) % lx;
+        const int ys = ((y - cy_of(p)) % ly + ly) % ly;
+        out[p * plane + (long long)x * ly + y] = in[p * plane + (long long)xs * ly + ys];
+    }
+}
+
+template <bool STRICT>
+__global__ void __launch_bounds__(256) k_scalar_collide(const double* __restrict__ in, double* __restrict__ out,
+                                                        int lx, int ly, ModelParams mp, double omega,
+                                                        int* __restrict__ flag) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long plane = (long long)lx * ly;
+    if (t >= plane) return;
+    double f[kNpop];
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) f[p] = in[p * plane + t];
+    const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
+    if (bad) *flag = 1;
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) out[p * plane + t] = f[p];
+}
+
+// ---------------------------------------------------------------------------
 // Edge (bc) kernel.  Thread t < nrows covers the ghost rows of every padded
 // column (6 rows x vl lanes per (p, X)); t >= nrows covers the physical rows of
 // the 6 ghost columns.  Every ghost slot is computed from its final physical
@@ -591,6 +626,19 @@ cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, 
                            int ly_global, cudaStream_t s) {
     (void)cudaGetLastError();
     k_init_rt<<<dim3((g.ly + 127) / 128, g.lx), 128, 0, s>>>(buf, g, mp, seed, y0, ly_global);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int lx, int ly, const ModelParams& mp,
+                               double omega, bool strict, int* flag, cudaStream_t s) {
+    const long long n = (long long)lx * ly;
+    const unsigned blocks = unsigned((n + 255) / 256);
+    (void)cudaGetLastError();
+    k_scalar_propagate<<<blocks, 256, 0, s>>>(in, tmp, lx, ly);
+    if (strict)
+        k_scalar_collide<true><<<blocks, 256, 0, s>>>(tmp, out, lx, ly, mp, omega, flag);
+    else
+        k_scalar_collide<false><<<blocks, 256, 0, s>>>(tmp, out, lx, ly, mp, omega, flag);
     return cudaGetLastError();
 }
 

@@ -81,6 +81,10 @@ cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed,
                           cudaStream_t s);
 cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, unsigned long long seed, int y0,
                            int ly_global, cudaStream_t s);
+// One scalar reference step (propagate then collide, periodic x and y) on a
+// halo-free canonical array: in -> tmp -> out (validation.cpp:13-38).
+cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int lx, int ly, const ModelParams& mp,
+                               double omega, bool strict, int* flag, cudaStream_t s);
 cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
 
 }  // namespace d2q37

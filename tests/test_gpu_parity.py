@@ -584,3 +584,68 @@ def test_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, varia
     ref.bc("periodic")
     ref.propagate_only()
     assert np.array_equal(s.dump(which=1), ref.dump(which=1))
+
+
+# --------------------------------------------------------------------------- run_validation / convert
+
+def test_scalar_reference_strict_bitwise_vs_oracle(gpu, lbm, po):
+    """The device scalar reference of run_validation in STRICT math is the no-contraction
+    oracle step (validation.cpp:13-38) bit for bit; FAST is within the 1e-12 bar."""
+    init = lbm.make_lattice("random", 20, 36, seed=8)
+    want, bad = po.orc_step(init, 1.3, 4, po.BC_PERIODIC)
+    assert not bad
+    assert np.array_equal(lbm.scalar_steps(init, 1.3, 4, math="strict"), want)
+    assert max_rel(lbm.scalar_steps(init, 1.3, 4, math="fast"), want) <= 1e-12
+
+
+@pytest.mark.parametrize("math", ["fast", "strict"])
+def test_run_validation_default_options_pass(gpu, lbm, math):
+    """validation.cpp:73-123 with ValidationOptions' defaults: 2 geometries x 4 layouts x
+    vl {1,2,4,8}, 10 steps -- every layout path equals the scalar reference bit for bit."""
+    from paper_1804_01918_b200 import validation as v
+
+    rep = v.run_validation(v.ValidationOptions(math=math))
+    assert len(rep.cases) == 32
+    assert rep.passed, [c for c in rep.cases if not c.passed][:3]
+    import io
+    buf = io.StringIO()
+    v.print_report(rep, buf)
+    lines = buf.getvalue().splitlines()
+    assert lines[0] == "pass  16x32  aos  vl=1"
+    assert lines[-1] == "validation passed (32 cases)"
+
+
+def test_run_validation_detects_corrupted_offsets(gpu, lbm):
+    """test_validation.cpp:49-67: a corrupted offset-table entry must fail every case (the
+    collide spreads the error to every population of the sites it reaches)."""
+    from paper_1804_01918_b200 import validation as v
+
+    rep = v.run_validation(v.ValidationOptions(geometries=[(16, 32)], vls=[1, 4], steps=1,
+                                               corrupt_population=7))
+    assert not rep.passed
+    assert all(not c.passed and c.divergence is not None for c in rep.cases)
+
+
+@pytest.mark.parametrize("src_layout,src_vl", [("caosoa", 32), ("soa", 1)])
+def test_convert_between_layouts(gpu, lbm, src_layout, src_vl):
+    """convert(src, to) (layout.cpp:105-116): the physical sites move bit for bit into any
+    other layout, and stepping the converted lattice equals stepping the source."""
+    lx, ly = 24, 192
+    src = sim_of(lbm, src_layout, lx, ly, src_vl, bc="wall")
+    src.load(lbm.make_lattice("random", lx, ly, seed=12))
+    src.step(1.2, 2)
+    state = src.dump()
+    for layout, vl in (("aos", 1), ("soa", 1), ("csoa", 8), ("caosoa", 4), ("caosoa", 32)):
+        dst = lbm.convert(src, layout, vl)
+        assert (dst.layout, dst.lx, dst.ly) == (layout, lx, ly)
+        assert np.array_equal(dst.dump(), state)
+        dst.step(1.2, 3)
+        dst.sync()
+        ref = sim_of(lbm, src_layout, lx, ly, src_vl, bc="wall")  # steps are layout-invariant bit for bit
+        ref.load(state)
+        ref.step(1.2, 3)
+        assert np.array_equal(dst.dump(), ref.dump())
+        dst.close()
+    with pytest.raises(ValueError, match="geometry mismatch"):
+        other = sim_of(lbm, "soa", lx, ly * 2)
+        lbm._check(lbm._load().d2q37_convert(src._h, other._h))

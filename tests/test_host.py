@@ -184,3 +184,22 @@ int main() {
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert float(r.stdout) == lbm.model().t0
+
+
+def test_validation_first_divergence_order_and_defaults(lbm):
+    """first_divergence scans x, then y, then p (validation.cpp:59-70); the options default to
+    the reference's ValidationOptions (validation.hpp:44-58)."""
+    from paper_1804_01918_b200 import validation as v
+
+    want = np.zeros((37, 3, 4))
+    got = want.copy()
+    assert v.first_divergence(got, want) is None
+    got[5, 2, 0] = 1.0
+    got[30, 1, 3] = 2.0
+    got[2, 1, 3] = -0.0  # a sign bit differs: bitwise compare catches it
+    d = v.first_divergence(got, want)
+    assert (d.x, d.y, d.p, d.got, d.want) == (1, 3, 2, -0.0, 0.0)
+    o = v.ValidationOptions()
+    assert o.geometries == [(16, 32), (64, 128)] and o.vls == [1, 2, 4, 8]
+    assert o.layouts == ["aos", "soa", "csoa", "caosoa"] and (o.steps, o.omega, o.seed) == (10, 1.0, 12345)
+    assert o.corrupt_population == -1
