@@ -139,6 +139,23 @@ class Dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def min(self, v: float) -> float:
+        if not self.pg:
+            return v
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return float(t.item())
+
+    def all_gather_bytes(self, b: bytes) -> list:
+        if not self.pg:
+            return [b]
+        import torch.distributed as dist
+        out = [None] * self.world
+        dist.all_gather_object(out, b)
+        return out
+
     def bcast_bytes(self, b: bytes | None) -> bytes:
         if not self.pg:
             return b
@@ -262,17 +279,22 @@ def bench_config0(lbm, warmup: int) -> dict:
 
 
 def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
-    """The multi-GPU schedule on one GPU: a 1-rank NCCL ring (pack -> ncclSend/Recv to self ->
-    remote edge, interior/boundary split) vs the plain single-domain step, same lattice.
+    """The multi-GPU schedules on one GPU: a 1-rank NCCL ring (y-major columns through
+    ncclSend/Recv to self) and a 1-rank P2P ring (the step kernel pushes its face columns into the
+    ghost columns through peer memory, step counters in device memory) vs the plain single-domain
+    step, same lattice.
     ly = 4096 is the per-GPU slab of the 8-GPU strong-scaling config (4096 x 32768 / 8)."""
     import torch  # noqa: F401  (NCCL comes from torch's libnccl.so.2)
     out = {}
-    for name in ("single_domain", "nccl_self_ring"):
+    for name in ("single_domain", "nccl_self_ring", "p2p_self_ring"):
         if name == "single_domain":
             sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="periodic")
-        else:
+        elif name == "nccl_self_ring":
             sim = lbm.Simulation.slab(layout, LX, ly, vl, device=0, rank=0, nranks=1,
                                       nccl_id=lbm.nccl_unique_id(), bc="periodic")
+        else:
+            sim = lbm.Simulation.slab(layout, LX, ly, vl, device=0, rank=0, nranks=1, bc="periodic",
+                                      transport="p2p")
         sim.init_rt_device(SEED)
         sim.step(OMEGA, warmup)
         ms = time_steps(sim, steps, lambda: sim.step(OMEGA, 1, sync=False))
@@ -290,7 +312,9 @@ def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
         out[name]["launches_per_step"] = {k: v[1] / 10 for k, v in kt.items() if v[1]}
         sim.close()
     out["schedule_overhead"] = out["nccl_self_ring"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
-    out["config"] = f"{LX}x{ly} {layout}{vl}, periodic y through NCCL to self vs local wrap, {steps} steps"
+    out["p2p_schedule_overhead"] = out["p2p_self_ring"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
+    out["config"] = (f"{LX}x{ly} {layout}{vl}, periodic y through NCCL to self / through the peer-memory "
+                     f"push to self vs local wrap, {steps} steps")
     return out
 
 
@@ -360,6 +384,38 @@ def run_reference(args, dist):
 
 # --------------------------------------------------------------------------- main arm
 
+def make_slab(lbm, args, dist: Dist, dev: int, ly_global: int):
+    """This rank's slab: the peer-memory P2P transport for site-major layouts (falls back to NCCL
+    if the ranks cannot map each other's memory), NCCL otherwise or when asked."""
+    rank, n = dist.rank, dist.world
+    if args.transport == "p2p" and args.layout in ("aos", "caosoa"):
+        sim, blob = None, b""
+        try:
+            sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
+                                      bc="wall", variant=args.variant, transport="p2p")
+            blob = sim.p2p_blob()
+        except Exception as e:  # noqa: BLE001 -- reported, then NCCL
+            print(f"[rank {rank}] p2p slab unavailable ({e}); using NCCL", file=sys.stderr, flush=True)
+        ok = dist.min(1.0 if blob else 0.0) > 0.5
+        if ok:  # every rank reaches the collectives below
+            blobs = dist.all_gather_bytes(blob)
+            try:
+                sim.p2p_connect(blobs[(rank - 1) % n], blobs[(rank + 1) % n])
+                conn = 1.0
+            except Exception as e:  # noqa: BLE001
+                print(f"[rank {rank}] p2p connect failed ({e}); using NCCL", file=sys.stderr, flush=True)
+                conn = 0.0
+            ok = dist.min(conn) > 0.5
+        if ok:
+            return sim, "p2p"
+        if sim is not None:
+            sim.close()
+    uid = dist.bcast_bytes(lbm.nccl_unique_id() if rank == 0 else None)
+    sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
+                              nccl_id=uid, bc="wall", variant=args.variant)
+    return sim, "nccl"
+
+
 def run_b200(args, dist: Dist):
     import torch
     import paper_1804_01918_b200 as lbm
@@ -375,12 +431,11 @@ def run_b200(args, dist: Dist):
     rank = dist.rank
 
     # ---- lattice + init: each rank generates its slab of the RT state on the device
+    transport = None
     if n == 1:
         sim = lbm.Simulation(args.layout, LX, ly_local, args.vl, device=dev, bc="wall", variant=args.variant)
     else:
-        uid = dist.bcast_bytes(lbm.nccl_unique_id() if rank == 0 else None)
-        sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
-                                  nccl_id=uid, bc="wall", variant=args.variant)
+        sim, transport = make_slab(lbm, args, dist, dev, ly_global)
     sim.init_rt_device(SEED)
 
     clocks = ClockSampler(dev)
@@ -427,7 +482,8 @@ def run_b200(args, dist: Dist):
                        "lx": LX, "ly_per_gpu": ly_local, "ly_global": ly_global, "layout": args.layout,
                        "vl": args.vl if args.layout in ("csoa", "caosoa") else 1, "variant": args.variant,
                        "l2": "inputs larger than L2 (2 x 19.9 GB lattice per GPU vs 126 MB L2): no flush needed",
-                       "parallelism": f"y-slab x{n}" if n > 1 else "single GPU"},
+                       "parallelism": f"y-slab x{n}" if n > 1 else "single GPU",
+                       "halo_transport": transport},
             "roofline": roofline, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
             "exposed_halo_ms_per_step": halo_ms}
 
@@ -527,6 +583,8 @@ def main():
     ap.add_argument("--vl", type=int, default=32)
     ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU (weak scaling)")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1 halo transport: peer-memory push from the step kernel (site-major layouts), or NCCL")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: --ly rows per GPU; strong: 4096 x 32768 split over the GPUs (config 4)")
     ap.add_argument("--e2e-steps", type=int, default=200)

@@ -30,6 +30,7 @@ extern "C" {
 #define D2Q37_NMOM 14
 #define D2Q37_HALO 3
 #define D2Q37_NCCL_ID_BYTES 128
+#define D2Q37_P2P_BLOB_BYTES 256
 
 /* Status codes.  Reference exception types:
  *   INVALID_ARGUMENT  <- std::invalid_argument / std::out_of_range
@@ -162,6 +163,22 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst);
  * math selects the collide arithmetic (compare like with like). */
 int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_in, double* host_out, size_t n,
                        double omega, int nsteps, int math, int device);
+
+/* Multi-GPU y-slabs without NCCL (site-major layouts, y-major storage): the
+ * fused step kernel stores its face columns straight into the neighbours'
+ * ghost columns through NVLink peer memory, and per-step counters in peer
+ * memory order the ranks.  create -> export a 256-byte
+ * blob -> exchange blobs (any host channel, e.g. torch.distributed) ->
+ * connect(lo neighbour's blob, hi neighbour's blob); a 1-rank ring connects
+ * to its own blob.  Neighbours in this process are used directly, others are
+ * mapped with CUDA IPC.  All ranks must issue the same sequence of steps and
+ * state-changing verbs (like NCCL collectives); a rank that waits more than
+ * 10 s for a neighbour reports D2Q37_ERR_NCCL from d2q37_sync. */
+int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
+                          d2q37_lattice** out);
+int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]);
+int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BYTES],
+                      const unsigned char hi[D2Q37_P2P_BLOB_BYTES]);
 
 /* Global sums over the physical sites of the state buffer (prv):
  * out = {mass, x-momentum, y-momentum, energy sum |c|^2 f}; deterministic

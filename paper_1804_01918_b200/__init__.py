@@ -34,7 +34,7 @@ import numpy as np
 __all__ = [
     "NPOP", "Model", "Simulation", "SlabGroup", "NonPhysicalError", "model", "mlups",
     "propagate_gbps", "collide_gflops", "make_lattice", "library_path", "nccl_unique_id",
-    "COLLIDE_FLOPS_PER_SITE", "__version__", "convert", "scalar_steps",
+    "COLLIDE_FLOPS_PER_SITE", "__version__", "convert", "scalar_steps", "p2p_ring", "step_slabs",
 ]
 __version__ = "0.1.0"
 
@@ -135,6 +135,9 @@ def _load():
         "d2q37_set_profiling": (i, [vp, i]),
         "d2q37_kernel_times": (i, [vp, _dp, P(C.c_long)]),
         "d2q37_convert": (i, [vp, vp]),
+        "d2q37_create_slab_p2p": (i, [i, i, i, i, i, i, i, P(vp)]),
+        "d2q37_p2p_export": (i, [vp, C.c_char_p]),
+        "d2q37_p2p_connect": (i, [vp, C.c_char_p, C.c_char_p]),
         "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
     }
     for name, (res, args) in sig.items():
@@ -341,6 +344,30 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def p2p_ring(layout: str, lx: int, ly: int, vl: int = 1, nslabs: int = 2, *, device: int = 0,
+             bc: str = "periodic", variant: str = "fused", math: str = "fast") -> list:
+    """``nslabs`` P2P y-slabs of one lattice in this process, connected as a ring (the same
+    peer-memory halo protocol as one slab per GPU; here every neighbour is in this process).
+    Step them together with :func:`step_slabs`."""
+    slabs = [Simulation.slab(layout, lx, ly, vl, device=device, rank=r, nranks=nslabs, bc=bc, variant=variant,
+                             math=math, transport="p2p")
+             for r in range(nslabs)]
+    if nslabs > 1:
+        blobs = [s.p2p_blob() for s in slabs]
+        for r, s in enumerate(slabs):
+            s.p2p_connect(blobs[(r - 1) % nslabs], blobs[(r + 1) % nslabs])
+    return slabs
+
+
+def step_slabs(slabs, omega: float, n: int = 1):
+    """Advance in-process slabs in lockstep (one step each, rank order), then sync them."""
+    for _ in range(n):
+        for s in slabs:
+            s.step(omega, 1, sync=False)
+    for s in slabs:
+        s.sync()
+
+
 # --------------------------------------------------------------------------- lattice
 
 class Simulation:
@@ -381,15 +408,48 @@ class Simulation:
     @classmethod
     def slab(cls, layout: str, lx: int, ly_global: int, vl: int = 1, *, device: int = 0, rank: int = 0,
              nranks: int = 1, nccl_id: bytes | None = None, bc: str = "periodic", variant: str = "fused",
-             math: str = "fast", mdl: Model | None = None) -> "Simulation":
-        """Rank `rank` of an `nranks`-GPU y-slab decomposition (d2q37_create_slab, NCCL halos)."""
+             math: str = "fast", mdl: Model | None = None, transport: str = "nccl",
+             exchange=None) -> "Simulation":
+        """Rank `rank` of an `nranks`-GPU y-slab decomposition.
+
+        ``transport="nccl"`` (d2q37_create_slab): NCCL send/recv halos; needs ``nccl_id``.
+        ``transport="p2p"`` (d2q37_create_slab_p2p, site-major layouts): the step kernel pushes
+        its face columns into the neighbours' ghost columns through peer memory.
+        ``exchange(blob) -> list of every rank's blob`` (e.g. an all_gather over
+        torch.distributed) connects the ranks; with ``nranks == 1`` and no ``exchange`` the slab
+        is a 1-rank ring connected to itself.  Without either, call ``p2p_blob`` /
+        ``p2p_connect`` yourself."""
         h = C.c_void_p()
-        _check(_load().d2q37_create_slab(LAYOUTS[layout], lx, ly_global, vl, device, rank, nranks,
-                                         nccl_id, C.byref(h)))
+        if transport == "p2p":
+            _check(_load().d2q37_create_slab_p2p(LAYOUTS[layout], lx, ly_global, vl, device, rank, nranks,
+                                                 C.byref(h)))
+        elif transport == "nccl":
+            _check(_load().d2q37_create_slab(LAYOUTS[layout], lx, ly_global, vl, device, rank, nranks,
+                                             nccl_id, C.byref(h)))
+        else:
+            raise ValueError(f"unknown transport: {transport}")
         sim = cls(layout, lx, ly_global // nranks, vl, device=device, bc=bc, variant=variant, math=math,
                   mdl=mdl, _handle=h)
         sim._owned = True
+        sim.rank, sim.nranks, sim.transport = rank, nranks, transport
+        if transport == "p2p":
+            if exchange is not None:
+                blobs = list(exchange(sim.p2p_blob()))
+                sim.p2p_connect(blobs[(rank - 1) % nranks], blobs[(rank + 1) % nranks])
+            elif nranks == 1:
+                b = sim.p2p_blob()
+                sim.p2p_connect(b, b)
         return sim
+
+    def p2p_blob(self) -> bytes:
+        """This slab's 256-byte connection blob (d2q37_p2p_export)."""
+        buf = C.create_string_buffer(256)
+        _check(_load().d2q37_p2p_export(self._h, buf))
+        return buf.raw
+
+    def p2p_connect(self, lo_blob: bytes | None, hi_blob: bytes | None):
+        """Maps the lo / hi neighbours' buffers and step counters (d2q37_p2p_connect)."""
+        _check(_load().d2q37_p2p_connect(self._h, lo_blob, hi_blob))
 
     def slab_info(self):
         out = (C.c_int * 4)()

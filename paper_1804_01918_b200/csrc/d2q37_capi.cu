@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "d2q37_b200.h"
 #include "d2q37_device.cuh"
 #include "d2q37_internal.h"
@@ -26,6 +28,7 @@ thread_local std::string g_last_error;
 constexpr int kTransportNone = 0;
 constexpr int kTransportNccl = 1;
 constexpr int kTransportGroup = 2;
+constexpr int kTransportP2P = 3;  // y-major slabs pushing halos through NVLink peer memory
 constexpr int kEventRing = 64;
 constexpr int kGraphSteps = 10;  // even, so a replay leaves the state in the same buffer
 
@@ -81,6 +84,15 @@ struct d2q37_lattice {
     std::vector<ProfEntry> prof_pending;
     std::vector<cudaEvent_t> prof_free;
     std::vector<d2q37_lattice*> group;  // transport == group: all slabs, in rank order
+    // P2P transport: the neighbours' state buffers and step counters, mapped
+    // into this process (CUDA IPC across processes, direct pointers within one)
+    unsigned long long* d_seq = nullptr;        // [0]: last step of the lo neighbour, [1]: of the hi one
+    double* peer_buf[2][2] = {};                // [lo / hi][buffer]
+    unsigned long long* peer_seq_slot[2] = {};  // my slot in the lo / hi neighbour's counters
+    std::vector<void*> ipc_mapped;              // opened with cudaIpcOpenMemHandle
+    unsigned long long p2p_seq = 0;             // steps (and primes) issued
+    bool p2p_connected = false;
+    bool p2p_dirty = true;  // prv changed outside a step: ghost columns must be re-primed
     // cached CUDA graph of kGraphSteps single-domain steps (d2q37_step)
     struct StepGraph {
         cudaGraphExec_t exec = nullptr;
@@ -304,6 +316,8 @@ void free_lattice(d2q37_lattice* h) {
     for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->send_lo, h->send_hi, h->recv_lo, h->recv_hi})
         if (p) cudaFree(p);
     if (h->d_flag) cudaFree(h->d_flag);
+    if (h->d_seq) cudaFree(h->d_seq);
+    for (void* p : h->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (h->h_flag) cudaFreeHost(h->h_flag);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
     if (h->ev_recv) cudaEventDestroy(h->ev_recv);
@@ -384,7 +398,9 @@ Segments all_sites(const DevGeo& g) {
 // A single rank with an NCCL communicator (d2q37_create_slab with nranks = 1
 // and an id) routes its periodic y wrap through NCCL to itself: the full
 // multi-GPU schedule on one GPU.
-bool local_only(const d2q37_lattice* h) { return h->nranks == 1 && h->transport != kTransportNccl; }
+bool local_only(const d2q37_lattice* h) {
+    return h->nranks == 1 && h->transport != kTransportNccl && h->transport != kTransportP2P;
+}
 
 int face_lo_of(const d2q37_lattice* h, int bc) {
     if (local_only(h)) return bc == D2Q37_BC_WALL ? kFaceWall : kFacePeriodic;
@@ -736,6 +752,117 @@ int ymajor_step_nccl_unfused(d2q37_lattice* h, double omega, int bc) {
     return step_local(h, omega, D2Q37_UNFUSED, bc);
 }
 
+// ---- P2P y-major slabs: halos pushed through peer memory ------------------
+//
+// Step k (counter seq = k) of every rank, with ping-pong buffers in lockstep:
+//   compute stream: interior columns (no ghost reads, no remote writes)
+//   halo stream:    wait until both neighbours finished step k-1 (their
+//                   counters >= seq-1: my ghost columns hold their step k-1
+//                   faces, and they no longer read the ghost columns of the
+//                   buffer I am about to write) -> the 3 + 3 face columns, whose
+//                   fused kernel also stores its results into the neighbours'
+//                   next buffers (ghost columns) over NVLink -> signal seq.
+// No NCCL, no pack, no exchange buffers: the halo travels with the kernel's
+// own stores.  A prime (after load / init / swap) pushes the current face
+// columns with peer copies under the same counter protocol.
+
+size_t face_bytes(const d2q37_lattice* h) { return ycols_count(h) * sizeof(double); }
+
+double* peer_cols(const d2q37_lattice* h, int side, int buffer, int X) {
+    return h->peer_buf[side][buffer] + h->g.lead + (long long)X * h->g.cstride;
+}
+
+int p2p_wait(d2q37_lattice* h, int bc, unsigned long long target) {
+    CK(launch_p2p_wait(h->d_seq, face_lo_of(h, bc) == kFaceRemote, face_hi_of(h, bc) == kFaceRemote, target,
+                       h->d_flag, h->halo_stream));
+    return D2Q37_OK;
+}
+
+int p2p_signal(d2q37_lattice* h, int bc, unsigned long long value) {
+    CK(launch_p2p_signal(face_lo_of(h, bc) == kFaceRemote ? h->peer_seq_slot[0] : nullptr,
+                         face_hi_of(h, bc) == kFaceRemote ? h->peer_seq_slot[1] : nullptr, value, h->halo_stream));
+    return D2Q37_OK;
+}
+
+// Pushes the current state's face columns into the neighbours' current ghost
+// columns (peer copies), then signals; the next step waits for the neighbours'
+// pushes.  Invariant of the counters: a neighbour's counter >= s means its
+// operation s has finished both its pushes and its reads of its own ghost
+// columns, so waiting for s - 1 before writing into its buffers is safe.
+int p2p_prime(d2q37_lattice* h, int bc) {
+    const unsigned long long seq = ++h->p2p_seq;
+    const int lx = h->g.lx;
+    CK(cudaEventRecord(h->ev_start, h->stream));
+    CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
+    RET(p2p_wait(h, bc, seq - 1));
+    if (face_lo_of(h, bc) == kFaceRemote)  // my first columns -> lo neighbour's high ghost columns
+        CK(cudaMemcpyAsync(peer_cols(h, 0, h->cur, lx + kHalo), ycols(h, kHalo), face_bytes(h),
+                           cudaMemcpyDeviceToDevice, h->halo_stream));
+    if (face_hi_of(h, bc) == kFaceRemote)  // my last columns -> hi neighbour's low ghost columns
+        CK(cudaMemcpyAsync(peer_cols(h, 1, h->cur, 0), ycols(h, lx), face_bytes(h), cudaMemcpyDeviceToDevice,
+                           h->halo_stream));
+    RET(p2p_signal(h, bc, seq));
+    RET(p2p_wait(h, bc, seq));  // the neighbours' pushes into my ghost columns
+    CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
+    h->p2p_dirty = false;
+    return D2Q37_OK;
+}
+
+int ymajor_step_p2p(d2q37_lattice* h, double omega, int variant, int bc) {
+    if (!h->p2p_connected) return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p slab is not connected to its neighbours");
+    if (h->p2p_dirty) RET(p2p_prime(h, bc));
+    if (variant != D2Q37_FUSED) {
+        // unfused: push the faces (counter c1), run the local verbs, then signal c1 + 1 once
+        // they are done reading the ghost columns -- the state stays in the same buffer, so a
+        // neighbour's next push must not land while propagate is still reading
+        RET(p2p_prime(h, bc));
+        RET(step_local(h, omega, D2Q37_UNFUSED, bc));
+        const unsigned long long done = ++h->p2p_seq;
+        CK(cudaEventRecord(h->ev_start, h->stream));
+        CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
+        RET(p2p_signal(h, bc, done));
+        return D2Q37_OK;
+    }
+    const unsigned long long seq = ++h->p2p_seq;
+    const Faces fc = step_faces(h, bc);
+    const bool lo_r = face_lo_of(h, bc) == kFaceRemote, hi_r = face_hi_of(h, bc) == kFaceRemote;
+    CK(cudaEventRecord(h->ev_start, h->stream));
+    CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
+    RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, ycols_interior(h, bc), 1, fc));
+    const int ring = h->ev_count % kEventRing;
+    CK(cudaEventRecord(h->ev_int[ring], h->stream));
+    {
+        OnStream on(h, h->halo_stream);
+        RET(p2p_wait(h, bc, seq - 1));
+        PeerStores ps{};
+        const long long span = (long long)h->g.lx * h->g.cstride;
+        if (lo_r) {
+            ps.lo = h->peer_buf[0][1 - h->cur];
+            ps.lo_shift = span;  // my column x -> the lo neighbour's ghost column lx + 3 + x
+        }
+        if (hi_r) {
+            ps.hi = h->peer_buf[1][1 - h->cur];
+            ps.hi_shift = -span;  // my column lx - 3 + c -> the hi neighbour's ghost column c
+        }
+        int nseg = 0;
+        const Segments bnd = ycols_boundary(h, bc, &nseg);
+        {
+            ProfScope prof(h, kProfBoundary);
+            CK(launch_collide(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, fc, h->mp, omega,
+                              h->math == D2Q37_MATH_STRICT, true, bnd, nseg, h->d_flag, h->stream, &ps));
+        }
+        RET(p2p_signal(h, bc, seq));
+        CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
+    }
+    CK(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
+    CK(cudaEventRecord(h->ev_wait[ring], h->stream));
+    ++h->ev_count;
+    h->cur = 1 - h->cur;
+    ++h->time_step;
+    return D2Q37_OK;
+}
+
 // Slab step, phase 1 (before the halos are needed): the interior rows, whose
 // pull stencil stays inside the slab (x wrap and lane shifts in-kernel).
 int slab_phase1(d2q37_lattice* h, double omega, int variant, int bc) {
@@ -774,6 +901,7 @@ int slab_phase2(d2q37_lattice* h, double omega, int variant, int bc) {
 }
 
 int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n, bool src_device) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 (prv) or 1 (nxt)");
     if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "from_canonical: dimension mismatch");
@@ -991,6 +1119,7 @@ int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
 }
 
 int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     RET(padded_verbs_ok(h, "write_padded"));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
@@ -1070,7 +1199,9 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
     }
     for (; s < nsteps; ++s) {
-        if (slab && h->g.tr) {
+        if (slab && h->transport == kTransportP2P) {
+            RET(ymajor_step_p2p(h, omega, variant, bc));
+        } else if (slab && h->g.tr) {
             RET(variant == D2Q37_FUSED ? ymajor_step_nccl(h, omega, bc) : ymajor_step_nccl_unfused(h, omega, bc));
         } else if (slab && h->halo_stream && variant == D2Q37_FUSED && can_split(h)) {
             RET(slab_step_overlapped(h, omega, bc));
@@ -1086,6 +1217,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
 }
 
 int d2q37_swap_buffers(d2q37_lattice* h) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     h->cur = 1 - h->cur;
     return D2Q37_OK;
@@ -1099,9 +1231,11 @@ int d2q37_sync(d2q37_lattice* h) {
     if (h->comm_stream) CK(cudaStreamSynchronize(h->comm_stream));
     if (h->halo_stream) CK(cudaStreamSynchronize(h->halo_stream));
     if (*h->h_flag) {
+        const int f = *h->h_flag;
         *h->h_flag = 0;
         CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        if (f & 2) return fail(D2Q37_ERR_NCCL, "p2p halo: a neighbour did not reach the step within 10 s");
         return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
     }
     return D2Q37_OK;
@@ -1189,6 +1323,7 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst) {
     CK(cudaFreeAsync(tmp, src->stream));
     CK(cudaStreamSynchronize(src->stream));
     dst->time_step = src->time_step;
+    dst->p2p_dirty = true;
     return D2Q37_OK;
 }
 
@@ -1212,6 +1347,7 @@ int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* pa
 }
 
 int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
     DeviceGuard dg(h->device);
@@ -1221,6 +1357,7 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
 }
 
 int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     DeviceGuard dg(h->device);
     CK(launch_init_rt(h->buf[h->cur], h->g, h->mp, seed, h->y0, h->ly_global, h->stream));
@@ -1307,6 +1444,7 @@ int d2q37_save_dump(d2q37_lattice* h, const char* path) {
 }
 
 int d2q37_load_dump(d2q37_lattice* h, const char* path) {
+    if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     if (!path) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null path");
     DeviceGuard dg(h->device);
@@ -1386,6 +1524,132 @@ int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, 
         if (rc != D2Q37_OK) return bail(fail(rc, "%s", why.c_str()));
     }
     h->transport = kTransportNccl;
+    return D2Q37_OK;
+}
+
+namespace {
+struct P2PBlob {
+    uint32_t magic;
+    int32_t pid, device, rank, nranks, layout, cols, rows, vl;
+    uint64_t buf0, buf1, seq;  // pointers, valid in the exporting process
+    cudaIpcMemHandle_t hbuf0, hbuf1, hseq;
+};
+static_assert(sizeof(P2PBlob) <= D2Q37_P2P_BLOB_BYTES, "P2P blob too large");
+constexpr uint32_t kP2PMagic = 0x50373344u;  // "D37P"
+}  // namespace
+
+int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
+                          d2q37_lattice** out) {
+    if (!site_major(layout))
+        return fail(D2Q37_ERR_UNSUPPORTED, "p2p slabs need a site-major layout (AoS, CAoSoA): y-major storage");
+    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks, true));
+    d2q37_lattice* h = *out;
+    auto bail = [&](int rc) {
+        d2q37_destroy(h);
+        *out = nullptr;
+        return rc;
+    };
+    DeviceGuard dg(device);
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&h->halo_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&h->d_seq, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(h->d_seq, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+        return bail(fail(D2Q37_ERR_CUDA, "p2p slab setup failed"));
+    for (int i = 0; i < kEventRing; ++i)
+        if (cudaEventCreate(&h->ev_int[i]) != cudaSuccess || cudaEventCreate(&h->ev_wait[i]) != cudaSuccess)
+            return bail(fail(D2Q37_ERR_CUDA, "p2p slab event creation failed"));
+    h->transport = kTransportP2P;
+    return D2Q37_OK;
+}
+
+int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]) {
+    RET(check_handle(h));
+    if (h->transport != kTransportP2P) return fail(D2Q37_ERR_INVALID_ARGUMENT, "not a p2p slab");
+    DeviceGuard dg(h->device);
+    P2PBlob b{};
+    b.magic = kP2PMagic;
+    b.pid = int32_t(getpid());
+    b.device = h->device;
+    b.rank = h->rank;
+    b.nranks = h->nranks;
+    b.layout = h->layout;
+    b.cols = h->g.lx;
+    b.rows = h->g.ly;
+    b.vl = h->g.vl;
+    b.buf0 = reinterpret_cast<uint64_t>(h->buf[0]);
+    b.buf1 = reinterpret_cast<uint64_t>(h->buf[1]);
+    b.seq = reinterpret_cast<uint64_t>(h->d_seq);
+    CK(cudaIpcGetMemHandle(&b.hbuf0, h->buf[0]));
+    CK(cudaIpcGetMemHandle(&b.hbuf1, h->buf[1]));
+    CK(cudaIpcGetMemHandle(&b.hseq, h->d_seq));
+    std::memset(blob, 0, D2Q37_P2P_BLOB_BYTES);
+    std::memcpy(blob, &b, sizeof b);
+    return D2Q37_OK;
+}
+
+namespace {
+// Maps a neighbour's allocation into this process: its own pointer when it
+// lives in this process, else a CUDA IPC mapping (reused if already open).
+int map_peer(d2q37_lattice* h, const P2PBlob& b, uint64_t ptr, const cudaIpcMemHandle_t& ipc, void** out) {
+    if (b.pid == int32_t(getpid())) {
+        if (b.device != h->device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(D2Q37_ERR_CUDA, "peer access to device %d: %s", b.device, cudaGetErrorString(e));
+            (void)cudaGetLastError();
+        }
+        *out = reinterpret_cast<void*>(ptr);
+        return D2Q37_OK;
+    }
+    CK(cudaIpcOpenMemHandle(out, ipc, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_mapped.push_back(*out);
+    return D2Q37_OK;
+}
+}  // namespace
+
+int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BYTES],
+                      const unsigned char hi[D2Q37_P2P_BLOB_BYTES]) {
+    RET(check_handle(h));
+    if (h->transport != kTransportP2P) return fail(D2Q37_ERR_INVALID_ARGUMENT, "not a p2p slab");
+    if (h->p2p_connected) return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p slab already connected");
+    DeviceGuard dg(h->device);
+    P2PBlob nb[2];
+    const unsigned char* in[2] = {lo, hi};
+    for (int side = 0; side < 2; ++side) {
+        if (!in[side]) continue;
+        std::memcpy(&nb[side], in[side], sizeof(P2PBlob));
+        const P2PBlob& b = nb[side];
+        if (b.magic != kP2PMagic) return fail(D2Q37_ERR_INVALID_ARGUMENT, "not a p2p slab blob");
+        if (b.layout != h->layout || b.vl != h->g.vl || b.rows != h->g.ly || b.cols != h->g.lx ||
+            b.nranks != h->nranks)
+            return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p neighbour has a different slab geometry");
+        const int want = side == 0 ? (h->rank - 1 + h->nranks) % h->nranks : (h->rank + 1) % h->nranks;
+        if (b.rank != want) return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p blob of rank %d, expected %d", b.rank, want);
+    }
+    // the same neighbour on both sides (2 ranks, or a 1-rank ring) is mapped once
+    for (int side = 0; side < 2; ++side) {
+        if (!in[side]) continue;
+        const P2PBlob& b = nb[side];
+        void *p0 = nullptr, *p1 = nullptr, *ps = nullptr;
+        if (side == 1 && in[0] && std::memcmp(&nb[0], &nb[1], sizeof(P2PBlob)) == 0) {
+            p0 = h->peer_buf[0][0];
+            p1 = h->peer_buf[0][1];
+            ps = h->peer_seq_slot[0] - 1;
+        } else {
+            RET(map_peer(h, b, b.buf0, b.hbuf0, &p0));
+            RET(map_peer(h, b, b.buf1, b.hbuf1, &p1));
+            RET(map_peer(h, b, b.seq, b.hseq, &ps));
+        }
+        h->peer_buf[side][0] = static_cast<double*>(p0);
+        h->peer_buf[side][1] = static_cast<double*>(p1);
+        // I am my lo neighbour's hi neighbour (its slot 1) and my hi neighbour's lo one (slot 0)
+        h->peer_seq_slot[side] = static_cast<unsigned long long*>(ps) + (side == 0 ? 1 : 0);
+    }
+    h->p2p_connected = true;
+    h->p2p_dirty = true;
     return D2Q37_OK;
 }
 
@@ -1507,7 +1771,7 @@ int d2q37_slab_info(const d2q37_lattice* h, int out[4]) {
 }
 
 double d2q37_exposed_halo_ms(const d2q37_lattice* h) {
-    if (!h || h->transport != kTransportNccl || h->ev_count == 0) return 0.0;
+    if (!h || (h->transport != kTransportNccl && h->transport != kTransportP2P) || h->ev_count == 0) return 0.0;
     DeviceGuard dg(h->device);
     cudaStreamSynchronize(h->stream);
     const int n = std::min(h->ev_count, kEventRing);

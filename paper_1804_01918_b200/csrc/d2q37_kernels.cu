@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __re
 template <bool STRICT, bool SHIFT, bool TR, int AM>
 __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, Faces fc,
-              ModelParams mp, double omega, Segments seg, int* __restrict__ flag) {
+              ModelParams mp, double omega, Segments seg, int* __restrict__ flag, PeerStores ps) {
     int x, q;
     if (!segment_site(g, seg, x, q)) return;
     const long long e = site_of(g, x + kHalo, q);
@@ -245,6 +245,50 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
     store_site<AM>(dst, e, g, off, f);
+    if (TR && SHIFT) {  // y-major slab: push the face columns into the neighbours' ghost columns
+        const bool lo = ps.lo && x < kHalo, hi = ps.hi && x >= g.lx - kHalo;
+        if (lo) store_site<kAddr64>(ps.lo, e + ps.lo_shift, g, off, f);
+        if (hi) store_site<kAddr64>(ps.hi, e + ps.hi_shift, g, off, f);
+        if (lo || hi) __threadfence_system();  // performed before the step counter is released
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P2P step counters (one thread each).
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+
+__global__ void k_p2p_wait(const unsigned long long* seq, int need_lo, int need_hi, unsigned long long target,
+                           int* flag) {
+    const unsigned long long t0 = global_ns();
+    for (;;) {
+        const bool lo = !need_lo || ld_acquire_sys(&seq[0]) >= target;
+        const bool hi = !need_hi || ld_acquire_sys(&seq[1]) >= target;
+        if (lo && hi) return;
+        if (global_ns() - t0 > 10000000000ULL) {  // a neighbour never arrived: report, do not hang
+            atomicOr(flag, 2);
+            return;
+        }
+        __nanosleep(256);
+    }
+}
+
+__global__ void k_p2p_signal(unsigned long long* lo_slot, unsigned long long* hi_slot, unsigned long long value) {
+    __threadfence_system();
+    if (lo_slot) st_release_sys(lo_slot, value);
+    if (hi_slot) st_release_sys(hi_slot, value);
 }
 
 // ---------------------------------------------------------------------------
@@ -548,9 +592,10 @@ cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, co
 namespace {
 template <bool S, bool SH, bool TR>
 void collide_am(dim3 grid, cudaStream_t s, const double* src, double* dst, const DevGeo& g, const Offsets& off,
-                const Faces& fc, const ModelParams& mp, double omega, const Segments& seg, int* flag) {
+                const Faces& fc, const ModelParams& mp, double omega, const Segments& seg, int* flag,
+                const PeerStores& ps) {
 #define D2Q37_COLL(AM) \
-    k_collide<S, SH, TR, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag)
+    k_collide<S, SH, TR, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag, ps)
     D2Q37_BY_ADDR(addr_mode(g, off), D2Q37_COLL)
 #undef D2Q37_COLL
 }
@@ -558,10 +603,11 @@ void collide_am(dim3 grid, cudaStream_t s, const double* src, double* dst, const
 
 cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
-                           int nseg, int* flag, cudaStream_t s) {
+                           int nseg, int* flag, cudaStream_t s, const PeerStores* peers) {
     if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
     const dim3 grid = stream_grid(g, seg, nseg);
-#define D2Q37_COLLIDE(S, SH, TR) collide_am<S, SH, TR>(grid, s, src, dst, g, off, fc, mp, omega, seg, flag)
+    const PeerStores ps = peers ? *peers : PeerStores{};
+#define D2Q37_COLLIDE(S, SH, TR) collide_am<S, SH, TR>(grid, s, src, dst, g, off, fc, mp, omega, seg, flag, ps)
     (void)cudaGetLastError();
     if (!shift) {  // no pull: the storage orientation does not matter
         if (strict)
@@ -583,6 +629,22 @@ cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, cons
     return cudaGetLastError();
 }
 #undef D2Q37_BY_ADDR
+
+cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
+                            int* flag, cudaStream_t s) {
+    if (!need_lo && !need_hi) return cudaSuccess;
+    (void)cudaGetLastError();
+    k_p2p_wait<<<1, 1, 0, s>>>(seq, need_lo ? 1 : 0, need_hi ? 1 : 0, target, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_signal(unsigned long long* lo_slot, unsigned long long* hi_slot, unsigned long long value,
+                              cudaStream_t s) {
+    if (!lo_slot && !hi_slot) return cudaSuccess;
+    (void)cudaGetLastError();
+    k_p2p_signal<<<1, 1, 0, s>>>(lo_slot, hi_slot, value);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s) {
     long long total = (long long)kNpop * g.px * 6 * (ep.lean ? 1 : g.vl);

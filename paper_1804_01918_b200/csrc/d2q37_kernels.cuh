@@ -68,11 +68,29 @@ struct PackParams {
     signed char hi_d[kMaxSlots], hi_p[kMaxSlots];  // entries of send_hi (cy_p >= d)
 };
 
+// Peer-memory halo push of a y-major slab (P2P transport): the fused kernel
+// also stores the updated sites of its 3 storage columns next to each remote
+// face straight into the neighbour's next buffer (its ghost columns), over
+// NVLink.  Element e of this slab lands at peer element e + shift.
+struct PeerStores {
+    double* lo;  // lo neighbour's next buffer (columns x < 3 go there), or null
+    double* hi;  // hi neighbour's next buffer (columns x >= lx - 3), or null
+    long long lo_shift, hi_shift;
+};
+
 cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                              const Segments& seg, int nseg, cudaStream_t s);
 cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
-                           int nseg, int* flag, cudaStream_t s);
+                           int nseg, int* flag, cudaStream_t s, const PeerStores* peers = nullptr);
+// P2P step protocol: wait until the step counters the neighbours wrote into
+// seq[0] (lo) / seq[1] (hi) reach `target` (system-scope acquire; gives up
+// after ~10 s and sets bit 2 of *flag); signal = system-scope release store
+// of `value` into the neighbours' counter slots.
+cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
+                            int* flag, cudaStream_t s);
+cudaError_t launch_p2p_signal(unsigned long long* lo_slot, unsigned long long* hi_slot, unsigned long long value,
+                              cudaStream_t s);
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s);
 cudaError_t launch_pack(const double* buf, const DevGeo& g, const PackParams& pp, cudaStream_t s);
 cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_plane, int p, cudaStream_t s);
