@@ -113,17 +113,26 @@ class ClockSampler:
 # --------------------------------------------------------------------------- distributed plumbing
 
 class Dist:
-    def __init__(self):
+    """torch.distributed plumbing (NCCL; gloo on CPU for the host-logic tests)."""
+
+    def __init__(self, backend: str | None = None):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = backend or os.environ.get("BENCH_DIST_BACKEND", "nccl")
         self.pg = False
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
             self.pg = True
+
+    def _dev(self) -> str:
+        return f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
 
     def barrier(self):
         if self.pg:
@@ -135,7 +144,7 @@ class Dist:
             return v
         import torch
         import torch.distributed as dist
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        t = torch.tensor([v], dtype=torch.float64, device=self._dev())
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -144,7 +153,7 @@ class Dist:
             return v
         import torch
         import torch.distributed as dist
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
+        t = torch.tensor([v], dtype=torch.float64, device=self._dev())
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return float(t.item())
 

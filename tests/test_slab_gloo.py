@@ -101,6 +101,108 @@ def _worker(rank, nranks, port, bc, steps, result_q):
         dist.destroy_process_group()
 
 
+def _exchange_faces(rank, nranks, slab, bc, lbm):
+    """The y-major / P2P message: the 3 face rows of all 37 populations each way.  Returns the
+    (lo, hi) ghost rows (3 each, lo ordered y = -3..-1, hi ordered y = n..n+2) or None at a wall."""
+    import torch
+
+    lo_peer, hi_peer = lbm.slab_neighbors(rank, nranks, bc)
+    n = slab.shape[2]
+    send_lo = np.ascontiguousarray(slab[:, :, 0:3])      # -> lo neighbour's high ghost rows
+    send_hi = np.ascontiguousarray(slab[:, :, n - 3:n])  # -> hi neighbour's low ghost rows
+    recv_lo, recv_hi = np.full_like(send_hi, np.nan), np.full_like(send_lo, np.nan)
+    t_lo, t_hi = torch.from_numpy(recv_lo), torch.from_numpy(recv_hi)
+    reqs = []
+    if hi_peer >= 0:
+        reqs.append(dist.isend(torch.from_numpy(send_hi), hi_peer, tag=3))
+    if lo_peer >= 0:
+        reqs.append(dist.irecv(t_lo, lo_peer, tag=3))
+    if lo_peer >= 0:
+        reqs.append(dist.isend(torch.from_numpy(send_lo), lo_peer, tag=4))
+    if hi_peer >= 0:
+        reqs.append(dist.irecv(t_hi, hi_peer, tag=4))
+    for r in reqs:
+        r.wait()
+    return (recv_lo if lo_peer >= 0 else None), (recv_hi if hi_peer >= 0 else None)
+
+
+def _push_step(slab, ghosts, bc, omega, po):
+    """One step of a slab whose ghost rows were pushed by the neighbours after their previous
+    step (the P2P schedule: compute, then push the new face rows)."""
+    m = po.orc_model()
+    ybar = m.ymirror()
+    npop, lx, n = slab.shape
+    P = np.full((npop, lx, n + 6), np.nan)
+    P[:, :, 3:n + 3] = slab
+    lo, hi = ghosts
+    if lo is not None:
+        P[:, :, 0:3] = lo
+    else:
+        for d in (1, 2, 3):
+            for p in range(npop):
+                P[p, :, 3 - d] = slab[ybar[p], :, d - 1]
+    if hi is not None:
+        P[:, :, n + 3:n + 6] = hi
+    else:
+        for d in (1, 2, 3):
+            for p in range(npop):
+                P[p, :, n + 2 + d] = slab[ybar[p], :, n - d]
+    out = np.empty_like(slab)
+    for p in range(npop):
+        cx, cy = int(m.cx[p]), int(m.cy[p])
+        out[p] = np.roll(P[p], cx, axis=0)[:, 3 - cy:3 - cy + n]
+    assert not np.isnan(out).any()
+    new, bad = po.orc_collide(out, omega, nthreads=1)
+    assert not bad
+    return new
+
+
+def _push_worker(rank, nranks, port, bc, steps, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import paper_1804_01918_b200 as lbm
+    from oracle import pyoracle as po
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=nranks)
+    try:
+        lx, ly = 8, 12 * nranks
+        glob = po.orc_lattice("random", lx, ly, seed=405)
+        n = ly // nranks
+        slab = np.ascontiguousarray(glob[:, :, rank * n:(rank + 1) * n])
+        ghosts = _exchange_faces(rank, nranks, slab, bc, lbm)  # prime after the load
+        for _ in range(steps):
+            slab = _push_step(slab, ghosts, bc, 0.9, po)
+            ghosts = _exchange_faces(rank, nranks, slab, bc, lbm)  # push the new faces
+        result_q.put((rank, slab))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_push_schedule_bitwise(nranks, bc, po):
+    """The P2P / y-major schedule over real process boundaries: prime after load, then every
+    step computes and pushes its 3 face rows (all 37 populations) into the neighbours' ghost
+    rows for the next step; walls on the outer faces.  Bit-identical to one domain."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_push_worker, args=(r, nranks, port, bc, 3, q)) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(nranks))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    result = np.concatenate([got[r] for r in range(nranks)], axis=2)
+    want, bad = po.orc_step(po.orc_lattice("random", 8, 12 * nranks, seed=405), 0.9, 3,
+                            po.BC_WALL if bc == "wall" else po.BC_PERIODIC)
+    assert not bad
+    assert np.array_equal(result, want)
+
+
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 def test_slab_decomposition_bitwise(nranks, bc, po):
