@@ -766,8 +766,6 @@ int ymajor_step_nccl_unfused(d2q37_lattice* h, double omega, int bc) {
 // own stores.  A prime (after load / init / swap) pushes the current face
 // columns with peer copies under the same counter protocol.
 
-size_t face_bytes(const d2q37_lattice* h) { return ycols_count(h) * sizeof(double); }
-
 double* peer_cols(const d2q37_lattice* h, int side, int buffer, int X) {
     return h->peer_buf[side][buffer] + h->g.lead + (long long)X * h->g.cstride;
 }
@@ -795,12 +793,11 @@ int p2p_prime(d2q37_lattice* h, int bc) {
     CK(cudaEventRecord(h->ev_start, h->stream));
     CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
     RET(p2p_wait(h, bc, seq - 1));
+    const long long n = (long long)ycols_count(h);
     if (face_lo_of(h, bc) == kFaceRemote)  // my first columns -> lo neighbour's high ghost columns
-        CK(cudaMemcpyAsync(peer_cols(h, 0, h->cur, lx + kHalo), ycols(h, kHalo), face_bytes(h),
-                           cudaMemcpyDeviceToDevice, h->halo_stream));
+        CK(launch_copy(peer_cols(h, 0, h->cur, lx + kHalo), ycols(h, kHalo), n, h->halo_stream));
     if (face_hi_of(h, bc) == kFaceRemote)  // my last columns -> hi neighbour's low ghost columns
-        CK(cudaMemcpyAsync(peer_cols(h, 1, h->cur, 0), ycols(h, lx), face_bytes(h), cudaMemcpyDeviceToDevice,
-                           h->halo_stream));
+        CK(launch_copy(peer_cols(h, 1, h->cur, 0), ycols(h, lx), n, h->halo_stream));
     RET(p2p_signal(h, bc, seq));
     RET(p2p_wait(h, bc, seq));  // the neighbours' pushes into my ghost columns
     CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
@@ -1561,6 +1558,7 @@ int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int ra
     for (int i = 0; i < kEventRing; ++i)
         if (cudaEventCreate(&h->ev_int[i]) != cudaSuccess || cudaEventCreate(&h->ev_wait[i]) != cudaSuccess)
             return bail(fail(D2Q37_ERR_CUDA, "p2p slab event creation failed"));
+    if (preload_kernels() != cudaSuccess) return bail(fail(D2Q37_ERR_CUDA, "kernel preload failed"));
     h->transport = kTransportP2P;
     return D2Q37_OK;
 }

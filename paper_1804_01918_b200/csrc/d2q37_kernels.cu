@@ -16,6 +16,8 @@
 // is 2.57 FLOP/B, below the FP64 ridge).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "d2q37_device.cuh"
 #include "d2q37_kernels.cuh"
 
@@ -629,6 +631,75 @@ cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, cons
     return cudaGetLastError();
 }
 #undef D2Q37_BY_ADDR
+
+// Plain device copy (also peer memory): the P2P prime uses it instead of
+// cudaMemcpyAsync so that every GPU operation of the protocol is a kernel of
+// this library, loaded up front.
+__global__ void __launch_bounds__(256) k_copy(double* __restrict__ dst, const double* __restrict__ src, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_copy(double* dst, const double* src, long long n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    const long long blocks = std::min<long long>((n + 255) / 256, 4096);
+    k_copy<<<unsigned(blocks), 256, 0, s>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
+// With CUDA's lazy module loading (the default), the first launch of a kernel
+// loads it, which can wait for the device to go idle.  A spin-waiting
+// k_p2p_wait of another slab never lets it go idle, so the P2P transport loads
+// every kernel up front (cudaFuncGetAttributes forces the load).
+namespace {
+template <typename F>
+void load_kernel(F f) {
+    cudaFuncAttributes a{};
+    (void)cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f));
+}
+template <bool S, bool SH, bool TR>
+void load_collide() {
+    load_kernel(k_collide<S, SH, TR, 32>);
+    load_kernel(k_collide<S, SH, TR, 16>);
+    load_kernel(k_collide<S, SH, TR, 1>);
+    load_kernel(k_collide<S, SH, TR, kAddr32>);
+    load_kernel(k_collide<S, SH, TR, kAddr64>);
+}
+template <bool TR>
+void load_propagate() {
+    load_kernel(k_propagate<TR, 32>);
+    load_kernel(k_propagate<TR, 16>);
+    load_kernel(k_propagate<TR, 1>);
+    load_kernel(k_propagate<TR, kAddr32>);
+    load_kernel(k_propagate<TR, kAddr64>);
+}
+}  // namespace
+
+cudaError_t preload_kernels() {
+    load_collide<false, false, false>();
+    load_collide<true, false, false>();
+    load_collide<false, true, false>();
+    load_collide<true, true, false>();
+    load_collide<false, true, true>();
+    load_collide<true, true, true>();
+    load_propagate<false>();
+    load_propagate<true>();
+    load_kernel(k_p2p_wait);
+    load_kernel(k_p2p_signal);
+    load_kernel(k_copy);
+    load_kernel(k_edge);
+    load_kernel(k_pack);
+    load_kernel(k_scatter);
+    load_kernel(k_gather);
+    load_kernel(k_philox);
+    load_kernel(k_init_rt);
+    load_kernel(k_moments);
+    load_kernel(k_scalar_propagate);
+    load_kernel(k_scalar_collide<false>);
+    load_kernel(k_scalar_collide<true>);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
                             int* flag, cudaStream_t s) {

@@ -89,6 +89,9 @@ cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, cons
 // of `value` into the neighbours' counter slots.
 cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
                             int* flag, cudaStream_t s);
+cudaError_t launch_copy(double* dst, const double* src, long long n, cudaStream_t s);
+// Loads every kernel of this library on the current device (see d2q37_kernels.cu).
+cudaError_t preload_kernels();
 cudaError_t launch_p2p_signal(unsigned long long* lo_slot, unsigned long long* hi_slot, unsigned long long value,
                               cudaStream_t s);
 cudaError_t launch_edge(double* buf, const DevGeo& g, const EdgeParams& ep, cudaStream_t s);

@@ -737,3 +737,26 @@ def test_p2p_connect_across_processes_maps_ipc(gpu, lbm, tmp_path):
     assert r.returncode == 0, r.stderr[-2000:]
     assert "mapped" in r.stdout
     a.close()
+
+
+@pytest.mark.slow
+def test_p2p_ring_full_size_bitwise(gpu, lbm):
+    """The bench lattice (4096 x 16384, CAoSoA32, walls) as a 2-slab P2P ring in one process:
+    the remote-store element shift (lx * cstride, ~2.5e9 elements) and the counters at full size,
+    bit-identical to the single domain after 3 fused steps."""
+    lx, ly = 4096, 16384
+    ref = sim_of(lbm, "caosoa", lx, ly, 32, bc="wall")
+    ref.init_rt_device(99)
+    init = ref.dump()
+    ref.step(0.8, 3)
+    want = ref.dump()
+    ref.close()
+    slabs = lbm.p2p_ring("caosoa", lx, ly, 32, 2, bc="wall")
+    ny = ly // 2
+    for r, s in enumerate(slabs):
+        s.load(np.ascontiguousarray(init[:, :, r * ny:(r + 1) * ny]))
+    del init
+    lbm.step_slabs(slabs, 0.8, 3)
+    for r, s in enumerate(slabs):
+        assert np.array_equal(s.dump(), want[:, :, r * ny:(r + 1) * ny]), r
+        s.close()
