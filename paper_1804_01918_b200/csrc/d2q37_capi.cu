@@ -1519,6 +1519,8 @@ int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, 
         std::string why;
         rc = nccl_comm_init(&h->comm, nranks, id, rank, &why);
         if (rc != D2Q37_OK) return bail(fail(rc, "%s", why.c_str()));
+        // no lazy kernel load while NCCL kernels wait on the other ranks
+        if (preload_kernels() != cudaSuccess) return bail(fail(D2Q37_ERR_CUDA, "kernel preload failed"));
     }
     h->transport = kTransportNccl;
     return D2Q37_OK;
