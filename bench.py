@@ -464,6 +464,8 @@ def run_b200(args, dist: Dist):
     ms_max = dist.max(ms)
     value = n * sites_local * args.steps / (ms_max / 1e3) / 1e6
     launches = sum(c for _, c in kt.values())
+    if transport == "p2p":  # + the one-thread step-counter wait and signal kernels of every step
+        launches += 2 * args.steps
 
     fused_ms, fused_n = kt["fused"]
     dom = "fused" if fused_n else "collide"
