@@ -39,6 +39,7 @@ OMEGA = 0.8
 SEED = 12345
 BYTES_PER_SITE = 592  # 37 x 8 B read + 37 x 8 B write (BASELINE north_star)
 FLOPS_PER_SITE = 1522  # VelocityModel::kCollideFlopsPerSite (model.hpp:74-78)
+HBM_NOMINAL_GBS = 8000.0  # B200 HBM3e datasheet figure (ncu's DRAM peak is ~8.2 TB/s)
 FP64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (CUDA cores), nominal -- no measured FP64 peak in MEASURED_PEAKS.json
 METRIC = "D2Q37 FP64 MLUPS (full step: propagate + bc + collide)"
 
@@ -478,6 +479,8 @@ def run_b200(args, dist: Dist):
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms,
+                "frac_of_nominal_hbm": achieved / HBM_NOMINAL_GBS if achieved else None,
+                "nominal_hbm_gbs": HBM_NOMINAL_GBS,
                 "edge_ms": kt["edge"][0] / max(1, kt["edge"][1])}
 
     # ---- e2e through the public API with host buffers
