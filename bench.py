@@ -549,7 +549,8 @@ def run_e2e(lbm, sim, args, dist: Dist):
     need = 37 * sim.lx * sim.ly * 8
     local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", dist.world))
     avail = host_mem_available()
-    if avail and avail < need * local_ranks * 1.25:
+    enough = not (avail and avail < need * local_ranks * 1.25)
+    if dist.min(1.0 if enough else 0.0) < 0.5:  # collective: every rank steps, or none does
         return {"value": None, "unit": "MLUPS",
                 "skipped": f"{local_ranks} x {need / 1e9:.1f} GB host buffers exceed available host memory"}
     canon = np.empty((37, sim.lx, sim.ly), dtype=np.float64)
