@@ -15,6 +15,9 @@
 //   G6  metric formulas reproduce Table 1                                (C6)
 //   G7  errors: invalid geometry -> std::invalid_argument,
 //       rho <= 0 -> NonPhysicalError                                     (test_kernels.cpp:424-433)
+//   G8  run_validation's scalar device reference <= 1e-12 vs the reference's
+//       oracle_propagate + oracle_collide (5 steps); convert between device
+//       layouts preserves every physical site                           (validation.cpp, layout.cpp:105-116)
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -205,16 +208,39 @@ bool g7() {
     return true;
 }
 
+bool g8() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(24, 48, 808);
+    const lbm::CanonicalLattice want = oracle_run(init, [&](lbm::OracleLattice& a, lbm::OracleLattice& b) {
+        lbm::OracleLattice t(init.lx, init.ly);
+        for (int n = 0; n < 5; ++n) {
+            lbm::oracle_propagate(a, t, m.velocities());
+            lbm::oracle_collide(t, a, m, 1.3);
+        }
+        b = a;
+    });
+    const auto got = lbm_b200::scalar_steps(reference_model(), to_gpu(init), 1.3, 5);
+    if (!(max_rel(got.values, want.values) <= 1e-12)) return false;
+    lbm_b200::LatticeState src(B::CAoSoA, lbm_b200::Geometry{24, 48, 3, 3, 8});
+    src.load(to_gpu(init));
+    for (const B kind : kLayouts) {
+        const lbm_b200::LatticeState dst = lbm_b200::convert(src, kind, lbm_b200::Geometry{24, 48, 3, 3, 4});
+        if (dst.dump().values != init.values) return false;
+    }
+    return true;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::array<std::pair<const char*, bool (*)()>, 7> all = {{{"G1", g1},
+    const std::array<std::pair<const char*, bool (*)()>, 8> all = {{{"G1", g1},
                                                                      {"G2", g2},
                                                                      {"G3", g3},
                                                                      {"G4", g4},
                                                                      {"G5", g5},
                                                                      {"G6", g6},
-                                                                     {"G7", g7}}};
+                                                                     {"G7", g7},
+                                                                     {"G8", g8}}};
     int failures = 0;
     for (const auto& [name, fn] : all) {
         if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;
