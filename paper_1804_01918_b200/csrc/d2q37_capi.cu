@@ -54,6 +54,12 @@ struct d2q37_lattice {
     int* h_flag = nullptr;
     double* d_part = nullptr;
     double* stage = nullptr;
+    // host <-> device canonical transfers: a second staging plane, a copy
+    // stream and events, so one plane's PCIe copy overlaps the next one's
+    // scatter / gather kernel
+    double* stage2 = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_io[4] = {};
     long time_step = 0;
 
     // y-slab decomposition
@@ -313,8 +319,13 @@ void free_lattice(d2q37_lattice* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
     if (h->halo_stream) cudaStreamSynchronize(h->halo_stream);
-    for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->send_lo, h->send_hi, h->recv_lo, h->recv_hi})
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->stage2, h->send_lo, h->send_hi, h->recv_lo,
+                      h->recv_hi})
         if (p) cudaFree(p);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    for (cudaEvent_t e : h->ev_io)
+        if (e) cudaEventDestroy(e);
     if (h->d_flag) cudaFree(h->d_flag);
     if (h->d_seq) cudaFree(h->d_seq);
     for (void* p : h->ipc_mapped) cudaIpcCloseMemHandle(p);
@@ -897,6 +908,16 @@ int slab_phase2(d2q37_lattice* h, double omega, int variant, int bc) {
     return D2Q37_OK;
 }
 
+// Two staging planes, a copy stream and 4 events for pipelined host transfers.
+int ensure_io_pipeline(d2q37_lattice* h, size_t plane_vals) {
+    if (!h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
+    if (!h->stage2) CK(cudaMalloc(&h->stage2, plane_vals * sizeof(double)));
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : h->ev_io)
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return D2Q37_OK;
+}
+
 int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n, bool src_device) {
     if (h) h->p2p_dirty = true;
     RET(check_handle(h));
@@ -913,15 +934,25 @@ int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n
             CK(cudaMemcpy2DAsync(dst + site_of(g, kHalo, 0) + p * g.pstride, size_t(g.cstride) * sizeof(double),
                                  src + p * plane_vals, size_t(g.ly) * sizeof(double), size_t(g.ly) * sizeof(double),
                                  size_t(g.lx), cudaMemcpyHostToDevice, h->stream));
+    } else if (src_device) {
+        for (int p = 0; p < kNpop; ++p) CK(launch_scatter(dst, g, src + p * plane_vals, p, h->stream));
     } else {
-        if (!src_device && !h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
+        // plane p's H2D copy (copy stream) overlaps plane p-1's scatter (compute stream)
+        RET(ensure_io_pipeline(h, plane_vals));
+        double* stage[2] = {h->stage, h->stage2};
+        cudaEvent_t* copied = h->ev_io;        // [2]
+        cudaEvent_t* consumed = h->ev_io + 2;  // [2]
+        CK(cudaEventRecord(consumed[0], h->stream));  // orders the copies after prior work on the lattice
+        CK(cudaEventRecord(consumed[1], h->stream));
         for (int p = 0; p < kNpop; ++p) {
-            const double* plane = src + p * plane_vals;
-            if (!src_device) {
-                CK(cudaMemcpyAsync(h->stage, plane, plane_vals * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-                plane = h->stage;
-            }
-            CK(launch_scatter(dst, g, plane, p, h->stream));
+            const int b = p & 1;
+            CK(cudaStreamWaitEvent(h->copy_stream, consumed[b], 0));
+            CK(cudaMemcpyAsync(stage[b], src + p * plane_vals, plane_vals * sizeof(double), cudaMemcpyHostToDevice,
+                               h->copy_stream));
+            CK(cudaEventRecord(copied[b], h->copy_stream));
+            CK(cudaStreamWaitEvent(h->stream, copied[b], 0));
+            CK(launch_scatter(dst, g, stage[b], p, h->stream));
+            CK(cudaEventRecord(consumed[b], h->stream));
         }
     }
     CK(cudaStreamSynchronize(h->stream));
@@ -943,15 +974,27 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
                                  src + site_of(g, kHalo, 0) + p * g.pstride, size_t(g.cstride) * sizeof(double),
                                  size_t(g.ly) * sizeof(double), size_t(g.lx),
                                  cudaMemcpyDeviceToHost, h->stream));
+    } else if (out_device) {
+        for (int p = 0; p < kNpop; ++p) CK(launch_gather(src, g, out + p * plane_vals, p, h->stream));
     } else {
-        if (!out_device && !h->stage) CK(cudaMalloc(&h->stage, plane_vals * sizeof(double)));
+        // plane p's gather (compute stream) overlaps plane p-1's D2H copy (copy stream)
+        RET(ensure_io_pipeline(h, plane_vals));
+        double* stage[2] = {h->stage, h->stage2};
+        cudaEvent_t* gathered = h->ev_io;     // [2]
+        cudaEvent_t* drained = h->ev_io + 2;  // [2]
+        CK(cudaEventRecord(drained[0], h->copy_stream));
+        CK(cudaEventRecord(drained[1], h->copy_stream));
         for (int p = 0; p < kNpop; ++p) {
-            double* plane = out_device ? out + p * plane_vals : h->stage;
-            CK(launch_gather(src, g, plane, p, h->stream));
-            if (!out_device)
-                CK(cudaMemcpyAsync(out + p * plane_vals, h->stage, plane_vals * sizeof(double), cudaMemcpyDeviceToHost,
-                                   h->stream));
+            const int b = p & 1;
+            CK(cudaStreamWaitEvent(h->stream, drained[b], 0));
+            CK(launch_gather(src, g, stage[b], p, h->stream));
+            CK(cudaEventRecord(gathered[b], h->stream));
+            CK(cudaStreamWaitEvent(h->copy_stream, gathered[b], 0));
+            CK(cudaMemcpyAsync(out + p * plane_vals, stage[b], plane_vals * sizeof(double), cudaMemcpyDeviceToHost,
+                               h->copy_stream));
+            CK(cudaEventRecord(drained[b], h->copy_stream));
         }
+        CK(cudaStreamSynchronize(h->copy_stream));
     }
     CK(cudaStreamSynchronize(h->stream));
     return D2Q37_OK;
