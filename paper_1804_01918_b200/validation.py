@@ -115,3 +115,40 @@ def print_report(report: ValidationReport, file=None) -> None:
             line += f"  first divergence at (x={d.x}, y={d.y}, p={d.p}): got {d.got:.6g}, want {d.want:.6g}"
         print(line, file=out)
     print(f"validation {'passed' if report.passed else 'FAILED'} ({len(report.cases)} cases)", file=out)
+
+
+def main(argv=None) -> int:
+    """``python -m paper_1804_01918_b200.validation`` -- the device analogue of ``lbmbench
+    validate`` (lbmbench_main.cpp:102-125): bare, it runs the default suite (both stock
+    geometries, vl 1/2/4/8); exit status 0 iff every case passes."""
+    import argparse
+
+    ap = argparse.ArgumentParser(description=main.__doc__.splitlines()[0])
+    ap.add_argument("--lx", type=int)
+    ap.add_argument("--ly", type=int)
+    ap.add_argument("--vl", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--layout", nargs="+", default=["aos", "soa", "csoa", "caosoa"],
+                    choices=["aos", "soa", "csoa", "caosoa"])
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--omega", type=float, default=1.0)
+    ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--math", choices=["fast", "strict"], default="fast")
+    ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--corrupt-population", type=int, default=-1)
+    ap.add_argument("-o", "--output", help="write the report here instead of stdout")
+    a = ap.parse_args(argv)
+    opts = ValidationOptions(vls=a.vl, layouts=a.layout, steps=a.steps, omega=a.omega, seed=a.seed, math=a.math,
+                             device=a.device, corrupt_population=a.corrupt_population)
+    if a.lx is not None or a.ly is not None:
+        opts.geometries = [(a.lx or 16, a.ly or 32)]
+    rep = run_validation(opts)
+    if a.output:
+        with open(a.output, "w") as f:
+            print_report(rep, f)
+    else:
+        print_report(rep)
+    return 0 if rep.passed else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
