@@ -760,3 +760,20 @@ def test_p2p_ring_full_size_bitwise(gpu, lbm):
     for r, s in enumerate(slabs):
         assert np.array_equal(s.dump(), want[:, :, r * ny:(r + 1) * ny]), r
         s.close()
+
+
+def test_validation_cli(gpu, lbm):
+    """python -m paper_1804_01918_b200.validation: exit 0 and the reference's summary line when
+    every case passes, exit 1 with a corrupted offset table (lbmbench validate's contract)."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    cmd = [sys.executable, "-m", "paper_1804_01918_b200.validation", "--lx", "16", "--ly", "32", "--vl", "1", "4",
+           "--steps", "2"]
+    ok = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert ok.returncode == 0, ok.stdout + ok.stderr
+    assert ok.stdout.strip().splitlines()[-1] == "validation passed (8 cases)"
+    bad = subprocess.run(cmd + ["--corrupt-population", "5"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert bad.returncode == 1 and "validation FAILED" in bad.stdout
