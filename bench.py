@@ -328,6 +328,39 @@ def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
     return out
 
 
+def bench_p2p_ring_emulation(lbm, layout, vl, nslabs, warmup, steps) -> dict:
+    """BASELINE config 4 strong (4096 x 32768) as `nslabs` P2P slabs on ONE GPU, stepped in
+    lockstep through the real peer-memory protocol (counters, remote stores, separate streams),
+    vs the same lattice as one domain.  The slabs share one GPU, so this measures the protocol's
+    cost at the per-GPU slab size of the 8-GPU run, not NVLink."""
+    import torch
+
+    ly = STRONG_LY
+    out = {"config": f"{LX}x{ly} {layout}{vl}, walls, {nslabs} P2P slabs on one GPU vs one domain, {steps} steps"}
+    sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="wall")
+    sim.init_rt_device(SEED)
+    sim.step(OMEGA, warmup)
+    ms = time_steps(sim, steps, lambda: sim.step(OMEGA, 1, sync=False))
+    out["single_domain"] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6}
+    sim.close()
+    del sim
+    slabs = lbm.p2p_ring(layout, LX, ly, vl, nslabs, bc="wall")
+    for s in slabs:
+        s.init_rt_device(SEED)
+    lbm.step_slabs(slabs, OMEGA, warmup)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lbm.step_slabs(slabs, OMEGA, steps)
+    torch.cuda.synchronize()
+    ms = 1e3 * (time.perf_counter() - t0)
+    out[f"p2p_ring_{nslabs}"] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6,
+                                 "timing": "host wall clock around the lockstep loop (several streams)"}
+    for s in slabs:
+        s.close()
+    out["protocol_overhead"] = out[f"p2p_ring_{nslabs}"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
+    return out
+
+
 def bench_variant(lbm, ly, layout, vl, variant, warmup, steps) -> dict:
     sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="wall", variant=variant)
     sim.init_rt_device(SEED)
@@ -525,6 +558,11 @@ def run_b200(args, dist: Dist):
                 "weak_slab": bench_slab_schedule(lbm, args.layout, args.vl, LY_PER_GPU, 3, 20)}
         except Exception as e:  # NCCL unavailable must not sink the line
             line["slab_schedule"] = {"error": str(e)}
+        if args.layout in ("aos", "caosoa"):
+            try:
+                line["p2p_ring_emulation"] = bench_p2p_ring_emulation(lbm, args.layout, args.vl, 8, 3, 20)
+            except Exception as e:  # noqa: BLE001
+                line["p2p_ring_emulation"] = {"error": str(e)}
     if n == 1 and not args.no_cpu:
         try:
             v, med, workers = reference_step_rate()
