@@ -777,3 +777,54 @@ def test_validation_cli(gpu, lbm):
     assert ok.stdout.strip().splitlines()[-1] == "validation passed (8 cases)"
     bad = subprocess.run(cmd + ["--corrupt-population", "5"], capture_output=True, text=True, cwd=ROOT, timeout=300)
     assert bad.returncode == 1 and "validation FAILED" in bad.stdout
+
+
+# --------------------------------------------------------------------------- more reference test mirrors
+
+@pytest.mark.parametrize("layout,vl", [("aos", 1), ("soa", 1), ("csoa", 4), ("caosoa", 8)])
+def test_bc_constant_lattice_fills_every_ghost(gpu, lbm, layout, vl):
+    """test_kernels.cpp:56-71 / :73-83: a constant lattice's ghosts all hold that value, also
+    with a single column (lx = 1: the ghost columns mirror it)."""
+    for lx, ly in ((6, 32), (1, 32)):
+        s = sim_of(lbm, layout, lx, ly, vl)
+        s.load(np.full((37, lx, ly), 0.375))
+        s.bc("periodic")
+        assert np.all(s.read_padded() == 0.375)
+
+
+@pytest.mark.parametrize("layout,vl", [("aos", 1), ("soa", 1), ("csoa", 4), ("caosoa", 8), ("caosoa", 32)])
+@pytest.mark.parametrize("variant", ["fused", "unfused"])
+def test_step_uniform_equilibrium_stays_uniform(gpu, lbm, layout, vl, variant):
+    """test_kernels.cpp:325-341: a uniform equilibrium lattice stays uniform across sites, bit for
+    bit, under periodic steps (every site sees identical inputs)."""
+    lx, ly = 16, 256
+    m = lbm.model()
+    s = sim_of(lbm, layout, lx, ly, vl, variant=variant)
+    s.load(lbm.make_lattice("equilibrium", lx, ly, params=[1.02, 0.03, -0.02, m.t0 * 1.05]))
+    s.step(1.4, 7)
+    out = s.dump()
+    assert np.all(out == out[:, :1, :1])
+
+
+@pytest.mark.parametrize("layout,vl", [("aos", 1), ("soa", 1), ("csoa", 2), ("csoa", 32), ("caosoa", 4),
+                                       ("caosoa", 32)])
+def test_dump_round_trip_bitwise(gpu, lbm, layout, vl):
+    """layout.cpp / test_layout.cpp "dump: canonical round trip across layouts is bitwise", for
+    both buffers, including signed zeros, subnormals and NaN payloads."""
+    lx, ly = 10, 96
+    a = lbm.make_lattice("random", lx, ly, seed=77)
+    a[0, 0, 0], a[1, 2, 3], a[2, 3, 4] = -0.0, 5e-324, np.inf
+    s = sim_of(lbm, layout, lx, ly, vl)
+    for which in (0, 1):
+        s.load(a, which=which)
+        got = s.dump(which=which)
+        assert got.view(np.uint64).tobytes() == a.view(np.uint64).tobytes()
+
+
+def test_run_validation_same_seed_same_report(gpu, lbm):
+    """test_validation.cpp: the same options give identical reports (deterministic device paths)."""
+    from paper_1804_01918_b200 import validation as v
+
+    o = v.ValidationOptions(geometries=[(16, 32)], vls=[1, 4], steps=3, corrupt_population=11)
+    a, b = v.run_validation(o), v.run_validation(o)
+    assert a == b and not a.passed
