@@ -428,10 +428,10 @@ def run_reference(args, dist):
 # --------------------------------------------------------------------------- main arm
 
 def make_slab(lbm, args, dist: Dist, dev: int, ly_global: int):
-    """This rank's slab: the peer-memory P2P transport for site-major layouts (falls back to NCCL
-    if the ranks cannot map each other's memory), NCCL otherwise or when asked."""
+    """This rank's slab: the peer-memory P2P transport (falls back to NCCL if the ranks cannot map
+    each other's memory), or NCCL when asked."""
     rank, n = dist.rank, dist.world
-    if args.transport == "p2p" and args.layout in ("aos", "caosoa"):
+    if args.transport == "p2p":
         sim, blob = None, b""
         try:
             sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
@@ -637,7 +637,7 @@ def main():
     ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU (weak scaling)")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
-                    help="N>1 halo transport: peer-memory push from the step kernel (site-major layouts), or NCCL")
+                    help="N>1 halo transport: peer-memory push from the step kernel, or NCCL")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: --ly rows per GPU; strong: 4096 x 32768 split over the GPUs (config 4)")
     ap.add_argument("--e2e-steps", type=int, default=200)

@@ -164,10 +164,12 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst);
 int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_in, double* host_out, size_t n,
                        double omega, int nsteps, int math, int device);
 
-/* Multi-GPU y-slabs without NCCL (site-major layouts, y-major storage): the
- * fused step kernel stores its face columns straight into the neighbours'
- * ghost columns through NVLink peer memory, and per-step counters in peer
- * memory order the ranks.  create -> export a 256-byte
+/* Multi-GPU y-slabs without NCCL, all four layouts: the fused step kernel of
+ * the face sites stores its results straight into the neighbours' ghost
+ * slots through NVLink peer memory (site-major layouts in y-major storage:
+ * 3 whole columns per face; SoA / CSoA: lane 0's first / lane vl-1's last 3
+ * rows), and per-step counters in peer memory order the ranks (DESIGN.md
+ * section 5).  create -> export a 256-byte
  * blob -> exchange blobs (any host channel, e.g. torch.distributed) ->
  * connect(lo neighbour's blob, hi neighbour's blob); a 1-rank ring connects
  * to its own blob.  Neighbours in this process are used directly, others are

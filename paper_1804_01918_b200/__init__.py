@@ -413,8 +413,8 @@ class Simulation:
         """Rank `rank` of an `nranks`-GPU y-slab decomposition.
 
         ``transport="nccl"`` (d2q37_create_slab): NCCL send/recv halos; needs ``nccl_id``.
-        ``transport="p2p"`` (d2q37_create_slab_p2p, site-major layouts): the step kernel pushes
-        its face columns into the neighbours' ghost columns through peer memory.
+        ``transport="p2p"`` (d2q37_create_slab_p2p): the step kernel pushes its face sites into
+        the neighbours' ghost slots through peer memory.
         ``exchange(blob) -> list of every rank's blob`` (e.g. an all_gather over
         torch.distributed) connects the ranks; with ``nranks == 1`` and no ``exchange`` the slab
         is a 1-rank ring connected to itself.  Without either, call ``p2p_blob`` /

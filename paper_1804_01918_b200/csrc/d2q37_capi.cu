@@ -777,10 +777,6 @@ int ymajor_step_nccl_unfused(d2q37_lattice* h, double omega, int bc) {
 // own stores.  A prime (after load / init / swap) pushes the current face
 // columns with peer copies under the same counter protocol.
 
-double* peer_cols(const d2q37_lattice* h, int side, int buffer, int X) {
-    return h->peer_buf[side][buffer] + h->g.lead + (long long)X * h->g.cstride;
-}
-
 int p2p_wait(d2q37_lattice* h, int bc, unsigned long long target) {
     CK(launch_p2p_wait(h->d_seq, face_lo_of(h, bc) == kFaceRemote, face_hi_of(h, bc) == kFaceRemote, target,
                        h->d_flag, h->halo_stream));
@@ -793,36 +789,60 @@ int p2p_signal(d2q37_lattice* h, int bc, unsigned long long value) {
     return D2Q37_OK;
 }
 
-// Pushes the current state's face columns into the neighbours' current ghost
-// columns (peer copies), then signals; the next step waits for the neighbours'
-// pushes.  Invariant of the counters: a neighbour's counter >= s means its
-// operation s has finished both its pushes and its reads of its own ghost
-// columns, so waiting for s - 1 before writing into its buffers is safe.
+// The face sites of a P2P slab for bc (both orientations) and the element
+// shifts that map each face site onto the neighbour's ghost slot for it.
+//   y-major: 3 storage columns per face; my column x < 3 is the lo
+//            neighbour's ghost column lx + 3 + x (shift +lx*cstride), my column
+//            lx - 3 + c is the hi neighbour's ghost column c (-lx*cstride).
+//   x-major: lane 0's rows r < 3 are the lo neighbour's lane vl-1 ghost rows
+//            strip + 3 + r (shift +strip*rstride + vl-1); lane vl-1's last rows
+//            are the hi neighbour's lane-0 ghost rows (the negative shift).
+Segments p2p_faces(const d2q37_lattice* h, int bc, int* nseg) {
+    return h->g.tr ? ycols_boundary(h, bc, nseg) : boundary(h, bc, nseg);
+}
+
+PeerStores p2p_peers(const d2q37_lattice* h, int bc, int buffer) {
+    const DevGeo& g = h->g;
+    const long long span = g.tr ? (long long)g.lx * g.cstride : (long long)g.strip * g.rstride + (g.vl - 1);
+    PeerStores ps{};
+    if (face_lo_of(h, bc) == kFaceRemote) {
+        ps.lo = h->peer_buf[0][buffer];
+        ps.lo_shift = span;
+    }
+    if (face_hi_of(h, bc) == kFaceRemote) {
+        ps.hi = h->peer_buf[1][buffer];
+        ps.hi_shift = -span;
+    }
+    return ps;
+}
+
+// Pushes the current state's face sites into the neighbours' current ghost
+// slots, then signals; waits for the neighbours' pushes into mine.  Invariant
+// of the counters: a neighbour's counter >= s means its operation s has
+// finished both its pushes and its reads of its own ghost slots, so waiting
+// for s - 1 before writing into its buffers is safe.
 int p2p_prime(d2q37_lattice* h, int bc) {
     const unsigned long long seq = ++h->p2p_seq;
-    const int lx = h->g.lx;
     CK(cudaEventRecord(h->ev_start, h->stream));
     CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
     RET(p2p_wait(h, bc, seq - 1));
-    const long long n = (long long)ycols_count(h);
-    if (face_lo_of(h, bc) == kFaceRemote)  // my first columns -> lo neighbour's high ghost columns
-        CK(launch_copy(peer_cols(h, 0, h->cur, lx + kHalo), ycols(h, kHalo), n, h->halo_stream));
-    if (face_hi_of(h, bc) == kFaceRemote)  // my last columns -> hi neighbour's low ghost columns
-        CK(launch_copy(peer_cols(h, 1, h->cur, 0), ycols(h, lx), n, h->halo_stream));
+    int nseg = 0;
+    const Segments faces = p2p_faces(h, bc, &nseg);
+    CK(launch_face_prime(h->buf[h->cur], h->g, h->off_pull, faces, nseg, p2p_peers(h, bc, h->cur), h->halo_stream));
     RET(p2p_signal(h, bc, seq));
-    RET(p2p_wait(h, bc, seq));  // the neighbours' pushes into my ghost columns
+    RET(p2p_wait(h, bc, seq));  // the neighbours' pushes into my ghost slots
     CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
     CK(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
     h->p2p_dirty = false;
     return D2Q37_OK;
 }
 
-int ymajor_step_p2p(d2q37_lattice* h, double omega, int variant, int bc) {
+int p2p_step(d2q37_lattice* h, double omega, int variant, int bc) {
     if (!h->p2p_connected) return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p slab is not connected to its neighbours");
     if (h->p2p_dirty) RET(p2p_prime(h, bc));
     if (variant != D2Q37_FUSED) {
         // unfused: push the faces (counter c1), run the local verbs, then signal c1 + 1 once
-        // they are done reading the ghost columns -- the state stays in the same buffer, so a
+        // they are done reading the ghost slots -- the state stays in the same buffer, so a
         // neighbour's next push must not land while propagate is still reading
         RET(p2p_prime(h, bc));
         RET(step_local(h, omega, D2Q37_UNFUSED, bc));
@@ -834,31 +854,23 @@ int ymajor_step_p2p(d2q37_lattice* h, double omega, int variant, int bc) {
     }
     const unsigned long long seq = ++h->p2p_seq;
     const Faces fc = step_faces(h, bc);
-    const bool lo_r = face_lo_of(h, bc) == kFaceRemote, hi_r = face_hi_of(h, bc) == kFaceRemote;
     CK(cudaEventRecord(h->ev_start, h->stream));
     CK(cudaStreamWaitEvent(h->halo_stream, h->ev_start, 0));
-    RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, ycols_interior(h, bc), 1, fc));
+    // interior: every site whose pull stays inside the slab (no ghost reads, no remote writes)
+    RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, h->g.tr ? ycols_interior(h, bc) : interior(h, bc), 1,
+                       fc));
     const int ring = h->ev_count % kEventRing;
     CK(cudaEventRecord(h->ev_int[ring], h->stream));
     {
         OnStream on(h, h->halo_stream);
         RET(p2p_wait(h, bc, seq - 1));
-        PeerStores ps{};
-        const long long span = (long long)h->g.lx * h->g.cstride;
-        if (lo_r) {
-            ps.lo = h->peer_buf[0][1 - h->cur];
-            ps.lo_shift = span;  // my column x -> the lo neighbour's ghost column lx + 3 + x
-        }
-        if (hi_r) {
-            ps.hi = h->peer_buf[1][1 - h->cur];
-            ps.hi_shift = -span;  // my column lx - 3 + c -> the hi neighbour's ghost column c
-        }
         int nseg = 0;
-        const Segments bnd = ycols_boundary(h, bc, &nseg);
+        const Segments faces = p2p_faces(h, bc, &nseg);
         {
             ProfScope prof(h, kProfBoundary);
-            CK(launch_collide(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, fc, h->mp, omega,
-                              h->math == D2Q37_MATH_STRICT, true, bnd, nseg, h->d_flag, h->stream, &ps));
+            CK(launch_face(h->buf[h->cur], h->buf[1 - h->cur], h->g, h->off_pull, fc, h->mp, omega,
+                           h->math == D2Q37_MATH_STRICT, faces, nseg, p2p_peers(h, bc, 1 - h->cur), h->d_flag,
+                           h->stream));
         }
         RET(p2p_signal(h, bc, seq));
         CK(cudaEventRecord(h->ev_bnd, h->halo_stream));
@@ -1240,7 +1252,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
     }
     for (; s < nsteps; ++s) {
         if (slab && h->transport == kTransportP2P) {
-            RET(ymajor_step_p2p(h, omega, variant, bc));
+            RET(p2p_step(h, omega, variant, bc));
         } else if (slab && h->g.tr) {
             RET(variant == D2Q37_FUSED ? ymajor_step_nccl(h, omega, bc) : ymajor_step_nccl_unfused(h, omega, bc));
         } else if (slab && h->halo_stream && variant == D2Q37_FUSED && can_split(h)) {
@@ -1582,9 +1594,10 @@ constexpr uint32_t kP2PMagic = 0x50373344u;  // "D37P"
 
 int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
                           d2q37_lattice** out) {
-    if (!site_major(layout))
-        return fail(D2Q37_ERR_UNSUPPORTED, "p2p slabs need a site-major layout (AoS, CAoSoA): y-major storage");
-    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks, true));
+    // site-major layouts slab in y-major storage (faces = contiguous columns), the others x-major
+    if (!site_major(layout) && nranks > 0 && ly % nranks == 0 && !clustered(layout) && ly / nranks < 2 * kHalo)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p SoA slab needs at least 6 rows per slab");
+    RET(create_impl(layout, lx, ly, vl, device, out, rank, nranks, site_major(layout)));
     d2q37_lattice* h = *out;
     auto bail = [&](int rc) {
         d2q37_destroy(h);

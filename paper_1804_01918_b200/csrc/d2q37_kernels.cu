@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_propagate(const double* __re
 template <bool STRICT, bool SHIFT, bool TR, int AM>
 __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     k_collide(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, Faces fc,
-              ModelParams mp, double omega, Segments seg, int* __restrict__ flag, PeerStores ps) {
+              ModelParams mp, double omega, Segments seg, int* __restrict__ flag) {
     int x, q;
     if (!segment_site(g, seg, x, q)) return;
     const long long e = site_of(g, x + kHalo, q);
@@ -247,12 +247,60 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
     if (bad) *flag = 1;
     store_site<AM>(dst, e, g, off, f);
-    if (TR && SHIFT) {  // y-major slab: push the face columns into the neighbours' ghost columns
-        const bool lo = ps.lo && x < kHalo, hi = ps.hi && x >= g.lx - kHalo;
-        if (lo) store_site<kAddr64>(ps.lo, e + ps.lo_shift, g, off, f);
-        if (hi) store_site<kAddr64>(ps.hi, e + ps.hi_shift, g, off, f);
-        if (lo || hi) __threadfence_system();  // performed before the step counter is released
+}
+
+// ---------------------------------------------------------------------------
+// P2P slab faces.  A face site is within 3 sites of a face shared with a
+// neighbour: y-major storage, the 3 storage columns next to the face; x-major,
+// lane 0's first 3 rows (lo) / lane vl-1's last 3 rows (hi).
+
+template <bool TR>
+__device__ __forceinline__ int face_side(const DevGeo& g, int x, int q) {
+    if (TR) return x < kHalo ? 0 : x >= g.lx - kHalo ? 1 : -1;
+    const int row = q >> g.lvl, k = q & (g.vl - 1);
+    if (k == 0 && row < kHalo) return 0;
+    if (k == g.vl - 1 && row >= g.strip - kHalo) return 1;
+    return -1;
+}
+
+// The fused step on face sites that also stores each result into the
+// neighbour's next buffer (its ghost slots for this site): the halo travels
+// with the kernel's own stores over NVLink.
+template <bool STRICT, bool TR>
+__global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
+    k_face(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Offsets off, Faces fc,
+           ModelParams mp, double omega, Segments seg, int* __restrict__ flag, PeerStores ps) {
+    int x, q;
+    if (!segment_site(g, seg, x, q)) return;
+    const long long e = site_of(g, x + kHalo, q);
+    double f[kNpop];
+    gather_site<kPullEdge, TR, kAddr64>(f, src, e, g, off, fc, x, q);
+    const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
+    if (bad) *flag = 1;
+    store_site<kAddr64>(dst, e, g, off, f);
+    const int side = face_side<TR>(g, x, q);
+    double* peer = side == 0 ? ps.lo : side == 1 ? ps.hi : nullptr;
+    if (peer) {
+        store_site<kAddr64>(peer, e + (side == 0 ? ps.lo_shift : ps.hi_shift), g, off, f);
+        __threadfence_system();  // performed before the step counter is released
     }
+}
+
+// Prime: copies the current state's face sites into the neighbours' current
+// ghost slots (after a load / init / swap).
+template <bool TR>
+__global__ void __launch_bounds__(kStreamThreads) k_face_prime(const double* __restrict__ buf, DevGeo g, Offsets off,
+                                                               Segments seg, PeerStores ps) {
+    int x, q;
+    if (!segment_site(g, seg, x, q)) return;
+    const int side = face_side<TR>(g, x, q);
+    double* peer = side == 0 ? ps.lo : side == 1 ? ps.hi : nullptr;
+    if (!peer) return;
+    const long long e = site_of(g, x + kHalo, q);
+    const long long shift = side == 0 ? ps.lo_shift : ps.hi_shift;
+#pragma unroll
+    for (int p = 0; p < kNpop; ++p) peer[e + shift + p * g.pstride] = buf[e + p * g.pstride];
+    __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -594,10 +642,9 @@ cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, co
 namespace {
 template <bool S, bool SH, bool TR>
 void collide_am(dim3 grid, cudaStream_t s, const double* src, double* dst, const DevGeo& g, const Offsets& off,
-                const Faces& fc, const ModelParams& mp, double omega, const Segments& seg, int* flag,
-                const PeerStores& ps) {
+                const Faces& fc, const ModelParams& mp, double omega, const Segments& seg, int* flag) {
 #define D2Q37_COLL(AM) \
-    k_collide<S, SH, TR, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag, ps)
+    k_collide<S, SH, TR, AM><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag)
     D2Q37_BY_ADDR(addr_mode(g, off), D2Q37_COLL)
 #undef D2Q37_COLL
 }
@@ -605,11 +652,10 @@ void collide_am(dim3 grid, cudaStream_t s, const double* src, double* dst, const
 
 cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
-                           int nseg, int* flag, cudaStream_t s, const PeerStores* peers) {
+                           int nseg, int* flag, cudaStream_t s) {
     if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
     const dim3 grid = stream_grid(g, seg, nseg);
-    const PeerStores ps = peers ? *peers : PeerStores{};
-#define D2Q37_COLLIDE(S, SH, TR) collide_am<S, SH, TR>(grid, s, src, dst, g, off, fc, mp, omega, seg, flag, ps)
+#define D2Q37_COLLIDE(S, SH, TR) collide_am<S, SH, TR>(grid, s, src, dst, g, off, fc, mp, omega, seg, flag)
     (void)cudaGetLastError();
     if (!shift) {  // no pull: the storage orientation does not matter
         if (strict)
@@ -688,6 +734,12 @@ cudaError_t preload_kernels() {
     load_kernel(k_p2p_wait);
     load_kernel(k_p2p_signal);
     load_kernel(k_copy);
+    load_kernel(k_face<false, false>);
+    load_kernel(k_face<true, false>);
+    load_kernel(k_face<false, true>);
+    load_kernel(k_face<true, true>);
+    load_kernel(k_face_prime<false>);
+    load_kernel(k_face_prime<true>);
     load_kernel(k_edge);
     load_kernel(k_pack);
     load_kernel(k_scatter);
@@ -698,6 +750,40 @@ cudaError_t preload_kernels() {
     load_kernel(k_scalar_propagate);
     load_kernel(k_scalar_collide<false>);
     load_kernel(k_scalar_collide<true>);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_face(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
+                        const ModelParams& mp, double omega, bool strict, const Segments& seg, int nseg,
+                        const PeerStores& ps, int* flag, cudaStream_t s) {
+    if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
+    const dim3 grid = stream_grid(g, seg, nseg);
+    (void)cudaGetLastError();
+#define D2Q37_FACE(S, TR) k_face<S, TR><<<grid, kStreamThreads, 0, s>>>(src, dst, g, off, fc, mp, omega, seg, flag, ps)
+    if (g.tr) {
+        if (strict)
+            D2Q37_FACE(true, true);
+        else
+            D2Q37_FACE(false, true);
+    } else {
+        if (strict)
+            D2Q37_FACE(true, false);
+        else
+            D2Q37_FACE(false, false);
+    }
+#undef D2Q37_FACE
+    return cudaGetLastError();
+}
+
+cudaError_t launch_face_prime(const double* buf, const DevGeo& g, const Offsets& off, const Segments& seg, int nseg,
+                              const PeerStores& ps, cudaStream_t s) {
+    if (seg.nq <= 0 || nseg <= 0) return cudaSuccess;
+    const dim3 grid = stream_grid(g, seg, nseg);
+    (void)cudaGetLastError();
+    if (g.tr)
+        k_face_prime<true><<<grid, kStreamThreads, 0, s>>>(buf, g, off, seg, ps);
+    else
+        k_face_prime<false><<<grid, kStreamThreads, 0, s>>>(buf, g, off, seg, ps);
     return cudaGetLastError();
 }
 

@@ -68,13 +68,13 @@ struct PackParams {
     signed char hi_d[kMaxSlots], hi_p[kMaxSlots];  // entries of send_hi (cy_p >= d)
 };
 
-// Peer-memory halo push of a y-major slab (P2P transport): the fused kernel
-// also stores the updated sites of its 3 storage columns next to each remote
-// face straight into the neighbour's next buffer (its ghost columns), over
-// NVLink.  Element e of this slab lands at peer element e + shift.
+// Peer-memory halo push of a slab (P2P transport): the face kernel also
+// stores the updated face sites straight into the neighbour's buffer (its
+// ghost slots), over NVLink.  Element e of this slab lands at peer element
+// e + shift (a constant per face: slabs share one geometry).
 struct PeerStores {
-    double* lo;  // lo neighbour's next buffer (columns x < 3 go there), or null
-    double* hi;  // hi neighbour's next buffer (columns x >= lx - 3), or null
+    double* lo;  // lo neighbour's buffer, or null
+    double* hi;  // hi neighbour's buffer, or null
     long long lo_shift, hi_shift;
 };
 
@@ -82,7 +82,14 @@ cudaError_t launch_propagate(const double* src, double* dst, const DevGeo& g, co
                              const Segments& seg, int nseg, cudaStream_t s);
 cudaError_t launch_collide(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
                            const ModelParams& mp, double omega, bool strict, bool shift, const Segments& seg,
-                           int nseg, int* flag, cudaStream_t s, const PeerStores* peers = nullptr);
+                           int nseg, int* flag, cudaStream_t s);
+// The fused step on the face sites of (seg, nseg) with the peer stores.
+cudaError_t launch_face(const double* src, double* dst, const DevGeo& g, const Offsets& off, const Faces& fc,
+                        const ModelParams& mp, double omega, bool strict, const Segments& seg, int nseg,
+                        const PeerStores& ps, int* flag, cudaStream_t s);
+// Copies the face sites of (seg, nseg) of buf into the peers (same buffer index).
+cudaError_t launch_face_prime(const double* buf, const DevGeo& g, const Offsets& off, const Segments& seg, int nseg,
+                              const PeerStores& ps, cudaStream_t s);
 // P2P step protocol: wait until the step counters the neighbours wrote into
 // seq[0] (lo) / seq[1] (hi) reach `target` (system-scope acquire; gives up
 // after ~10 s and sets bit 2 of *flag); signal = system-scope release store

@@ -653,7 +653,8 @@ def test_convert_between_layouts(gpu, lbm, src_layout, src_vl):
 
 # --------------------------------------------------------------------------- P2P (peer-memory halo) slabs
 
-@pytest.mark.parametrize("layout,vl", [("caosoa", 8), ("caosoa", 32), ("aos", 1)])
+@pytest.mark.parametrize("layout,vl", [("caosoa", 8), ("caosoa", 32), ("aos", 1), ("soa", 1), ("csoa", 8),
+                                       ("csoa", 32)])
 @pytest.mark.parametrize("variant", ["fused", "unfused"])
 def test_p2p_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, variant):
     """A 1-rank P2P ring: the periodic y wrap goes through the peer-memory push (the fused
@@ -673,7 +674,8 @@ def test_p2p_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, varian
 @pytest.mark.parametrize("nslabs", [2, 4])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 @pytest.mark.parametrize("layout,vl,variant", [("caosoa", 8, "fused"), ("caosoa", 32, "fused"),
-                                               ("aos", 1, "fused"), ("caosoa", 4, "unfused")])
+                                               ("aos", 1, "fused"), ("caosoa", 4, "unfused"), ("soa", 1, "fused"),
+                                               ("csoa", 4, "fused"), ("soa", 1, "unfused")])
 def test_p2p_ring_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, vl, variant):
     """N P2P slabs in one process (separate streams, counters in device memory, pushes into
     each other's ghost columns) step bit-identically to one domain, walls on the outer faces."""
@@ -700,8 +702,8 @@ def test_p2p_ring_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, layout, vl,
 
 
 def test_p2p_errors(gpu, lbm):
-    with pytest.raises(ValueError, match="site-major"):
-        lbm.Simulation.slab("soa", 32, 256, 1, transport="p2p")
+    with pytest.raises(ValueError, match="6 rows"):
+        lbm.Simulation.slab("soa", 32, 8, 1, rank=0, nranks=2, transport="p2p")
     a = lbm.Simulation.slab("caosoa", 32, 256, 8, rank=0, nranks=2, transport="p2p")
     with pytest.raises(ValueError, match="not connected"):
         a.step(1.0, 1)
