@@ -361,7 +361,9 @@ def bench_p2p_ring_emulation(lbm, layout, vl, nslabs, warmup, steps) -> dict:
     return out
 
 
-def bench_variant(lbm, ly, layout, vl, variant, warmup, steps) -> dict:
+def bench_variant(lbm, ly, layout, vl, variant, warmup, steps, hbm_peak: float = 0.0) -> dict:
+    """BASELINE config 3: one step variant on 4096 x ly, with each kernel's roofline fraction
+    (592 B/site per sweep against the HBM peak; collide also against the nominal FP64 peak)."""
     sim = lbm.Simulation(layout, LX, ly, vl, device=0, bc="wall", variant=variant)
     sim.init_rt_device(SEED)
     sim.step(OMEGA, warmup)
@@ -375,7 +377,14 @@ def bench_variant(lbm, ly, layout, vl, variant, warmup, steps) -> dict:
     out = {"mlups": sites * steps / (ms / 1e3) / 1e6, "ms_per_step": ms / steps}
     for k, (tot, n) in kt.items():
         if n:
-            out[f"{k}_ms"] = tot / n
+            kms = tot / n
+            out[f"{k}_ms"] = kms
+            gbs = sites * BYTES_PER_SITE / (kms / 1e3) / 1e9
+            out[f"{k}_GBps"] = gbs
+            if hbm_peak:
+                out[f"{k}_frac_of_hbm"] = gbs / hbm_peak
+            if k in ("fused", "collide"):
+                out[f"{k}_frac_of_fp64_nominal"] = sites * FLOPS_PER_SITE / (kms / 1e3) / (FP64_NOMINAL_TFLOPS * 1e12)
     return out
 
 
@@ -550,7 +559,8 @@ def run_b200(args, dist: Dist):
                              ("caosoa", 32, "unfused")):
             if (lay, var) == (args.layout, args.variant):
                 continue
-            variants[f"{lay}{vl if vl > 1 else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20)
+            variants[f"{lay}{vl if vl > 1 else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20,
+                                                                            hbm_peak)
         line["variants_c3"] = variants
         try:
             line["slab_schedule"] = {
