@@ -11,7 +11,8 @@ import time
 lib = C.CDLL(sys.argv[1])
 layout = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}[sys.argv[2] if len(sys.argv) > 2 else "caosoa"]
 vl = int(sys.argv[3]) if len(sys.argv) > 3 else 32
-variant = {"unfused": 0, "fused": 1}[sys.argv[4] if len(sys.argv) > 4 else "fused"]
+mode = sys.argv[4] if len(sys.argv) > 4 else "fused"  # fused | unfused | propagate (config 1 verb)
+variant = {"unfused": 0, "fused": 1, "propagate": 1}[mode]
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 200
 lx = int(sys.argv[6]) if len(sys.argv) > 6 else 4096
 ly = int(sys.argv[7]) if len(sys.argv) > 7 else 16384
@@ -22,7 +23,19 @@ lib.d2q37_destroy.argtypes = [C.c_void_p]
 h = C.c_void_p()
 assert lib.d2q37_create(layout, lx, ly, vl if layout >= 2 else 1, 0, C.byref(h)) == 0
 assert lib.d2q37_init_rt_device(h, 2018) == 0
-assert lib.d2q37_step(h, 0.8, 20, variant, 1) == 0
+if mode == "propagate":
+    lib.d2q37_bc.argtypes = [C.c_void_p, C.c_int]
+    lib.d2q37_propagate.argtypes = [C.c_void_p]
+    assert lib.d2q37_bc(h, 0) == 0
+
+
+def run(n):
+    if mode == "propagate":
+        for _ in range(n):
+            assert lib.d2q37_propagate(h) == 0
+    else:
+        assert lib.d2q37_step(h, 0.8, n, variant, 1) == 0
+run(20)
 lib.d2q37_sync(h)
 samples = []
 stop = threading.Event()
@@ -45,7 +58,7 @@ th.start()
 best = 1e30
 for _ in range(3):
     t0 = time.perf_counter()
-    assert lib.d2q37_step(h, 0.8, steps, variant, 1) == 0
+    run(steps)
     rc = lib.d2q37_sync(h)
     assert rc == 0 or os.environ.get("AB_IGNORE_ERRORS")  # timing-only variants may compute garbage
     best = min(best, time.perf_counter() - t0)
