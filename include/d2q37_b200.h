@@ -164,24 +164,6 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst);
 int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_in, double* host_out, size_t n,
                        double omega, int nsteps, int math, int device);
 
-/* Multi-GPU y-slabs without NCCL, all four layouts: the fused step kernel of
- * the face sites stores its results straight into the neighbours' ghost
- * slots through NVLink peer memory (site-major layouts in y-major storage:
- * 3 whole columns per face; SoA / CSoA: lane 0's first / lane vl-1's last 3
- * rows), and per-step counters in peer memory order the ranks (DESIGN.md
- * section 5).  create -> export a 256-byte
- * blob -> exchange blobs (any host channel, e.g. torch.distributed) ->
- * connect(lo neighbour's blob, hi neighbour's blob); a 1-rank ring connects
- * to its own blob.  Neighbours in this process are used directly, others are
- * mapped with CUDA IPC.  All ranks must issue the same sequence of steps and
- * state-changing verbs (like NCCL collectives); a rank that waits more than
- * 10 s for a neighbour reports D2Q37_ERR_NCCL from d2q37_sync. */
-int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
-                          d2q37_lattice** out);
-int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]);
-int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BYTES],
-                      const unsigned char hi[D2Q37_P2P_BLOB_BYTES]);
-
 /* Global sums over the physical sites of the state buffer (prv):
  * out = {mass, x-momentum, y-momentum, energy sum |c|^2 f}; deterministic
  * for a given geometry.  Conservation checks at full size. */
@@ -214,7 +196,9 @@ int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed);
 int d2q37_nccl_unique_id(unsigned char id[D2Q37_NCCL_ID_BYTES]);
 /* Rank `rank` of `nranks` owns global rows [rank*ly/nranks, (rank+1)*ly/nranks)
  * of an lx x ly lattice; load/dump take that slab's canonical array (lx x ly/nranks).
- * Halo rows travel by ncclSend/ncclRecv between y neighbours each step.
+ * Halos travel by ncclSend/ncclRecv between y neighbours each step: the 3 face
+ * columns of a y-major (AoS / CAoSoA) slab straight from / into the lattice
+ * buffer, the 26 planned pop-rows of an SoA / CSoA slab through pack buffers.
  * nranks = 1 with a non-NULL id builds a one-rank NCCL ring: the periodic y
  * wrap goes through NCCL send/recv to self (the whole multi-GPU schedule on
  * one GPU); with id = NULL it is a plain single-domain lattice. */
@@ -236,11 +220,29 @@ int d2q37_halo_plan(int lo_d[32], int lo_p[32], int hi_d[32], int hi_p[32]);
 int d2q37_slab_neighbors(int rank, int nranks, int bc, int out[2]);
 /* rank, nranks, first global row, rows of this slab. */
 int d2q37_slab_info(const d2q37_lattice* h, int out[4]);
+/* Multi-GPU y-slabs without NCCL (the P2P transport), all four layouts: the
+ * fused kernel of the face sites stores its results straight into the
+ * neighbours' ghost slots through NVLink peer memory (site-major layouts in
+ * y-major storage: 3 whole columns per face; SoA / CSoA: lane 0's first /
+ * lane vl-1's last 3 rows), and per-step counters in peer memory order the
+ * ranks.  create -> export a 256-byte blob -> exchange
+ * the blobs (any host channel, e.g. torch.distributed) -> connect(lo
+ * neighbour's blob, hi neighbour's blob); a 1-rank ring connects to its own
+ * blob.  Neighbours in this process are used directly, others are mapped
+ * with CUDA IPC.  All ranks must issue the same sequence of steps and
+ * state-changing verbs (like NCCL collectives); a rank that waits more than
+ * 10 s for a neighbour reports D2Q37_ERR_NCCL from d2q37_sync. */
+int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
+                          d2q37_lattice** out);
+int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]);
+int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BYTES],
+                      const unsigned char hi[D2Q37_P2P_BLOB_BYTES]);
 /* Per-kernel device timing (CUDA events recorded around each launch on the
  * handle's stream while profiling is on).  d2q37_kernel_times returns the
  * summed milliseconds and launch counts since the last call, per class:
  * 0 edge (bc), 1 propagate, 2 collide, 3 fused propagate+collide, 4 pack,
- * 5 fused boundary sites of a slab (after its halos arrived). */
+ * 5 fused face sites of a slab (after its halos arrived; P2P: with the peer
+ * stores). */
 int d2q37_set_profiling(d2q37_lattice* h, int on);
 int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
 /* Average device time (ms) of the last step's halo phase that was not hidden
