@@ -5,8 +5,8 @@
   --case unfused    same lattice, unfused steps (edge + propagate + collide)
   --case csoa       same lattice, CSoA vl=32 fused steps
   --case caosoa     same lattice, CAoSoA vl=32 fused steps                    (bench default)
-  --case propagate  1024x8192 SoA Philox input, propagate prv->nxt            (BASELINE config 1)
-  --case collide    1024x8192 SoA c2 input, collide nxt->prv                  (BASELINE config 2)
+  --case propagate  1024x8192 Philox input, propagate prv->nxt (--layout/--vl, default SoA)  (BASELINE config 1)
+  --case collide    1024x8192 c2 input, collide nxt->prv (--layout/--vl, default SoA)         (BASELINE config 2)
 """
 import argparse
 import os
@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--lx", type=int, default=4096)
     ap.add_argument("--ly", type=int, default=16384)
+    ap.add_argument("--layout", default="soa", help="propagate / collide cases: layout (soa, csoa, caosoa, aos)")
+    ap.add_argument("--vl", type=int, default=1)
     a = ap.parse_args()
     if a.case in ("step", "unfused", "csoa", "caosoa"):
         layout, vl = (a.case, 32) if a.case in ("csoa", "caosoa") else ("soa", 1)
@@ -32,14 +34,14 @@ def main():
             s.step(0.8, 1, sync=False)
         s.sync()
     elif a.case == "propagate":
-        s = lbm.Simulation("soa", 1024, 8192)
+        s = lbm.Simulation(a.layout, 1024, 8192, a.vl)
         s.init_philox(12345)
         s.bc("periodic")
         for _ in range(a.steps):
             s.propagate_only(sync=False)
         s.sync()
     else:
-        s = lbm.Simulation("soa", 1024, 8192)
+        s = lbm.Simulation(a.layout, 1024, 8192, a.vl)
         s.load(lbm.make_lattice("c2", 1024, 8192, 12345), which=1)
         for _ in range(a.steps):
             s.collide(1.0, sync=False)
