@@ -237,6 +237,13 @@ int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int ra
 int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]);
 int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BYTES],
                       const unsigned char hi[D2Q37_P2P_BLOB_BYTES]);
+/* Single-process multi-GPU (SURVEY.md 8(b) "create_multi"): nslabs P2P
+ * y-slabs of one lx x ly lattice, slab r on devices[r] (devices may repeat:
+ * several slabs per GPU), connected as a ring; out[r] are ordinary slab
+ * handles (load/dump their rows).  multi_step advances all of them in
+ * lockstep and syncs. */
+int d2q37_create_multi(int layout, int lx, int ly, int vl, int nslabs, const int* devices, d2q37_lattice** out);
+int d2q37_multi_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps, int variant, int bc);
 /* Per-kernel device timing (CUDA events recorded around each launch on the
  * handle's stream while profiling is on).  d2q37_kernel_times returns the
  * summed milliseconds and launch counts since the last call, per class:

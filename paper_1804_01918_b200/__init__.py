@@ -34,7 +34,7 @@ import numpy as np
 __all__ = [
     "NPOP", "Model", "Simulation", "SlabGroup", "NonPhysicalError", "model", "mlups",
     "propagate_gbps", "collide_gflops", "make_lattice", "library_path", "nccl_unique_id",
-    "COLLIDE_FLOPS_PER_SITE", "__version__", "convert", "scalar_steps", "p2p_ring", "step_slabs",
+    "COLLIDE_FLOPS_PER_SITE", "__version__", "convert", "scalar_steps", "p2p_ring", "step_slabs", "MultiGPU",
 ]
 __version__ = "0.1.0"
 
@@ -136,6 +136,8 @@ def _load():
         "d2q37_kernel_times": (i, [vp, _dp, P(C.c_long)]),
         "d2q37_convert": (i, [vp, vp]),
         "d2q37_create_slab_p2p": (i, [i, i, i, i, i, i, i, P(vp)]),
+        "d2q37_create_multi": (i, [i, i, i, i, i, P(C.c_int), P(vp)]),
+        "d2q37_multi_step": (i, [P(vp), i, d, i, i, i]),
         "d2q37_p2p_export": (i, [vp, C.c_char_p]),
         "d2q37_p2p_connect": (i, [vp, C.c_char_p, C.c_char_p]),
         "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
@@ -668,3 +670,26 @@ class SlabGroup:
         _check(_load().d2q37_group_step(self._hs, self.nslabs, float(omega), int(n),
                                         VARIANTS[variant or self.variant], BCS[bc or self.bc_mode]))
         self.slabs[0].sync()
+
+
+class MultiGPU(SlabGroup):
+    """One lattice as P2P y-slabs on several GPUs driven by this one process
+    (d2q37_create_multi; SURVEY.md 8(b) ``create_multi``).  ``devices[r]`` holds slab r;
+    devices may repeat (several slabs per GPU).  Same load / dump / step as SlabGroup."""
+
+    def __init__(self, layout: str, lx: int, ly: int, vl: int = 1, devices=(0, 0), *, bc: str = "periodic",
+                 variant: str = "fused", math: str = "fast", mdl: Model | None = None):
+        lib = _load()
+        n = len(devices)
+        hs = (C.c_void_p * n)()
+        devs = (C.c_int * n)(*[int(v) for v in devices])
+        _check(lib.d2q37_create_multi(LAYOUTS[layout], lx, ly, vl, n, devs, hs))
+        self._hs = hs
+        self.slabs = [Simulation(layout, lx, ly // n, vl, device=int(devices[r]), bc=bc, variant=variant,
+                                 math=math, mdl=mdl, _handle=C.c_void_p(hs[r])) for r in range(n)]
+        self.lx, self.ly, self.nslabs, self.devices = lx, ly, n, list(devices)
+        self.bc_mode, self.variant = bc, variant
+
+    def step(self, omega: float = 1.0, n: int = 1, *, bc: str | None = None, variant: str | None = None):
+        _check(_load().d2q37_multi_step(self._hs, self.nslabs, float(omega), int(n),
+                                        VARIANTS[variant or self.variant], BCS[bc or self.bc_mode]))

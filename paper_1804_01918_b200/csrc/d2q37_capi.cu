@@ -1709,6 +1709,52 @@ int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BY
     return D2Q37_OK;
 }
 
+int d2q37_create_multi(int layout, int lx, int ly, int vl, int nslabs, const int* devices, d2q37_lattice** out) {
+    if (!out || !devices || nslabs < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad multi-GPU arguments");
+    std::vector<d2q37_lattice*> slabs(nslabs, nullptr);
+    auto bail = [&](int rc) {
+        for (d2q37_lattice* sl : slabs) d2q37_destroy(sl);
+        for (int r = 0; r < nslabs; ++r) out[r] = nullptr;
+        return rc;
+    };
+    std::vector<std::vector<unsigned char>> blobs(nslabs, std::vector<unsigned char>(D2Q37_P2P_BLOB_BYTES));
+    for (int r = 0; r < nslabs; ++r) {
+        int rc = d2q37_create_slab_p2p(layout, lx, ly, vl, devices[r], r, nslabs, &slabs[r]);
+        if (rc == D2Q37_OK) rc = d2q37_p2p_export(slabs[r], blobs[r].data());
+        if (rc != D2Q37_OK) {
+            const std::string why = g_last_error;
+            bail(rc);
+            return fail(rc, "%s", why.c_str());
+        }
+    }
+    for (int r = 0; r < nslabs; ++r) {
+        const int rc = d2q37_p2p_connect(slabs[r], blobs[(r - 1 + nslabs) % nslabs].data(),
+                                         blobs[(r + 1) % nslabs].data());
+        if (rc != D2Q37_OK) {
+            const std::string why = g_last_error;
+            bail(rc);
+            return fail(rc, "%s", why.c_str());
+        }
+    }
+    for (int r = 0; r < nslabs; ++r) out[r] = slabs[r];
+    return D2Q37_OK;
+}
+
+int d2q37_multi_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps, int variant, int bc) {
+    if (!slabs || nslabs < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad multi-GPU slabs");
+    for (int r = 0; r < nslabs; ++r) {
+        RET(check_handle(slabs[r]));
+        if (slabs[r]->transport != kTransportP2P || slabs[r]->nranks != nslabs)
+            return fail(D2Q37_ERR_INVALID_ARGUMENT, "not the slabs of one d2q37_create_multi lattice");
+    }
+    // lockstep: every slab's step k is enqueued before any slab's step k + 1, so no
+    // slab's counter wait depends on work the host has not issued yet
+    for (int k = 0; k < nsteps; ++k)
+        for (int r = 0; r < nslabs; ++r) RET(d2q37_step(slabs[r], omega, 1, variant, bc));
+    for (int r = 0; r < nslabs; ++r) RET(d2q37_sync(slabs[r]));
+    return D2Q37_OK;
+}
+
 int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslabs, d2q37_lattice** out) {
     if (!out || nslabs < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "bad group arguments");
     std::vector<d2q37_lattice*> slabs(nslabs, nullptr);

@@ -830,3 +830,19 @@ def test_run_validation_same_seed_same_report(gpu, lbm):
     o = v.ValidationOptions(geometries=[(16, 32)], vls=[1, 4], steps=3, corrupt_population=11)
     a, b = v.run_validation(o), v.run_validation(o)
     assert a == b and not a.passed
+
+
+@pytest.mark.parametrize("layout,vl", [("caosoa", 32), ("csoa", 8)])
+def test_create_multi_bitwise_equals_single_domain(gpu, lbm, layout, vl):
+    """d2q37_create_multi / d2q37_multi_step (single-process multi-GPU): 3 slabs, here all on
+    cuda:0, stepped in lockstep through the P2P protocol with walls, equal to one domain."""
+    lx, ly = 96, 768
+    init = lbm.make_lattice("random", lx, ly, seed=51)
+    ref = sim_of(lbm, layout, lx, ly, vl, bc="wall")
+    ref.load(init)
+    ref.step(1.1, 5)
+    m = lbm.MultiGPU(layout, lx, ly, vl, devices=[0, 0, 0], bc="wall")
+    m.load(init)
+    m.step(1.1, 5)
+    assert np.array_equal(m.dump(), ref.dump())
+    m.close()
