@@ -205,6 +205,61 @@ inline CanonicalLattice scalar_steps(const VelocityModel& m, const CanonicalLatt
     return out;
 }
 
+/// One lattice as P2P y-slabs on several GPUs of this process
+/// (d2q37_create_multi): slab r holds rows [r*ly/n, (r+1)*ly/n) on devices[r].
+/// load / dump take the whole canonical lattice; step advances every slab in
+/// lockstep through the peer-memory halo protocol.
+class MultiGpuLattice {
+  public:
+    MultiGpuLattice(LayoutKind kind, Geometry g, const std::vector<int>& devices) : geom_(g), h_(devices.size()) {
+        if (g.hx != kHaloExtent || g.hy != kHaloExtent)
+            throw std::invalid_argument("halos narrower than the velocity reach");
+        check(d2q37_create_multi(int(kind), g.lx, g.ly, g.vl, int(devices.size()), devices.data(), h_.data()));
+    }
+    ~MultiGpuLattice() {
+        for (d2q37_lattice* h : h_) d2q37_destroy(h);
+    }
+    MultiGpuLattice(const MultiGpuLattice&) = delete;
+    MultiGpuLattice& operator=(const MultiGpuLattice&) = delete;
+
+    int slabs() const { return int(h_.size()); }
+
+    void load(const CanonicalLattice& c) {
+        if (c.lx != geom_.lx || c.ly != geom_.ly) throw std::invalid_argument("from_canonical: dimension mismatch");
+        const int n = slabs(), ny = geom_.ly / n;
+        std::vector<double> part(size_t(kNpop) * geom_.lx * ny);
+        for (int r = 0; r < n; ++r) {
+            for (int p = 0; p < kNpop; ++p)
+                for (int x = 0; x < geom_.lx; ++x)
+                    for (int y = 0; y < ny; ++y)
+                        part[(size_t(p) * geom_.lx + x) * ny + y] = c.values[(size_t(p) * geom_.lx + x) * geom_.ly + r * ny + y];
+            check(d2q37_load_canonical(h_[r], part.data(), part.size()));
+        }
+    }
+    CanonicalLattice dump() const {
+        CanonicalLattice c = make_canonical(geom_.lx, geom_.ly);
+        const int n = slabs(), ny = geom_.ly / n;
+        std::vector<double> part(size_t(kNpop) * geom_.lx * ny);
+        for (int r = 0; r < n; ++r) {
+            check(d2q37_dump_canonical(h_[r], part.data(), part.size()));
+            for (int p = 0; p < kNpop; ++p)
+                for (int x = 0; x < geom_.lx; ++x)
+                    for (int y = 0; y < ny; ++y)
+                        c.values[(size_t(p) * geom_.lx + x) * geom_.ly + r * ny + y] = part[(size_t(p) * geom_.lx + x) * ny + y];
+        }
+        return c;
+    }
+    void step(const VelocityModel& m, double omega, int nsteps = 1, StepVariant variant = StepVariant::Fused,
+              Boundary bc = Boundary::Periodic) {
+        for (d2q37_lattice* h : h_) check(d2q37_set_model(h, &m.raw()));
+        check(d2q37_multi_step(h_.data(), slabs(), omega, nsteps, int(variant), int(bc)));
+    }
+
+  private:
+    Geometry geom_;
+    std::vector<d2q37_lattice*> h_;
+};
+
 inline void halo_exchange(LatticeState& s, Boundary bc = Boundary::Periodic) {
     check(d2q37_bc(s.handle(), int(bc)));
     s.sync();

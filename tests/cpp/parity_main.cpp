@@ -18,6 +18,8 @@
 //   G8  run_validation's scalar device reference <= 1e-12 vs the reference's
 //       oracle_propagate + oracle_collide (5 steps); convert between device
 //       layouts preserves every physical site                           (validation.cpp, layout.cpp:105-116)
+//   G9  a 4-slab MultiGpuLattice (P2P halos; all slabs on device 0 here)
+//       <= 1e-12 vs the reference lbm::step over 6 periodic steps
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -230,17 +232,35 @@ bool g8() {
     return true;
 }
 
+bool g9() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(96, 256, 909);
+    lbm::LatticeState ref{lbm::Descriptor(lbm::LayoutKind::CAoSoA, [] {
+        lbm::Geometry g{96, 256};
+        g.vl = 8;
+        return g;
+    }())};
+    ref.load(init);
+    lbm::ThreadPool pool(4);
+    for (int n = 0; n < 6; ++n) lbm::step(ref, m, 1.05, pool);
+    lbm_b200::MultiGpuLattice gpu(B::CAoSoA, lbm_b200::Geometry{96, 256, 3, 3, 8}, {0, 0, 0, 0});
+    gpu.load(to_gpu(init));
+    gpu.step(reference_model(), 1.05, 6);
+    return max_rel(gpu.dump().values, ref.dump().values) <= 1e-12;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::array<std::pair<const char*, bool (*)()>, 8> all = {{{"G1", g1},
+    const std::array<std::pair<const char*, bool (*)()>, 9> all = {{{"G1", g1},
                                                                      {"G2", g2},
                                                                      {"G3", g3},
                                                                      {"G4", g4},
                                                                      {"G5", g5},
                                                                      {"G6", g6},
                                                                      {"G7", g7},
-                                                                     {"G8", g8}}};
+                                                                     {"G8", g8},
+                                                                     {"G9", g9}}};
     int failures = 0;
     for (const auto& [name, fn] : all) {
         if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;
