@@ -230,8 +230,9 @@ int d2q37_slab_info(const d2q37_lattice* h, int out[4]);
  * neighbour's blob, hi neighbour's blob); a 1-rank ring connects to its own
  * blob.  Neighbours in this process are used directly, others are mapped
  * with CUDA IPC.  All ranks must issue the same sequence of steps and
- * state-changing verbs (like NCCL collectives); a rank that waits more than
- * 10 s for a neighbour reports D2Q37_ERR_NCCL from d2q37_sync. */
+ * state-changing verbs (like NCCL collectives); a rank that waits longer than
+ * D2Q37_P2P_TIMEOUT_S seconds (environment, default 60) for a neighbour
+ * reports D2Q37_ERR_NCCL from d2q37_sync instead of hanging. */
 int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
                           d2q37_lattice** out);
 int d2q37_p2p_export(const d2q37_lattice* h, unsigned char blob[D2Q37_P2P_BLOB_BYTES]);

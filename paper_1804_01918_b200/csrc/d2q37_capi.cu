@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -777,9 +778,20 @@ int ymajor_step_nccl_unfused(d2q37_lattice* h, double omega, int bc) {
 // own stores.  A prime (after load / init / swap) pushes the current face
 // columns with peer copies under the same counter protocol.
 
+// How long a rank waits for a neighbour before reporting instead of hanging:
+// D2Q37_P2P_TIMEOUT_S (default 60 s).
+unsigned long long p2p_timeout_ns() {
+    static const unsigned long long ns = [] {
+        const char* v = std::getenv("D2Q37_P2P_TIMEOUT_S");
+        const double sec = v ? std::atof(v) : 60.0;
+        return (unsigned long long)((sec > 0 ? sec : 60.0) * 1e9);
+    }();
+    return ns;
+}
+
 int p2p_wait(d2q37_lattice* h, int bc, unsigned long long target) {
     CK(launch_p2p_wait(h->d_seq, face_lo_of(h, bc) == kFaceRemote, face_hi_of(h, bc) == kFaceRemote, target,
-                       h->d_flag, h->halo_stream));
+                       p2p_timeout_ns(), h->d_flag, h->halo_stream));
     return D2Q37_OK;
 }
 
@@ -1287,7 +1299,7 @@ int d2q37_sync(d2q37_lattice* h) {
         *h->h_flag = 0;
         CK(cudaMemsetAsync(h->d_flag, 0, sizeof(int), h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        if (f & 2) return fail(D2Q37_ERR_NCCL, "p2p halo: a neighbour did not reach the step within 10 s");
+        if (f & 2) return fail(D2Q37_ERR_NCCL, "p2p halo: a neighbour did not reach the step in time (D2Q37_P2P_TIMEOUT_S)");
         return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
     }
     return D2Q37_OK;

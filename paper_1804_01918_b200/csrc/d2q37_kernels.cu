@@ -321,13 +321,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 __global__ void k_p2p_wait(const unsigned long long* seq, int need_lo, int need_hi, unsigned long long target,
-                           int* flag) {
+                           unsigned long long timeout_ns, int* flag) {
     const unsigned long long t0 = global_ns();
     for (;;) {
         const bool lo = !need_lo || ld_acquire_sys(&seq[0]) >= target;
         const bool hi = !need_hi || ld_acquire_sys(&seq[1]) >= target;
         if (lo && hi) return;
-        if (global_ns() - t0 > 10000000000ULL) {  // a neighbour never arrived: report, do not hang
+        if (global_ns() - t0 > timeout_ns) {  // a neighbour never arrived: report, do not hang
             atomicOr(flag, 2);
             return;
         }
@@ -788,10 +788,10 @@ cudaError_t launch_face_prime(const double* buf, const DevGeo& g, const Offsets&
 }
 
 cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
-                            int* flag, cudaStream_t s) {
+                            unsigned long long timeout_ns, int* flag, cudaStream_t s) {
     if (!need_lo && !need_hi) return cudaSuccess;
     (void)cudaGetLastError();
-    k_p2p_wait<<<1, 1, 0, s>>>(seq, need_lo ? 1 : 0, need_hi ? 1 : 0, target, flag);
+    k_p2p_wait<<<1, 1, 0, s>>>(seq, need_lo ? 1 : 0, need_hi ? 1 : 0, target, timeout_ns, flag);
     return cudaGetLastError();
 }
 

@@ -92,10 +92,10 @@ cudaError_t launch_face_prime(const double* buf, const DevGeo& g, const Offsets&
                               const PeerStores& ps, cudaStream_t s);
 // P2P step protocol: wait until the step counters the neighbours wrote into
 // seq[0] (lo) / seq[1] (hi) reach `target` (system-scope acquire; gives up
-// after ~10 s and sets bit 2 of *flag); signal = system-scope release store
-// of `value` into the neighbours' counter slots.
+// after timeout_ns and sets bit 2 of *flag); signal = system-scope release
+// store of `value` into the neighbours' counter slots.
 cudaError_t launch_p2p_wait(const unsigned long long* seq, bool need_lo, bool need_hi, unsigned long long target,
-                            int* flag, cudaStream_t s);
+                            unsigned long long timeout_ns, int* flag, cudaStream_t s);
 cudaError_t launch_copy(double* dst, const double* src, long long n, cudaStream_t s);
 // Loads every kernel of this library on the current device (see d2q37_kernels.cu).
 cudaError_t preload_kernels();
