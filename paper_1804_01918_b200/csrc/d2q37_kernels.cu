@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     else
         gather_site<kPullNone, TR, AM>(f, src, e, g, off, fc, x, q);
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
-    if (bad) *flag = 1;
+    if (bad) atomicOr(flag, 1);  // keeps other status bits (P2P timeout = 2)
     store_site<AM>(dst, e, g, off, f);
 }
 
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kStreamThreads, kCollideMinBlocks)
     double f[kNpop];
     gather_site<kPullEdge, TR, kAddr64>(f, src, e, g, off, fc, x, q);
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
-    if (bad) *flag = 1;
+    if (bad) atomicOr(flag, 1);  // keeps other status bits (P2P timeout = 2)
     store_site<kAddr64>(dst, e, g, off, f);
     const int side = face_side<TR>(g, x, q);
     double* peer = side == 0 ? ps.lo : side == 1 ? ps.hi : nullptr;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256) k_scalar_collide(const double* __restrict
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) f[p] = in[p * plane + t];
     const bool bad = STRICT ? collide_site<true>(f, omega, mp) : collide_site_sym(f, omega, mp);
-    if (bad) *flag = 1;
+    if (bad) atomicOr(flag, 1);  // keeps other status bits (P2P timeout = 2)
 #pragma unroll
     for (int p = 0; p < kNpop; ++p) out[p * plane + t] = f[p];
 }

@@ -846,3 +846,29 @@ def test_create_multi_bitwise_equals_single_domain(gpu, lbm, layout, vl):
     m.step(1.1, 5)
     assert np.array_equal(m.dump(), ref.dump())
     m.close()
+
+
+def test_p2p_missing_neighbour_reports_instead_of_hanging(gpu, lbm):
+    """Failure detection: slab 0 of a 2-slab ring steps while slab 1 never does; with
+    D2Q37_P2P_TIMEOUT_S=1 the wait gives up and sync raises instead of hanging."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1804_01918_b200 as lbm\n"
+        "a, b = lbm.p2p_ring('caosoa', 96, 256, 8, 2)\n"
+        "a.init_rt_device(1)\n"
+        "b.init_rt_device(1)\n"
+        "a.step(1.0, 1, sync=False)\n"
+        "try:\n"
+        "    a.sync()\n"
+        "    print('no error')\n"
+        "except RuntimeError as e:\n"
+        "    print('reported:', e)\n" % ROOT)
+    env = dict(__import__("os").environ, D2Q37_P2P_TIMEOUT_S="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "reported:" in r.stdout and "in time" in r.stdout, r.stdout
