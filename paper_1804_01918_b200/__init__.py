@@ -46,7 +46,7 @@ COLLIDE_FLOPS_PER_SITE = 1522  # VelocityModel::kCollideFlopsPerSite (model.hpp:
 OK, ERR_INVALID, ERR_NON_PHYSICAL, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(6)
 LAYOUTS = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}
 BCS = {"periodic": 0, "wall": 1}
-VARIANTS = {"unfused": 0, "fused": 1}
+VARIANTS = {"unfused": 0, "fused": 1, "fused2": 2}
 MATHS = {"fast": 0, "strict": 1}
 INITS = {"random": 0, "equilibrium": 1, "shear": 2, "rt": 3, "c2": 4, "philox": 5}
 

@@ -585,6 +585,15 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
     return D2Q37_OK;
 }
 
+// Two time steps in one HBM sweep (D2Q37_FUSED2, d2q37_step2.cu).
+int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
+    ProfScope ps(h, kProfFused);
+    CK(launch_step2(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, h->d_flag, h->stream));
+    h->cur = 1 - h->cur;
+    h->time_step += 2;
+    return D2Q37_OK;
+}
+
 void drop_step_graph(d2q37_lattice* h) {
     if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
     h->graph = d2q37_lattice::StepGraph{};
@@ -1244,14 +1253,22 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
     RET(check_handle(h));
     RET(validate_bc(h, bc));
     if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
-    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
     DeviceGuard dg(h->device);
     if (h->transport == kTransportGroup) {
         d2q37_lattice** slabs = h->group.data();
+        if (variant == D2Q37_FUSED2) variant = D2Q37_FUSED;
         return d2q37_group_step(slabs, int(h->group.size()), omega, nsteps, variant, bc);
     }
     const bool slab = !local_only(h) && remote_faces(h, bc);
     int s = 0;
+    if (variant == D2Q37_FUSED2) {
+        const Faces fc = step_faces(h, bc);
+        if (!slab && h->math == D2Q37_MATH_FAST && step2_supported(h->g, fc))
+            for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
+        variant = D2Q37_FUSED;  // the odd last step, and every layout / case k_step2 does not cover
+    }
     if (!slab && !h->prof_on && nsteps >= kGraphSteps) {
         // Launch-bound small lattices: replay kGraphSteps steps as one CUDA graph.
         RET(ensure_step_graph(h, omega, variant, bc));

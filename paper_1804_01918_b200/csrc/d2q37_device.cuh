@@ -253,7 +253,15 @@ __device__ __forceinline__ void eq_axis(double (&f)[kNpop], const double* mom, c
     }
 }
 
-__device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omega, const ModelParams& mp) {
+// collide_site_sym in two parts -- the moments (consume all 37 inputs) and the
+// relaxation -- so a caller can issue independent work in between (k_step2
+// issues the next column's loads there).
+struct SymMoments {
+    double rho;
+    double mom[kNmom];
+};
+
+__device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const ModelParams& mp, SymMoments& m) {
     double rho = 0.0;
 #pragma unroll
     for (int i = 0; i < kNpop; ++i) rho += f[i];
@@ -276,7 +284,7 @@ __device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omeg
     const double dt = temp - mp.t0;
     const double ux2 = ux * ux, uy2 = uy * uy, uxuy = ux * uy;
     const double dt3 = 3.0 * dt, dt6 = 6.0 * dt, dt2 = dt * dt, dt2x3 = 3.0 * dt2;
-    double mom[kNmom];
+    double* mom = m.mom;
     mom[0] = ux;
     mom[1] = uy;
     mom[2] = ux2 + dt;
@@ -291,6 +299,14 @@ __device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omeg
     mom[11] = uxuy * uxuy + dt * (ux2 + uy2) + dt2;
     mom[12] = uxuy * (uy2 + dt3);
     mom[13] = uy2 * (uy2 + dt6) + dt2x3;
+    m.rho = rho;
+    return bad;
+}
+
+__device__ __forceinline__ void sym_relax(double (&f)[kNpop], const SymMoments& m, double omega,
+                                          const ModelParams& mp) {
+    const double* mom = m.mom;
+    const double rho = m.rho;
     {  // rest velocity: even terms only
         const double* g = mp.eq[0];
         double ee = fma(g[2], mom[2], 1.0);
@@ -309,6 +325,12 @@ __device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omeg
     eq_quad<2, 2>(f, mom, mp, rho, omega);
     eq_quad<3, 1>(f, mom, mp, rho, omega);
     eq_quad<1, 3>(f, mom, mp, rho, omega);
+}
+
+__device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omega, const ModelParams& mp) {
+    SymMoments m;
+    const bool bad = sym_moments(f, mp, m);
+    sym_relax(f, m, omega, mp);
     return bad;
 }
 

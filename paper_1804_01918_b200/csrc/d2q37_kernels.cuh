@@ -113,6 +113,11 @@ cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, 
 // halo-free canonical array: in -> tmp -> out (validation.cpp:13-38).
 cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int lx, int ly, const ModelParams& mp,
                                double omega, bool strict, int* flag, cudaStream_t s);
+// Two fused steps in one sweep (d2q37_step2.cu): SoA (vl = 1), x-major storage,
+// periodic x, periodic or wall y faces, FAST math.  src and dst must differ.
+bool step2_supported(const DevGeo& g, const Faces& fc);
+cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                         double omega, int* flag, cudaStream_t s);
 cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
 
 }  // namespace d2q37

@@ -1,0 +1,233 @@
+// d2q37_step2.cu -- two D2Q37 time steps per HBM sweep (temporal blocking).
+//
+// The single-step kernel (k_collide<.., SHIFT>) moves the algorithmic 592 B per
+// site and step at ~105 % of the measured copy bandwidth, so past it a step
+// has to cost fewer HBM bytes.  k_step2 reads the state once and writes the
+// state two steps later: 592 B per site per TWO steps.
+//
+// Storage: SoA (layout.hpp:74-75, vl = 1, x-major), the padded buffer of the
+// other kernels; physical sites only are read and written, the boundary is
+// resolved in the kernel (x periodic; y periodic or specular wall).
+//
+// Schedule (persistent CTAs, one per SM):
+//   * the lattice is cut into bands of kT2Out = 122 rows; a CTA walks a
+//     contiguous range of (band, column) items in band-major order, marching
+//     along x;
+//   * producer warps (threads 0-127) compute step 1 -- the pull of step
+//     kernels.cpp:50-63 from HBM plus collide, model.cpp:293-298 -- for the 128
+//     rows y0-3 .. y0+124 of column r and park the result in a shared-memory
+//     ring; the next column's 37 loads are issued before this column's
+//     collide (register double buffer);
+//   * consumer warps (threads 128-255) compute step 2 for the 122 rows of
+//     column r-4, pulling every population from the ring, and stream it to
+//     HBM;
+//   * population p of a step-1 column is read by step 2 of column r + cx_p,
+//     i.e. it lives cx_p + 4 iterations (+1: producer and consumer run
+//     concurrently), so the ring holds sum_p (cx_p + 5) = 185 population
+//     columns of 128 doubles = 185 KB.
+// Every site is updated with the same gathered values and the same
+// collide_site_sym as the single-step kernel, so two steps of k_step2 are bit
+// for bit two steps of k_collide<FAST, SHIFT> (tests/test_gpu_parity.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <utility>
+
+#include "d2q37_device.cuh"
+#include "d2q37_kernels.cuh"
+
+namespace d2q37 {
+
+namespace {
+
+constexpr int kT2Band = 128;                    // step-1 rows per band column (= producer threads)
+constexpr int kT2Out = kT2Band - 2 * kHalo;     // step-2 (output) rows per band
+D2Q37_HD constexpr int t2_depth(int p) { return cx_of(p) + 5; }
+D2Q37_HD constexpr int t2_base(int p) {
+    int s = 0;
+    for (int q = 0; q < p; ++q) s += t2_depth(q);
+    return s;
+}
+constexpr int kT2RingCols = t2_base(kNpop);  // 185
+D2Q37_HD constexpr int ybar_of(int p) { return vel_index(cx_of(p), -cy_of(p)); }
+
+// Compile-time loop over the populations (keeps ring offsets constants).
+template <typename F, int... Ps>
+__device__ __forceinline__ void for_pops_(F&& f, std::integer_sequence<int, Ps...>) {
+    (f(std::integral_constant<int, Ps>{}), ...);
+}
+template <typename F>
+__device__ __forceinline__ void for_pops(F&& f) {
+    for_pops_(f, std::make_integer_sequence<int, kNpop>{});
+}
+
+__device__ __forceinline__ int wrap_mod(int v, int n) {
+    if (v < 0) v += n;
+    else if (v >= n) v -= n;
+    if (v < 0 || v >= n) {  // degenerate extents (n < 7)
+        v %= n;
+        if (v < 0) v += n;
+    }
+    return v;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(2 * kT2Band, 1)
+    k_step2(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
+            double omega, int nbands, long long per_cta, int* __restrict__ flag) {
+    extern __shared__ double ring[];
+    const bool prod = threadIdx.x < kT2Band;
+    const int tid = threadIdx.x & (kT2Band - 1);
+    const int lx = g.lx, ly = g.ly;
+    const bool wall_lo = fc.lo == kFaceWall, wall_hi = fc.hi == kFaceWall;
+    // element of (p = 0, x = 0, y = 0); site (x, y) of population p at + p*plane + x*cs + y
+    const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
+    double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
+    const long long plane = g.pstride, cs = g.cstride;
+    const long long total = (long long)nbands * lx;
+    long long item = (long long)blockIdx.x * per_cta;
+    const long long item_end = min(total, item + per_cta);
+    bool bad = false;
+    while (item < item_end) {
+        const int band = (int)(item / lx);
+        const int xs = (int)(item % lx);
+        const int xe = (int)min((long long)lx, xs + (item_end - item));
+        item += xe - xs;
+        const int y0 = band * kT2Out;
+        const int ny = min(kT2Out, ly - y0);
+        const int niter = xe - xs + 7;  // producer rows t = 0 .. niter-2, consumer t = 7 .. niter-1
+        if (prod) {
+            // Step-1 row of this thread: y0 - 3 + tid, periodic image; beyond a
+            // wall the value is never read (step 2 mirrors into the lattice).
+            const int yr = y0 - kHalo + tid;
+            int y1;
+            if (yr >= 0 && yr < ly)
+                y1 = yr;
+            else if ((yr < 0 && wall_lo) || (yr >= ly && wall_hi))
+                y1 = min(max(yr, 0), ly - 1);
+            else
+                y1 = wrap_mod(yr, ly);
+            // pull row of y1 - cy (k = cy + 3) and whether it is a wall image
+            // (then population ybar(p) is read: specular reflection)
+            int yo[2 * kHalo + 1];
+            unsigned mirm = 0;
+#pragma unroll
+            for (int k = 0; k < 2 * kHalo + 1; ++k) {
+                int ys = y1 - (k - kHalo);
+                const bool m = (ys < 0 && wall_lo) || (ys >= ly && wall_hi);
+                if (m)
+                    ys = ys < 0 ? -1 - ys : 2 * ly - 1 - ys;
+                else
+                    ys = wrap_mod(ys, ly);
+                mirm |= unsigned(m) << k;
+                yo[k] = ys;
+            }
+            auto load = [&](double(&v)[kNpop], int r) {
+                const int rw = wrap_mod(r, lx);
+                int col[2 * kHalo + 1];  // element offset of source column cx = k - 3 (< 2^31: one plane)
+#pragma unroll
+                for (int k = 0; k < 2 * kHalo + 1; ++k) col[k] = wrap_mod(rw - (k - kHalo), lx) * int(cs);
+#pragma unroll
+                for (int p = 0; p < kNpop; ++p) {
+                    const int k = cy_of(p) + kHalo;
+                    const int pp = (mirm >> k) & 1u ? ybar_of(p) : p;
+                    v[p] = __ldg(sb + pp * plane + (col[cx_of(p) + kHalo] + yo[k]));
+                }
+            };
+            auto body = [&](double(&f)[kNpop], double(&fn)[kNpop], int t) {
+                if (t < niter - 1) {
+                    const int r = xs - kHalo + t;
+                    // moments first (they consume all 37 loads of this column), then
+                    // the next column's loads, then the relaxation: the loads stay
+                    // in flight for the relaxation, the ring stores and the barrier
+                    SymMoments m;
+                    bad |= sym_moments(f, mp, m);
+                    asm volatile("" ::"d"(m.rho), "d"(m.mom[0]), "d"(m.mom[13]) : "memory");
+                    if (t < niter - 2) load(fn, r + 1);
+                    sym_relax(f, m, omega, mp);
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2_base(p), dp = t2_depth(p);
+                        ring[(rb + t % dp) * kT2Band + tid] = f[p];
+                    });
+                }
+                __syncthreads();
+            };
+            double fa[kNpop], fb[kNpop];
+            load(fa, xs - kHalo);
+            int t = 0;
+#pragma unroll 1
+            for (; t + 1 < niter; t += 2) {
+                body(fa, fb, t);
+                body(fb, fa, t + 1);
+            }
+            if (t < niter) body(fa, fb, t);
+        } else {
+            const int y = y0 + tid;
+            const bool active = tid < ny;
+            // ring position of y - cy (k = cy + 3) and whether it is a wall image
+            int pos[2 * kHalo + 1];
+            unsigned mirm = 0;
+#pragma unroll
+            for (int k = 0; k < 2 * kHalo + 1; ++k) {
+                int ys = y - (k - kHalo);
+                const bool m = (ys < 0 && wall_lo) || (ys >= ly && wall_hi);
+                if (m) ys = ys < 0 ? -1 - ys : 2 * ly - 1 - ys;
+                mirm |= unsigned(m) << k;
+                pos[k] = ys - (y0 - kHalo);
+            }
+#pragma unroll 1
+            for (int t = 0; t < niter; ++t) {
+                if (t >= 7 && active) {
+                    double v[kNpop];
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, dp = t2_depth(p);
+                        constexpr int k = cy_of(p) + kHalo, rb = t2_base(p), rbb = t2_base(ybar_of(p));
+                        const int base = (mirm >> k) & 1u ? rbb : rb;
+                        v[p] = ring[(base + (t + 1) % dp) * kT2Band + pos[k]];
+                    });
+                    bad |= collide_site_sym(v, omega, mp);
+                    double* __restrict__ o = db + (long long)(xs - 7 + t) * cs + y;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(o + p * plane, v[p]);
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+bool step2_supported(const DevGeo& g, const Faces& fc) {
+    const bool face_ok = (fc.lo == kFacePeriodic || fc.lo == kFaceWall) && (fc.hi == kFacePeriodic || fc.hi == kFaceWall);
+    return g.vl == 1 && !g.tr && g.pstride != g.vl && face_ok && fc.col_lo == kFacePeriodic &&
+           fc.col_hi == kFacePeriodic && g.lx >= 1 && g.ly >= kHalo &&
+           (long long)(g.lx + 2 * kHalo) * g.cstride < 0x7fffffffLL;  // 32-bit offsets inside a plane
+}
+
+size_t step2_smem_bytes() { return (size_t)kT2RingCols * kT2Band * sizeof(double); }
+
+cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                         double omega, int* flag, cudaStream_t s) {
+    constexpr int kMaxDev = 64;
+    static int nsm_of[kMaxDev] = {};  // per device: SM count once the attribute is set
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int nsm = dev < kMaxDev ? nsm_of[dev] : 0;
+    if (nsm == 0) {
+        e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step2_smem_bytes());
+        if (e != cudaSuccess) return e;
+        if (dev < kMaxDev) nsm_of[dev] = nsm;
+    }
+    const int nbands = (g.ly + kT2Out - 1) / kT2Out;
+    const long long total = (long long)nbands * g.lx;
+    const int grid = (int)std::min<long long>(nsm, total);
+    const long long per_cta = (total + grid - 1) / grid;
+    k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, nbands, per_cta, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace d2q37

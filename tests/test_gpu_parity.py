@@ -872,3 +872,86 @@ def test_p2p_missing_neighbour_reports_instead_of_hanging(gpu, lbm):
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "reported:" in r.stdout and "in time" in r.stdout, r.stdout
+
+
+# --------------------------------------------------------------------------- two steps per sweep (FUSED2)
+
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+@pytest.mark.parametrize("lx,ly", [(64, 128), (37, 300), (130, 245), (5, 7), (1, 16), (9, 3), (300, 123)])
+def test_fused2_bitwise_equals_fused(gpu, lbm, bc, lx, ly):
+    """Temporal blocking (two steps per HBM sweep, csrc/d2q37_step2.cu) is bit-identical to single
+    fused steps: band edges (ly = 2*122 + 1 leaves a 1-row last band), degenerate extents (lx = 1,
+    ly = 3), odd step counts (the last step runs FUSED) and both y faces."""
+    init = lbm.make_lattice("random", lx, ly, seed=17)
+    want = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused")
+    want.load(init)
+    got = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused2")
+    got.load(init)
+    for n in (2, 1, 4, 3):
+        want.step(1.3, n)
+        got.step(1.3, n)
+        assert np.array_equal(got.dump(), want.dump()), n
+    assert got.time_step == want.time_step == 10
+
+
+def test_fused2_vs_oracle_wall_rt(gpu, lbm, po):
+    """FUSED2 on the config-0 recipe (RT init, walls, omega 0.8): within 1e-12 of the oracle after 2 steps."""
+    lx, ly = 256, 1024
+    init = lbm.make_lattice("rt", lx, ly, seed=12345)
+    s = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    s.load(init)
+    s.step(0.8, 2)
+    want, bad = po.orc_step(init, 0.8, 2, po.BC_WALL)
+    assert not bad
+    assert max_rel(s.dump(), want) <= 1e-12
+
+
+def test_fused2_other_layouts_fall_back_to_fused(gpu, lbm):
+    """FUSED2 covers SoA; on the other layouts (and in STRICT math) it runs fused steps: same bits."""
+    lx, ly = 24, 96
+    init = lbm.make_lattice("random", lx, ly, seed=5)
+    ref = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused")
+    ref.load(init)
+    ref.step(1.1, 4)
+    want = ref.dump()
+    for layout, vl in (("caosoa", 32), ("csoa", 8), ("aos", 1)):
+        s = sim_of(lbm, layout, lx, ly, vl, bc="wall", variant="fused2")
+        s.load(init)
+        s.step(1.1, 4)
+        assert np.array_equal(s.dump(), want), layout
+    st = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2", math="strict")
+    st.load(init)
+    st.step(1.1, 4)
+    sf = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused", math="strict")
+    sf.load(init)
+    sf.step(1.1, 4)
+    assert np.array_equal(st.dump(), sf.dump())
+
+
+def test_fused2_nonphysical_raises(gpu, lbm):
+    """NonPhysicalError (model.hpp:28-30) is raised from the two-step kernel too."""
+    lx, ly = 16, 32
+    bad = lbm.make_lattice("random", lx, ly, seed=3)
+    bad[:, 5, 7] = -1.0
+    s = sim_of(lbm, "soa", lx, ly, variant="fused2")
+    s.load(bad)
+    with pytest.raises(lbm.NonPhysicalError):
+        s.step(1.0, 2)
+
+
+@pytest.mark.slow
+def test_fused2_full_size_bitwise(gpu, lbm):
+    """The bench workload (4096 x 16384 RT, walls, omega 0.8): 4 steps as two FUSED2 sweeps are bit for
+    bit 4 single fused steps (CAoSoA32, the single-step bench layout)."""
+    lx, ly = 4096, 16384
+    s = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    s.init_rt_device(4242)
+    s.step(0.8, 4)
+    got = s.dump()
+    s.close()
+    r = sim_of(lbm, "caosoa", lx, ly, 32, bc="wall", variant="fused")
+    r.init_rt_device(4242)
+    r.step(0.8, 4)
+    want = r.dump()
+    r.close()
+    assert np.array_equal(got, want)
