@@ -4,7 +4,12 @@
 Workload (BASELINE configs 3/4): a 4096 x 16384 lattice per GPU (weak
 scaling; the global lattice is 4096 x 16384*N, split into y-slabs), config-0
 Rayleigh-Taylor-like init, periodic x, top/bottom specular walls, omega 0.8
-(SURVEY.md 0.5), one "step" = bc + fused propagate/collide on the CAoSoA (vl = 32) store.
+(SURVEY.md 0.5).  On one GPU the steps run as FUSED2 on the SoA store: every pair
+of steps is one kernel that reads the lattice once and writes it two steps
+later (temporal blocking, csrc/d2q37_step2.cu; bit-identical to two fused
+steps).  On N > 1 GPUs every step is the single-sweep fused pull+collide on the
+CAoSoA (vl = 32) y-slab store with the peer-memory halo push (the multi-GPU
+path, which FUSED2 does not cover).
 value = whole-job MLUPS over the K timed steps (max over ranks of the device
 time).  Inputs are larger than L2 (2 x 19.9 GB per GPU vs 126 MB), so no
 explicit flush is needed.
@@ -187,6 +192,19 @@ def cuda_events():
     return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
 
+def steps_per_call(variant: str) -> int:
+    """FUSED2 advances two steps per kernel: the timed loop calls step(omega, 2)."""
+    return 2 if variant == "fused2" else 1
+
+
+def time_stepping(sim, steps: int, variant: str) -> float:
+    """Device time (ms) of exactly `steps` time steps, issued as step(omega, 2) calls for FUSED2."""
+    spc = steps_per_call(variant)
+    calls = [spc] * (steps // spc) + ([steps % spc] if steps % spc else [])
+    it = iter(calls)
+    return time_steps(sim, len(calls), lambda: sim.step(OMEGA, next(it), sync=False))
+
+
 def time_steps(sim, steps: int, fn) -> float:
     """Device time (ms) of `steps` calls of fn on the lattice stream (CUDA events)."""
     import torch
@@ -277,7 +295,8 @@ def bench_config0(lbm, warmup: int) -> dict:
     lx, ly, n = 256, 1024, 100
     canon = lbm.make_lattice("rt", lx, ly, SEED)
     out = {}
-    for layout, vl, variant in (("caosoa", 32, "fused"), ("soa", 1, "fused"), ("soa", 1, "unfused")):
+    for layout, vl, variant in (("caosoa", 32, "fused"), ("soa", 1, "fused2"), ("soa", 1, "fused"),
+                                ("soa", 1, "unfused")):
         sim = lbm.Simulation(layout, lx, ly, vl, device=0, bc="wall", variant=variant)
         sim.load(canon)
         sim.step(OMEGA, warmup)
@@ -369,7 +388,7 @@ def bench_variant(lbm, ly, layout, vl, variant, warmup, steps, hbm_peak: float =
     sim.step(OMEGA, warmup)
     sim.set_profiling(True)
     sim.kernel_times()
-    ms = time_steps(sim, steps, lambda: sim.step(OMEGA, 1, sync=False))
+    ms = time_stepping(sim, steps, variant)
     kt = sim.kernel_times()
     sim.set_profiling(False)
     sim.close()
@@ -378,13 +397,17 @@ def bench_variant(lbm, ly, layout, vl, variant, warmup, steps, hbm_peak: float =
     for k, (tot, n) in kt.items():
         if n:
             kms = tot / n
+            upd = steps_per_call(variant) if k == "fused" else 1  # time steps per launch
             out[f"{k}_ms"] = kms
-            gbs = sites * BYTES_PER_SITE / (kms / 1e3) / 1e9
+            gbs = sites * BYTES_PER_SITE / (kms / 1e3) / 1e9  # one read + one write of the lattice per launch
             out[f"{k}_GBps"] = gbs
             if hbm_peak:
                 out[f"{k}_frac_of_hbm"] = gbs / hbm_peak
             if k in ("fused", "collide"):
-                out[f"{k}_frac_of_fp64_nominal"] = sites * FLOPS_PER_SITE / (kms / 1e3) / (FP64_NOMINAL_TFLOPS * 1e12)
+                out[f"{k}_frac_of_fp64_nominal"] = (upd * sites * FLOPS_PER_SITE / (kms / 1e3) /
+                                                    (FP64_NOMINAL_TFLOPS * 1e12))
+            if upd > 1:
+                out[f"{k}_steps_per_launch"] = upd
     return out
 
 
@@ -497,7 +520,7 @@ def run_b200(args, dist: Dist):
     sim.kernel_times()
     dist.barrier()
     torch.cuda.synchronize()
-    ms = time_steps(sim, args.steps, lambda: sim.step(OMEGA, 1, sync=False))
+    ms = time_stepping(sim, args.steps, args.variant)
     torch.cuda.synchronize()
     dist.barrier()
     kt = sim.kernel_times()
@@ -513,17 +536,31 @@ def run_b200(args, dist: Dist):
     fused_ms, fused_n = kt["fused"]
     dom = "fused" if fused_n else "collide"
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
+    # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
+    upd = steps_per_call(args.variant) if (n == 1 and dom == "fused") else 1
     achieved = sites_local * BYTES_PER_SITE / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     step_ms = ms_max / args.steps
-    roofline = {"bound": "hbm", "kernel": "k_collide<FAST,SHIFT> (fused pull-gather + collide)",
+    two = upd == 2
+    roofline = {"bound": "hbm",
+                "kernel": ("k_step2 (two fused pull+collide steps per HBM sweep, temporal blocking)" if two else
+                           "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak if achieved else None, "traffic": load_ncu_traffic(args.layout, ly_local),
+                "frac": achieved / hbm_peak if achieved else None,
+                "traffic": load_ncu_traffic(args.layout, ly_local, args.variant if n == 1 else "fused"),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
-                "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / step_ms,
+                "time_steps_per_launch": upd,
+                "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / (step_ms * upd),
                 "frac_of_nominal_hbm": achieved / HBM_NOMINAL_GBS if achieved else None,
                 "nominal_hbm_gbs": HBM_NOMINAL_GBS,
+                "fp64_tflops_reference_count": (upd * sites_local * FLOPS_PER_SITE / (dom_ms / 1e3) / 1e12
+                                                if dom_ms > 0 else None),
+                "frac_of_fp64_nominal": (upd * sites_local * FLOPS_PER_SITE / (dom_ms / 1e3) /
+                                         (FP64_NOMINAL_TFLOPS * 1e12) if dom_ms > 0 else None),
                 "edge_ms": kt["edge"][0] / max(1, kt["edge"][1])}
+    if two:
+        roofline["note"] = ("592 B/site per launch = per two time steps; the single-step bound at this "
+                            "peak is peak/592 B site-steps/s, the two-step bound peak/296 B")
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -554,7 +591,7 @@ def run_b200(args, dist: Dist):
         kernels["step_c0"] = bench_config0(lbm, 5)
         line["kernels"] = kernels
         variants = {}
-        for lay, vl, var in (("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"),
+        for lay, vl, var in (("soa", 1, "fused2"), ("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"),
                              ("csoa", 32, "unfused"), ("aos", 1, "fused"), ("caosoa", 32, "fused"),
                              ("caosoa", 32, "unfused")):
             if (lay, var) == (args.layout, args.variant):
@@ -562,17 +599,17 @@ def run_b200(args, dist: Dist):
             variants[f"{lay}{vl if vl > 1 else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20,
                                                                             hbm_peak)
         line["variants_c3"] = variants
+        # the multi-GPU schedules, on the layout the N > 1 runs use (CAoSoA vl 32)
         try:
             line["slab_schedule"] = {
-                "strong_8gpu_slab": bench_slab_schedule(lbm, args.layout, args.vl, 4096, 3, 50),
-                "weak_slab": bench_slab_schedule(lbm, args.layout, args.vl, LY_PER_GPU, 3, 20)}
+                "strong_8gpu_slab": bench_slab_schedule(lbm, "caosoa", 32, 4096, 3, 50),
+                "weak_slab": bench_slab_schedule(lbm, "caosoa", 32, LY_PER_GPU, 3, 20)}
         except Exception as e:  # NCCL unavailable must not sink the line
             line["slab_schedule"] = {"error": str(e)}
-        if args.layout in ("aos", "caosoa"):
-            try:
-                line["p2p_ring_emulation"] = bench_p2p_ring_emulation(lbm, args.layout, args.vl, 8, 3, 20)
-            except Exception as e:  # noqa: BLE001
-                line["p2p_ring_emulation"] = {"error": str(e)}
+        try:
+            line["p2p_ring_emulation"] = bench_p2p_ring_emulation(lbm, "caosoa", 32, 8, 3, 20)
+        except Exception as e:  # noqa: BLE001
+            line["p2p_ring_emulation"] = {"error": str(e)}
     if n == 1 and not args.no_cpu:
         try:
             v, med, workers = reference_step_rate()
@@ -620,13 +657,15 @@ def run_e2e(lbm, sim, args, dist: Dist):
             "d2h_bytes_per_step": need / nsteps, "steps_per_call": nsteps,
             "h2d_bytes_per_call": need, "d2h_bytes_per_call": need, "pinned": pinned,
             "seconds_per_call": t,
-            "call": "Simulation.load(host canonical) + step(0.8, n, fused, wall) + dump(host canonical)"}
+            "call": f"Simulation.load(host canonical) + step(0.8, n, {sim.variant}, wall) + dump(host canonical)"}
 
 
-def load_ncu_traffic(layout: str, ly: int):
-    """DRAM bytes/launch of the fused kernel from the committed ncu capture (profiles/), else None."""
+def load_ncu_traffic(layout: str, ly: int, variant: str = "fused"):
+    """DRAM bytes/launch of the step kernel from the committed ncu capture (profiles/), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
     key = {"csoa": "prof_fused_csoa", "caosoa": "prof_fused_caosoa"}.get(layout, "prof_fused")
+    if variant == "fused2" and layout == "soa":
+        key = "prof_step2_soa"
     try:
         with open(path) as f:
             rec = json.load(f)[key]
@@ -642,9 +681,11 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--layout", choices=["aos", "soa", "csoa", "caosoa"], default="caosoa")
-    ap.add_argument("--vl", type=int, default=32)
-    ap.add_argument("--variant", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--layout", choices=["aos", "soa", "csoa", "caosoa"], default=None,
+                    help="default: soa (1 GPU, FUSED2), caosoa vl 32 (N > 1)")
+    ap.add_argument("--vl", type=int, default=None)
+    ap.add_argument("--variant", choices=["fused", "unfused", "fused2"], default=None,
+                    help="default: fused2 (1 GPU: two steps per sweep), fused (N > 1)")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU (weak scaling)")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 halo transport: peer-memory push from the step kernel, or NCCL")
@@ -657,6 +698,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: at least 3 warm-up steps
+    multi = int(os.environ.get("WORLD_SIZE", "1")) > 1
+    if args.layout is None:
+        args.layout = "caosoa" if multi else "soa"
+    if args.vl is None:
+        args.vl = 32 if args.layout in ("csoa", "caosoa") else 1
+    if args.variant is None:
+        args.variant = "fused" if multi else "fused2"
     if args.impl == "reference":
         # rank 0 alone runs the CPU reference; other ranks exit 0 without work
         if int(os.environ.get("RANK", "0")) == 0:
