@@ -463,7 +463,7 @@ def make_slab(lbm, args, dist: Dist, dev: int, ly_global: int):
     """This rank's slab: the peer-memory P2P transport (falls back to NCCL if the ranks cannot map
     each other's memory), or NCCL when asked."""
     rank, n = dist.rank, dist.world
-    if args.transport == "p2p":
+    if args.transport == "p2p" and args.variant != "fused2":  # FUSED2 slabs exchange 6-row halos over NCCL
         sim, blob = None, b""
         try:
             sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
@@ -527,6 +527,8 @@ def run_b200(args, dist: Dist):
     sim.set_profiling(False)
     clk = clocks.stop()
     halo_ms = dist.max(sim.exposed_halo_ms()) if n > 1 else 0.0  # the slowest rank's exposed halo
+    if n > 1 and args.variant == "fused2":
+        halo_ms /= 2  # one 6-row exchange per two-step sweep
     ms_max = dist.max(ms)
     value = n * sites_local * args.steps / (ms_max / 1e3) / 1e6
     launches = sum(c for _, c in kt.values())
@@ -537,7 +539,7 @@ def run_b200(args, dist: Dist):
     dom = "fused" if fused_n else "collide"
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
-    upd = steps_per_call(args.variant) if (n == 1 and dom == "fused") else 1
+    upd = steps_per_call(args.variant) if dom == "fused" else 1
     achieved = sites_local * BYTES_PER_SITE / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     step_ms = ms_max / args.steps
     two = upd == 2
@@ -546,7 +548,7 @@ def run_b200(args, dist: Dist):
                            "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak if achieved else None,
-                "traffic": load_ncu_traffic(args.layout, ly_local, args.variant if n == 1 else "fused"),
+                "traffic": load_ncu_traffic(args.layout, ly_local, args.variant),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
                 "time_steps_per_launch": upd,

@@ -71,6 +71,8 @@ struct d2q37_lattice {
     double* send_hi = nullptr;
     double* recv_lo = nullptr;
     double* recv_hi = nullptr;
+    // FUSED2 slab halos: 6 rows x 37 populations per face, [send lo, send hi, recv lo, recv hi]
+    double* h6[4] = {nullptr, nullptr, nullptr, nullptr};
     void* comm = nullptr;
     cudaStream_t comm_stream = nullptr;
     // NCCL slabs: pack / unpack / boundary sites run on a high-priority stream
@@ -179,7 +181,11 @@ int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
     // a 32-double boundary.
     g->rstride = site_major(layout) ? (long long)kNpop * vl : vl;
     const int per = int(32 / std::gcd(g->rstride, 32LL));
-    g->pitch = (g->sy + per - 1) / per * per;
+    // SoA: room for 3 more ghost rows on each side of a column (rows j = -3..-1
+    // sit in the previous column's unused tail): the 6-row halos of two-step
+    // (FUSED2) slab sweeps; the reference's 3-row ghost rows are unchanged.
+    g->deep = layout == D2Q37_SOA ? 1 : 0;
+    g->pitch = (g->sy + (g->deep ? 2 * kHalo : 0) + per - 1) / per * per;
     g->cstride = (long long)g->pitch * g->rstride;
     g->lead = (32 - (kHalo * g->rstride) % 32) % 32;
     g->pstride = site_major(layout) ? vl : (g->px * g->cstride + 31) / 32 * 32;
@@ -322,7 +328,7 @@ void free_lattice(d2q37_lattice* h) {
     if (h->halo_stream) cudaStreamSynchronize(h->halo_stream);
     if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
     for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->stage2, h->send_lo, h->send_hi, h->recv_lo,
-                      h->recv_hi})
+                      h->recv_hi, h->h6[0], h->h6[1], h->h6[2], h->h6[3]})
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     for (cudaEvent_t e : h->ev_io)
@@ -591,6 +597,64 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
     CK(launch_step2(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, h->d_flag, h->stream));
     h->cur = 1 - h->cur;
     h->time_step += 2;
+    return D2Q37_OK;
+}
+
+int ensure_halo6(d2q37_lattice* h) {
+    if (h->h6[0]) return D2Q37_OK;
+    DeviceGuard dg(h->device);
+    const size_t bytes = halo6_count(h->g) * sizeof(double);
+    for (double*& p : h->h6) {
+        CK(cudaMalloc(&p, bytes));
+        CK(cudaMemset(p, 0, bytes));
+    }
+    return D2Q37_OK;
+}
+
+// FUSED2 on a y-slab: 6-row halos of the current state (pack, NCCL to / from
+// both neighbours, unpack into the deep ghost rows), then one two-step sweep
+// reading them.  Everything on the lattice stream; the exchange is ~7 MB per
+// face per two steps, tens of microseconds against a ~10 ms sweep.
+int step2_slab_exchange_nccl(d2q37_lattice* h, int bc) {
+    RET(ensure_halo6(h));
+    const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+    CK(cudaEventRecord(h->ev_int[h->ev_count % kEventRing], h->stream));
+    {
+        ProfScope ps(h, kProfPack);
+        CK(launch_pack6(h->buf[h->cur], h->g, h->h6[0], h->h6[1], h->stream));
+        std::string why;
+        const int rc = nccl_exchange(h->comm, h->stream, h->h6[0], h->h6[2], lo, h->h6[1], h->h6[3], hi,
+                                     halo6_count(h->g), &why);
+        if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+    }
+    {
+        ProfScope ps(h, kProfEdge);
+        CK(launch_unpack6(h->buf[h->cur], h->g, lo >= 0 ? h->h6[2] : nullptr, hi >= 0 ? h->h6[3] : nullptr,
+                          h->stream));
+    }
+    CK(cudaEventRecord(h->ev_wait[h->ev_count % kEventRing], h->stream));
+    ++h->ev_count;
+    return D2Q37_OK;
+}
+
+int step2_group_exchange(std::vector<d2q37_lattice*>& slabs, int bc) {
+    for (d2q37_lattice* h : slabs) {
+        RET(ensure_halo6(h));
+        ProfScope ps(h, kProfPack);
+        CK(launch_pack6(h->buf[h->cur], h->g, h->h6[0], h->h6[1], h->stream));
+    }
+    for (d2q37_lattice* h : slabs) {
+        const size_t bytes = halo6_count(h->g) * sizeof(double);
+        const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+        if (lo >= 0) CK(cudaMemcpyAsync(h->h6[2], slabs[lo]->h6[1], bytes, cudaMemcpyDeviceToDevice, h->stream));
+        if (hi >= 0) CK(cudaMemcpyAsync(h->h6[3], slabs[hi]->h6[0], bytes, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    for (d2q37_lattice* h : slabs) {
+        const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+        ProfScope ps(h, kProfEdge);
+        CK(launch_unpack6(h->buf[h->cur], h->g, lo >= 0 ? h->h6[2] : nullptr, hi >= 0 ? h->h6[3] : nullptr,
+                          h->stream));
+    }
     return D2Q37_OK;
 }
 
@@ -1258,15 +1322,22 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
     DeviceGuard dg(h->device);
     if (h->transport == kTransportGroup) {
         d2q37_lattice** slabs = h->group.data();
-        if (variant == D2Q37_FUSED2) variant = D2Q37_FUSED;
         return d2q37_group_step(slabs, int(h->group.size()), omega, nsteps, variant, bc);
     }
     const bool slab = !local_only(h) && remote_faces(h, bc);
     int s = 0;
     if (variant == D2Q37_FUSED2) {
         const Faces fc = step_faces(h, bc);
-        if (!slab && h->math == D2Q37_MATH_FAST && step2_supported(h->g, fc))
-            for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
+        if (h->math == D2Q37_MATH_FAST && step2_supported(h->g, fc)) {
+            if (!slab) {
+                for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
+            } else if (h->transport == kTransportNccl) {
+                for (; s + 2 <= nsteps; s += 2) {
+                    RET(step2_slab_exchange_nccl(h, bc));
+                    RET(step2_local(h, omega, fc));
+                }
+            }
+        }
         variant = D2Q37_FUSED;  // the odd last step, and every layout / case k_step2 does not cover
     }
     if (!slab && !h->prof_on && nsteps >= kGraphSteps) {
@@ -1820,9 +1891,23 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
         RET(check_handle(h));
         RET(validate_bc(h, bc));
     }
-    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
     DeviceGuard dg(slabs[0]->device);
-    for (int s = 0; s < nsteps; ++s) {
+    int s = 0;
+    if (variant == D2Q37_FUSED2) {
+        bool ok = true;
+        for (d2q37_lattice* h : slabs) ok = ok && h->math == D2Q37_MATH_FAST && step2_supported(h->g, step_faces(h, bc));
+        if (ok) {
+            const bool remote = nslabs > 1 && remote_faces(slabs[0], bc);
+            for (; s + 2 <= nsteps; s += 2) {
+                if (remote) RET(step2_group_exchange(slabs, bc));
+                for (d2q37_lattice* h : slabs) RET(step2_local(h, omega, step_faces(h, bc)));
+            }
+        }
+        variant = D2Q37_FUSED;
+    }
+    for (; s < nsteps; ++s) {
         if (nslabs == 1 || !remote_faces(slabs[0], bc)) {
             for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
             continue;

@@ -32,7 +32,7 @@ struct DevGeo {
     int px;         // lx + 6
     int lvl;        // log2(vl)
     int tr;         // 1: y-major storage (storage column = lattice y, storage row = lattice x)
-    int pad_;
+    int deep;       // 1: x-major SoA with 6 ghost rows per side (j = -3 .. strip+8; FUSED2 slab halos)
     long long lead;     // element offset of (p, X, j, k) = (0, 0, 0, 0)
     long long pstride;  // between populations of one site: plane (SoA/CSoA) or vl (AoS/CAoSoA)
     long long rstride;  // between padded rows j of a lane: vl (SoA/CSoA) or 37*vl (AoS/CAoSoA)

@@ -118,6 +118,12 @@ cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int l
 bool step2_supported(const DevGeo& g, const Faces& fc);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                          double omega, int* flag, cudaStream_t s);
+// FUSED2 slab halos (deep SoA geometry): 6 rows per face and population,
+// buffers of halo6_count(g) doubles laid out [p][x][6].
+size_t halo6_count(const DevGeo& g);
+cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s);
+cudaError_t launch_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
+                           cudaStream_t s);
 cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
 
 }  // namespace d2q37

@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     const int tid = threadIdx.x & (kT2Band - 1);
     const int lx = g.lx, ly = g.ly;
     const bool wall_lo = fc.lo == kFaceWall, wall_hi = fc.hi == kFaceWall;
+    // ghost faces (y-slabs): rows -6..-1 / ly..ly+5 hold the neighbours' rows (k_unpack6)
+    const bool ghost_lo = fc.lo == kFaceGhost, ghost_hi = fc.hi == kFaceGhost;
     // element of (p = 0, x = 0, y = 0); site (x, y) of population p at + p*plane + x*cs + y
     const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
@@ -106,6 +108,10 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                 y1 = yr;
             else if ((yr < 0 && wall_lo) || (yr >= ly && wall_hi))
                 y1 = min(max(yr, 0), ly - 1);
+            else if (yr < 0 && ghost_lo)
+                y1 = yr;  // >= -3: its pulls reach row -6
+            else if (yr >= ly && ghost_hi)
+                y1 = min(yr, ly + kHalo - 1);  // rows past ly + 2 are never read
             else
                 y1 = wrap_mod(yr, ly);
             // pull row of y1 - cy (k = cy + 3) and whether it is a wall image
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                 const bool m = (ys < 0 && wall_lo) || (ys >= ly && wall_hi);
                 if (m)
                     ys = ys < 0 ? -1 - ys : 2 * ly - 1 - ys;
-                else
+                else if (!((ys < 0 && ghost_lo) || (ys >= ly && ghost_hi)))
                     ys = wrap_mod(ys, ly);
                 mirm |= unsigned(m) << k;
                 yo[k] = ys;
@@ -198,8 +204,53 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     if (bad) atomicOr(flag, 1);
 }
 
+// 6-row slab halos of FUSED2: rows 0..5 / ly-6..ly-1 of every physical column
+// and population -> send buffers [p][x][6]; received buffers -> ghost rows
+// -6..-1 / ly..ly+5 (a null buffer skips that face).
+__global__ void __launch_bounds__(256) k_pack6(const double* __restrict__ buf, DevGeo g, double* __restrict__ send_lo,
+                                               double* __restrict__ send_hi) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = int(i % (2 * kHalo));
+    const long long px = i / (2 * kHalo);
+    const int x = int(px % g.lx), p = int(px / g.lx);
+    const long long base = elem_of(g, p, x + kHalo, kHalo, 0);  // row y = 0
+    if (send_lo) send_lo[i] = buf[base + r];
+    if (send_hi) send_hi[i] = buf[base + g.ly - 2 * kHalo + r];
+}
+
+__global__ void __launch_bounds__(256) k_unpack6(double* __restrict__ buf, DevGeo g, const double* __restrict__ recv_lo,
+                                                 const double* __restrict__ recv_hi) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = int(i % (2 * kHalo));
+    const long long px = i / (2 * kHalo);
+    const int x = int(px % g.lx), p = int(px / g.lx);
+    const long long base = elem_of(g, p, x + kHalo, kHalo, 0);  // row y = 0
+    if (recv_lo) buf[base - 2 * kHalo + r] = recv_lo[i];  // rows -6 .. -1
+    if (recv_hi) buf[base + g.ly + r] = recv_hi[i];       // rows ly .. ly+5
+}
+
+size_t halo6_count(const DevGeo& g) { return size_t(kNpop) * g.lx * 2 * kHalo; }
+
+cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s) {
+    const long long n = (long long)halo6_count(g);
+    k_pack6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g, send_lo, send_hi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
+                           cudaStream_t s) {
+    const long long n = (long long)halo6_count(g);
+    k_unpack6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g, recv_lo, recv_hi);
+    return cudaGetLastError();
+}
+
 bool step2_supported(const DevGeo& g, const Faces& fc) {
-    const bool face_ok = (fc.lo == kFacePeriodic || fc.lo == kFaceWall) && (fc.hi == kFacePeriodic || fc.hi == kFaceWall);
+    auto ok = [&](int f) { return f == kFacePeriodic || f == kFaceWall || (f == kFaceGhost && g.deep); };
+    const bool face_ok = ok(fc.lo) && ok(fc.hi) && (fc.lo != kFaceGhost && fc.hi != kFaceGhost ? true : g.ly >= 2 * kHalo);
     return g.vl == 1 && !g.tr && g.pstride != g.vl && face_ok && fc.col_lo == kFacePeriodic &&
            fc.col_hi == kFacePeriodic && g.lx >= 1 && g.ly >= kHalo &&
            (long long)(g.lx + 2 * kHalo) * g.cstride < 0x7fffffffLL;  // 32-bit offsets inside a plane

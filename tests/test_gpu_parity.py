@@ -955,3 +955,62 @@ def test_fused2_full_size_bitwise(gpu, lbm):
     want = r.dump()
     r.close()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("nslabs", [2, 4])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+@pytest.mark.parametrize("lx,ly", [(32, 256), (7, 48), (130, 600)])
+def test_fused2_slab_group_bitwise_equals_single_domain(gpu, lbm, nslabs, bc, lx, ly):
+    """FUSED2 on y-slabs (6-row halos of 37 populations per face and two steps, deep ghost rows of the
+    SoA store) is bit for bit the single domain: 2 and 4 slabs on one GPU, periodic and wall, slabs
+    of 12 rows (the 6-row halo minimum) to multi-band slabs, odd step counts."""
+    init = lbm.make_lattice("random", lx, ly, seed=41)
+    ref = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused")
+    ref.load(init)
+    grp = lbm.SlabGroup("soa", lx, ly, 1, nslabs, bc=bc, variant="fused2")
+    grp.load(init)
+    for n in (2, 3, 4):
+        ref.step(1.1, n)
+        grp.step(1.1, n)
+        assert np.array_equal(grp.dump(), ref.dump()), n
+
+
+def test_fused2_slab_ghost_rows_are_the_only_remote_reads(gpu, lbm):
+    """NaN-poisoned deep ghost rows are overwritten by the 6-row exchange before every FUSED2 sweep:
+    poisoning them between sweeps changes nothing."""
+    lx, ly = 16, 96
+    init = lbm.make_lattice("random", lx, ly, seed=43)
+    ref = sim_of(lbm, "soa", lx, ly, bc="periodic", variant="fused")
+    ref.load(init)
+    ref.step(1.1, 4)
+    grp = lbm.SlabGroup("soa", lx, ly, 1, 2, bc="periodic", variant="fused2")
+    grp.load(init)
+    grp.step(1.1, 2)
+    for s in grp.slabs:  # standard 3-row ghosts (the deep rows are not in the reference's padded order)
+        pad = s.read_padded()
+        lyl = ly // 2
+        pad_nan = pad.copy().reshape(37, lx + 6, lyl + 6)
+        pad_nan[:, :, :3] = np.nan
+        pad_nan[:, :, lyl + 3:] = np.nan
+        s.write_padded(pad_nan.reshape(pad.shape))
+    grp.step(1.1, 2)
+    assert np.array_equal(grp.dump(), ref.dump())
+
+
+@pytest.mark.parametrize("bc", ["periodic"])
+def test_fused2_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, bc):
+    """FUSED2 through the real NCCL transport: a 1-rank ring whose 6-row halos go through
+    ncclSend/ncclRecv to self before every two-step sweep."""
+    import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library binds to)
+
+    lx, ly = 32, 256
+    init = lbm.make_lattice("random", lx, ly, seed=47)
+    ref = sim_of(lbm, "soa", lx, ly, variant="fused")
+    ref.load(init)
+    ref.step(1.2, 7)
+    s = lbm.Simulation.slab("soa", lx, ly, 1, rank=0, nranks=1, nccl_id=lbm.nccl_unique_id(), bc=bc,
+                            variant="fused2")
+    s.load(init)
+    s.step(1.2, 7)
+    assert np.array_equal(s.dump(), ref.dump())
+    assert s.exposed_halo_ms() > 0.0
