@@ -4,12 +4,14 @@
 Workload (BASELINE configs 3/4): a 4096 x 16384 lattice per GPU (weak
 scaling; the global lattice is 4096 x 16384*N, split into y-slabs), config-0
 Rayleigh-Taylor-like init, periodic x, top/bottom specular walls, omega 0.8
-(SURVEY.md 0.5).  On one GPU the steps run as FUSED2 on the SoA store: every pair
-of steps is one kernel that reads the lattice once and writes it two steps
-later (temporal blocking, csrc/d2q37_step2.cu; bit-identical to two fused
-steps).  On N > 1 GPUs every step is the single-sweep fused pull+collide on the
-CAoSoA (vl = 32) y-slab store with the peer-memory halo push (the multi-GPU
-path, which FUSED2 does not cover).
+(SURVEY.md 0.5).  The steps run as FUSED2 on the SoA store: every pair of
+steps is one kernel that reads the lattice once and writes it two steps later
+(temporal blocking, csrc/d2q37_step2.cu; bit-identical to two fused steps).
+On N > 1 GPUs each rank owns a y-slab; before every two-step sweep the 6-row x
+37-population halos of both faces go to the neighbours through NCCL
+send/recv (pack, exchange, unpack into the deep ghost rows).
+``--variant fused --layout caosoa`` selects the single-step kernel with the
+peer-memory halo push instead.
 value = whole-job MLUPS over the K timed steps (max over ranks of the device
 time).  Inputs are larger than L2 (2 x 19.9 GB per GPU vs 126 MB), so no
 explicit flush is needed.
@@ -347,6 +349,30 @@ def bench_slab_schedule(lbm, layout, vl, ly, warmup, steps) -> dict:
     return out
 
 
+def bench_slab_schedule_fused2(lbm, ly, warmup, steps) -> dict:
+    """The FUSED2 y-slab schedule on one GPU: a 1-rank NCCL ring (6-row halos of both faces through
+    ncclSend/Recv to self before every two-step sweep) vs the single domain, same lattice."""
+    import torch  # noqa: F401  (NCCL comes from torch's libnccl.so.2)
+    out = {}
+    for name in ("single_domain", "nccl_self_ring"):
+        if name == "single_domain":
+            sim = lbm.Simulation("soa", LX, ly, 1, device=0, bc="periodic", variant="fused2")
+        else:
+            sim = lbm.Simulation.slab("soa", LX, ly, 1, device=0, rank=0, nranks=1, nccl_id=lbm.nccl_unique_id(),
+                                      bc="periodic", variant="fused2")
+        sim.init_rt_device(SEED)
+        sim.step(OMEGA, warmup)
+        ms = time_stepping(sim, steps, "fused2")
+        out[name] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6}
+        if name != "single_domain":
+            out[name]["exposed_halo_ms_per_step"] = sim.exposed_halo_ms() / 2
+        sim.close()
+    out["schedule_overhead"] = out["nccl_self_ring"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
+    out["config"] = (f"{LX}x{ly} soa FUSED2, periodic y through 6-row NCCL halos to self vs local wrap, "
+                     f"{steps} steps")
+    return out
+
+
 def bench_p2p_ring_emulation(lbm, layout, vl, nslabs, warmup, steps) -> dict:
     """BASELINE config 4 strong (4096 x 32768) as `nslabs` P2P slabs on ONE GPU, stepped in
     lockstep through the real peer-memory protocol (counters, remote stores, separate streams),
@@ -601,7 +627,13 @@ def run_b200(args, dist: Dist):
             variants[f"{lay}{vl if vl > 1 else ''}-{var}"] = bench_variant(lbm, ly_local, lay, vl, var, 3, 20,
                                                                             hbm_peak)
         line["variants_c3"] = variants
-        # the multi-GPU schedules, on the layout the N > 1 runs use (CAoSoA vl 32)
+        try:
+            line["slab_schedule_fused2"] = {
+                "strong_8gpu_slab": bench_slab_schedule_fused2(lbm, 4096, 4, 40),
+                "weak_slab": bench_slab_schedule_fused2(lbm, LY_PER_GPU, 4, 20)}
+        except Exception as e:  # noqa: BLE001
+            line["slab_schedule_fused2"] = {"error": str(e)}
+        # the single-step multi-GPU schedules (CAoSoA vl 32: NCCL columns / peer-memory push)
         try:
             line["slab_schedule"] = {
                 "strong_8gpu_slab": bench_slab_schedule(lbm, "caosoa", 32, 4096, 3, 50),
@@ -684,10 +716,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--layout", choices=["aos", "soa", "csoa", "caosoa"], default=None,
-                    help="default: soa (1 GPU, FUSED2), caosoa vl 32 (N > 1)")
+                    help="default: soa (the FUSED2 store)")
     ap.add_argument("--vl", type=int, default=None)
     ap.add_argument("--variant", choices=["fused", "unfused", "fused2"], default=None,
-                    help="default: fused2 (1 GPU: two steps per sweep), fused (N > 1)")
+                    help="default: fused2 (two steps per HBM sweep)")
     ap.add_argument("--ly", type=int, default=LY_PER_GPU, help="rows per GPU (weak scaling)")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N>1 halo transport: peer-memory push from the step kernel, or NCCL")
@@ -702,11 +734,12 @@ def main():
     args.warmup = max(3, args.warmup)  # timing rule: at least 3 warm-up steps
     multi = int(os.environ.get("WORLD_SIZE", "1")) > 1
     if args.layout is None:
-        args.layout = "caosoa" if multi else "soa"
+        args.layout = "soa"
     if args.vl is None:
         args.vl = 32 if args.layout in ("csoa", "caosoa") else 1
     if args.variant is None:
-        args.variant = "fused" if multi else "fused2"
+        args.variant = "fused2"
+    del multi
     if args.impl == "reference":
         # rank 0 alone runs the CPU reference; other ranks exit 0 without work
         if int(os.environ.get("RANK", "0")) == 0:

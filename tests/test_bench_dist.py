@@ -53,7 +53,7 @@ class _FakeLbm:
         return S
 
 
-def _worker(rank, world, port, fail_rank, q):
+def _worker(rank, world, port, fail_rank, q, variant="fused"):
     sys.path.insert(0, ROOT)
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
                       MASTER_PORT=str(port), BENCH_DIST_BACKEND="gloo")
@@ -63,7 +63,8 @@ def _worker(rank, world, port, fail_rank, q):
 
     d = bench.Dist()
     try:
-        args = argparse.Namespace(transport="p2p", layout="caosoa", vl=32, variant="fused")
+        layout, vl = ("soa", 1) if variant == "fused2" else ("caosoa", 32)
+        args = argparse.Namespace(transport="p2p", layout=layout, vl=vl, variant=variant)
         sim, transport = bench.make_slab(_FakeLbm(fail_rank), args, d, 0, 4096)
         q.put((rank, transport, sim.transport, sim.connected))
     finally:
@@ -88,3 +89,19 @@ def test_make_slab_transport_choice_is_collective(fail_rank):
     else:
         assert [got[r][0] for r in (0, 1)] == ["nccl", "nccl"]
         assert [got[r][1] for r in (0, 1)] == ["nccl", "nccl"]
+
+
+def test_make_slab_fused2_uses_nccl_on_every_rank():
+    """FUSED2 slabs exchange 6-row halos through NCCL: no rank tries the peer-memory transport."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, -1, q, "fused2")) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [got[r][0] for r in (0, 1)] == ["nccl", "nccl"]
+    assert [got[r][1] for r in (0, 1)] == ["nccl", "nccl"]

@@ -222,3 +222,80 @@ def test_slab_decomposition_bitwise(nranks, bc, po):
                             po.BC_WALL if bc == "wall" else po.BC_PERIODIC)
     assert not bad
     assert np.array_equal(result, want)
+
+
+# --------------------------------------------------------------------------- FUSED2: 6-row halos per two steps
+
+def _two_step_slab(rank, nranks, slab, omega, lbm, po):
+    """One FUSED2 sweep of a periodic y-slab: rows 0..5 / n-6..n-1 of all 37 populations go to the
+    lo / hi neighbour (k_pack6 -> NCCL -> k_unpack6 order), step 1 runs on rows -3 .. n+2 of the
+    extended slab (pulls reach rows -6 .. n+5), step 2 on rows 0 .. n-1 from step 1's rows."""
+    import torch
+
+    m = po.orc_model()
+    lo_peer, hi_peer = lbm.slab_neighbors(rank, nranks, "periodic")
+    npop, lx, n = slab.shape
+    h = 6
+    send_lo = np.ascontiguousarray(slab[:, :, :h])
+    send_hi = np.ascontiguousarray(slab[:, :, n - h:])
+    recv_lo, recv_hi = np.full_like(send_hi, np.nan), np.full_like(send_lo, np.nan)
+    t_rlo, t_rhi = torch.from_numpy(recv_lo), torch.from_numpy(recv_hi)
+    reqs = [dist.isend(torch.from_numpy(send_hi), hi_peer, tag=1), dist.irecv(t_rlo, lo_peer, tag=1),
+            dist.isend(torch.from_numpy(send_lo), lo_peer, tag=2), dist.irecv(t_rhi, hi_peer, tag=2)]
+    for r in reqs:
+        r.wait()
+    ext = np.concatenate([recv_lo, slab, recv_hi], axis=2)  # rows -6 .. n+5
+
+    def step(src, first, count):  # pull rows first .. first+count-1 of src (row 0 of src = y -6 or -3), collide
+        out = np.empty((npop, lx, count))
+        for p in range(npop):
+            cx, cy = int(m.cx[p]), int(m.cy[p])
+            out[p] = np.roll(src[p], cx, axis=0)[:, first - cy:first - cy + count]
+        assert not np.isnan(out).any(), "a row outside the 6-row halo was read"
+        new, bad = po.orc_collide(np.ascontiguousarray(out), omega, nthreads=1)
+        assert not bad
+        return new
+
+    s1 = step(ext, 3, n + 6)  # y -3 .. n+2 (ext row index = y + 6)
+    return step(s1, 3, n)  # y 0 .. n-1 (s1 row index = y + 3)
+
+
+def _two_step_worker(rank, nranks, port, sweeps, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import paper_1804_01918_b200 as lbm
+    from oracle import pyoracle as po
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=nranks)
+    try:
+        lx, ly = 8, 12 * nranks
+        glob = po.orc_lattice("random", lx, ly, seed=406)
+        n = ly // nranks
+        slab = np.ascontiguousarray(glob[:, :, rank * n:(rank + 1) * n])
+        for _ in range(sweeps):
+            slab = _two_step_slab(rank, nranks, slab, 0.9, lbm, po)
+        result_q.put((rank, slab))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_fused2_six_row_halo_schedule_bitwise(nranks, po):
+    """The FUSED2 slab plan over real process boundaries: 6 rows x 37 populations per face per two
+    steps are all a slab needs (unsent rows are NaN); 2 sweeps == 4 single-domain oracle steps."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_step_worker, args=(r, nranks, port, 2, q)) for r in range(nranks)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(nranks))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    result = np.concatenate([got[r] for r in range(nranks)], axis=2)
+    want, bad = po.orc_step(po.orc_lattice("random", 8, 12 * nranks, seed=406), 0.9, 4, po.BC_PERIODIC)
+    assert not bad
+    assert np.array_equal(result, want)
