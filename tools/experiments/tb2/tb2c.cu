@@ -176,7 +176,11 @@ __device__ __forceinline__ void producer(const double* __restrict__ in, double* 
     auto body = [&](double(&f)[kNpop], double(&fn)[kNpop], int t) {
         if (t < niter - 1) {
             const int r = xs - 3 + t;
+#ifdef NOPF
+            load(f, r);
+#else
             if (t < niter - 2) load(fn, r + 1);
+#endif
             const Part mine = half_sums<H>(f);
             double* xs_ = xch + H * 4 * NB + tid;
             xs_[0] = mine.rho;
@@ -214,6 +218,10 @@ __device__ __forceinline__ void producer(const double* __restrict__ in, double* 
         __syncthreads();
     };
     double fa[kNpop], fb[kNpop];
+#ifdef NOPF
+#pragma unroll 1
+    for (int t = 0; t < niter; ++t) body(fa, fb, t);
+#else
     load(fa, xs - 3);
     int t = 0;
 #pragma unroll 1
@@ -222,6 +230,7 @@ __device__ __forceinline__ void producer(const double* __restrict__ in, double* 
         body(fb, fa, t + 1);
     }
     if (t < niter) body(fa, fb, t);
+#endif
 }
 
 template <int NB>
