@@ -259,7 +259,9 @@ int d2q37_multi_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps
 int d2q37_set_profiling(d2q37_lattice* h, int on);
 int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
 /* Average device time (ms) of the last step's halo phase that was not hidden
- * behind interior compute (0 for single-domain lattices); see DESIGN.md. */
+ * behind interior compute (0 for single-domain lattices; one entry per
+ * two-step sweep for FUSED2 slabs); see DESIGN.md.  d2q37_set_profiling(h, 1)
+ * restarts the averaging window. */
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
 #ifdef __cplusplus

@@ -1928,6 +1928,11 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
 int d2q37_set_profiling(d2q37_lattice* h, int on) {
     RET(check_handle(h));
     h->prof_on = on != 0;
+    if (h->prof_on) {  // a new measurement window: the exposed-halo ring restarts too (no warm-up exchanges)
+        DeviceGuard dg(h->device);
+        CK(cudaStreamSynchronize(h->stream));
+        h->ev_count = 0;
+    }
     return D2Q37_OK;
 }
 
