@@ -20,6 +20,8 @@
 //       layouts preserves every physical site                           (validation.cpp, layout.cpp:105-116)
 //   G9  a 4-slab MultiGpuLattice (P2P halos; all slabs on device 0 here)
 //       <= 1e-12 vs the reference lbm::step over 6 periodic steps
+//   G10 StepVariant::Fused2 (two steps per HBM sweep) on SoA: 10 steps
+//       <= 1e-12 vs the reference lbm::step, and bit for bit == 10 fused steps
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -184,6 +186,24 @@ bool g5() {
     return s.time_step() == ref.time_step && max_rel(s.dump().values, ref.dump().values) <= 1e-12;
 }
 
+bool g10() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(40, 300, 89);
+    lbm::LatticeState ref{lbm::Descriptor(lbm::LayoutKind::SoA, lbm::Geometry{40, 300})};
+    ref.load(init);
+    lbm::ThreadPool pool(4);
+    for (int n = 0; n < 10; ++n) lbm::step(ref, m, 0.9, pool);
+    lbm_b200::LatticeState two(B::SoA, lbm_b200::Geometry{40, 300});
+    two.load(to_gpu(init));
+    lbm_b200::step(two, reference_model(), 0.9, 10, lbm_b200::StepVariant::Fused2);
+    lbm_b200::LatticeState one(B::SoA, lbm_b200::Geometry{40, 300});
+    one.load(to_gpu(init));
+    lbm_b200::step(one, reference_model(), 0.9, 10, lbm_b200::StepVariant::Fused);
+    const auto a = two.dump().values, b = one.dump().values;
+    return two.time_step() == ref.time_step && max_rel(a, ref.dump().values) <= 1e-12 &&
+           std::memcmp(a.data(), b.data(), a.size() * sizeof(double)) == 0;
+}
+
 bool g6() {
     auto within = [](double got, double want, double tol) { return std::abs(got - want) / want <= tol; };
     return within(lbm_b200::propagate_gbps(1024, 8192, 37, 0.0125), 398.0, 0.01) &&
@@ -252,7 +272,7 @@ bool g9() {
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::array<std::pair<const char*, bool (*)()>, 9> all = {{{"G1", g1},
+    const std::array<std::pair<const char*, bool (*)()>, 10> all = {{{"G1", g1},
                                                                      {"G2", g2},
                                                                      {"G3", g3},
                                                                      {"G4", g4},
@@ -260,7 +280,8 @@ int main(int argc, char** argv) {
                                                                      {"G6", g6},
                                                                      {"G7", g7},
                                                                      {"G8", g8},
-                                                                     {"G9", g9}}};
+                                                                     {"G9", g9},
+                                                                     {"G10", g10}}};
     int failures = 0;
     for (const auto& [name, fn] : all) {
         if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;

@@ -33,4 +33,4 @@ def test_cpp_parity_all_criteria(gpu):
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 9
+    assert r.stdout.count("PASS") == 10
