@@ -7,8 +7,13 @@ import paper_1804_01918_b200 as lbm  # noqa: E402
 
 lx, ly = (int(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (4096, 16384)))
 n = 40
+import os
+BC = os.environ.get("BC", "wall")
+ONLY = os.environ.get("ONLY")
 for layout, vl, variant in (("caosoa", 32, "fused"), ("soa", 1, "fused"), ("soa", 1, "fused2")):
-    s = lbm.Simulation(layout, lx, ly, vl, device=0, bc="wall", variant=variant)
+    if ONLY and variant != ONLY:
+        continue
+    s = lbm.Simulation(layout, lx, ly, vl, device=0, bc=BC, variant=variant)
     s.init_rt_device(12345)
     s.step(0.8, 4)
     best = 1e9
