@@ -264,6 +264,12 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
  * restarts the averaging window. */
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
+/* Measurement helper (no reference counterpart): the achieved FP64 rate of
+ * independent DFMA chains on every SM of `device`, in TFLOP/s (2 FLOP per
+ * DFMA) -- the FP64 roofline denominator at the clocks the GPU holds under
+ * load (bench.py; MEASURED_PEAKS.json has no FP64 figure). */
+int d2q37_fp64_peak(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -141,6 +141,7 @@ def _load():
         "d2q37_p2p_export": (i, [vp, C.c_char_p]),
         "d2q37_p2p_connect": (i, [vp, C.c_char_p, C.c_char_p]),
         "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
+        "d2q37_fp64_peak": (i, [i, P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -338,6 +339,14 @@ def slab_neighbors(rank: int, nranks: int, bc: str = "periodic"):
     out = (C.c_int * 2)()
     _check(_load().d2q37_slab_neighbors(rank, nranks, BCS[bc], out))
     return out[0], out[1]
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Achieved FP64 TFLOP/s of independent DFMA chains on every SM (the FP64 roofline denominator
+    at the clocks the GPU holds under load; MEASURED_PEAKS.json has no FP64 figure)."""
+    out = C.c_double(0.0)
+    _check(_load().d2q37_fp64_peak(int(device), C.byref(out)))
+    return out.value
 
 
 def nccl_unique_id() -> bytes:

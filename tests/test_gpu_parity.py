@@ -1014,3 +1014,10 @@ def test_fused2_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, bc):
     s.step(1.2, 7)
     assert np.array_equal(s.dump(), ref.dump())
     assert s.exposed_halo_ms() > 0.0
+
+
+def test_fp64_peak_probe_is_plausible(gpu, lbm):
+    """The FP64 roofline denominator of bench.py: a B200 has 64 FP64 lanes per SM, 37 TFLOP/s at
+    the 1.965 GHz boost clock; under the power cap the probe lands below that, never above ~40."""
+    tf = lbm.fp64_peak(0)
+    assert 10.0 < tf < 41.0, tf
