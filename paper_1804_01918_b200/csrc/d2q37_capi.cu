@@ -592,9 +592,14 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
 }
 
 // Two time steps in one HBM sweep (D2Q37_FUSED2, d2q37_step2.cu).
+// Profiling: the interior-band kernel is class "fused", each face-band launch
+// class "boundary" (bench.py adds them up per sweep).
 int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
-    ProfScope ps(h, kProfFused);
-    CK(launch_step2(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, h->d_flag, h->stream));
+    for (int part = 0; part < 3; ++part) {
+        if (!step2_part_nonempty(h->g, fc, part)) continue;
+        ProfScope ps(h, part == 0 ? kProfFused : kProfBoundary);
+        CK(launch_step2(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, h->d_flag, h->stream, part));
+    }
     h->cur = 1 - h->cur;
     h->time_step += 2;
     return D2Q37_OK;

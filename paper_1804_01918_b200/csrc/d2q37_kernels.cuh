@@ -116,8 +116,11 @@ cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int l
 // Two fused steps in one sweep (d2q37_step2.cu): SoA (vl = 1), x-major storage,
 // periodic x, periodic or wall y faces, FAST math.  src and dst must differ.
 bool step2_supported(const DevGeo& g, const Faces& fc);
+// One part of a sweep: 0 = the plain (interior) bands, 1 / 2 = the low / high
+// face bands (general kernel); step2_part_nonempty says whether a part exists.
+bool step2_part_nonempty(const DevGeo& g, const Faces& fc, int part);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                         double omega, int* flag, cudaStream_t s);
+                         double omega, int* flag, cudaStream_t s, int part);
 // FUSED2 slab halos (deep SoA geometry): 6 rows per face and population,
 // buffers of halo6_count(g) doubles laid out [p][x][6].
 size_t halo6_count(const DevGeo& g);

@@ -338,8 +338,33 @@ bool step2_supported(const DevGeo& g, const Faces& fc) {
 
 size_t step2_smem_bytes() { return (size_t)kT2RingCols * kT2Band * sizeof(double); }
 
+namespace {
+// Band split of one sweep: plain bands [b_lo, b_hi) -- every pull row (y0 - 6 ..
+// y0 + 127) inside [0, ly), or any band of a y-periodic lattice -- and the face
+// bands [0, b_lo) / [b_hi, nbands), which take the general kernel.
+void step2_bands(const DevGeo& g, const Faces& fc, int* nbands, int* b_lo, int* b_hi) {
+    *nbands = (g.ly + kT2Out - 1) / kT2Out;
+    const bool per_lo = fc.lo == kFacePeriodic, per_hi = fc.hi == kFacePeriodic;
+    int lo = 0, hi = *nbands;
+    if (!(per_lo && per_hi)) {
+        lo = per_lo ? 0 : 1;
+        hi = per_hi ? *nbands : (g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0);
+    }
+    hi = std::min(hi, *nbands);
+    if (g.lx < kHalo || hi <= lo) lo = hi = 0;  // degenerate: every band general
+    *b_lo = lo;
+    *b_hi = hi;
+}
+}  // namespace
+
+bool step2_part_nonempty(const DevGeo& g, const Faces& fc, int part) {
+    int nb, lo, hi;
+    step2_bands(g, fc, &nb, &lo, &hi);
+    return part == 0 ? hi > lo : part == 1 ? lo > 0 : hi < nb;
+}
+
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                         double omega, int* flag, cudaStream_t s) {
+                         double omega, int* flag, cudaStream_t s, int part) {
     constexpr int kMaxDev = 64;
     static int nsm_of[kMaxDev] = {};  // per device: SM count once the attributes are set
     int dev = 0;
@@ -356,32 +381,18 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
         if (e != cudaSuccess) return e;
         if (dev < kMaxDev) nsm_of[dev] = nsm;
     }
-    const int nbands = (g.ly + kT2Out - 1) / kT2Out;
-    // plain bands [b_lo, b_hi): every pull row (y0 - 6 .. y0 + 127) inside [0, ly), or any band of a
-    // y-periodic lattice; the face bands around them take the general kernel
-    const bool per_lo = fc.lo == kFacePeriodic, per_hi = fc.hi == kFacePeriodic;
-    int b_lo = 0, b_hi = nbands;
-    if (!(per_lo && per_hi)) {
-        b_lo = per_lo ? 0 : 1;
-        b_hi = per_hi ? nbands : (g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0);
-    }
-    if (g.lx < kHalo || b_hi <= b_lo) b_lo = b_hi = 0;  // degenerate: all bands general
-    b_hi = std::min(b_hi, nbands);
-    auto launch = [&](bool plain, int band0, int nb) {
-        if (nb <= 0) return;
-        const long long total = (long long)nb * g.lx;
-        const int grid = (int)std::min<long long>(nsm, total);
-        const long long per_cta = (total + grid - 1) / grid;
-        if (plain)
-            k_step2_plain<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
-                                                                        flag);
-        else
-            k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta,
-                                                                  flag);
-    };
-    launch(true, b_lo, b_hi - b_lo);
-    launch(false, 0, b_lo);
-    launch(false, b_hi, nbands - b_hi);
+    int nbands, b_lo, b_hi;
+    step2_bands(g, fc, &nbands, &b_lo, &b_hi);
+    const int band0 = part == 0 ? b_lo : part == 1 ? 0 : b_hi;
+    const int nb = part == 0 ? b_hi - b_lo : part == 1 ? b_lo : nbands - b_hi;
+    if (nb <= 0) return cudaSuccess;
+    const long long total = (long long)nb * g.lx;
+    const int grid = (int)std::min<long long>(nsm, total);
+    const long long per_cta = (total + grid - 1) / grid;
+    if (part == 0)
+        k_step2_plain<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta, flag);
+    else
+        k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
     return cudaGetLastError();
 }
 
