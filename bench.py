@@ -438,8 +438,8 @@ def bench_variant(lbm, ly, layout, vl, variant, warmup, steps, hbm_peak: float =
                                                     (FP64_NOMINAL_TFLOPS * 1e12))
             if upd > 1:
                 out[f"{k}_steps_per_launch"] = upd
-    if variant == "fused2" and kt["fused"][1]:  # a sweep = interior-band kernel + face-band launches
-        sweep = (kt["fused"][0] + kt["boundary"][0]) / kt["fused"][1]
+    if variant == "fused2" and kt["fused"][1]:  # one launch per sweep
+        sweep = kt["fused"][0] / kt["fused"][1]
         out["sweep_ms"] = sweep
         out["sweep_frac_of_hbm"] = sites * BYTES_PER_SITE / (sweep / 1e3) / 1e9 / hbm_peak if hbm_peak else None
     return out
@@ -572,16 +572,15 @@ def run_b200(args, dist: Dist):
     fused_ms, fused_n = kt["fused"]
     dom = "fused" if fused_n else "collide"
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
-    if args.variant == "fused2" and fused_n:  # one sweep = the interior-band kernel + the face-band launches
-        dom_ms = (kt["fused"][0] + kt["boundary"][0]) / fused_n
+    # FUSED2: one launch per sweep (k_step2_split: interior bands beside the face bands)
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
     upd = steps_per_call(args.variant) if dom == "fused" else 1
     achieved = sites_local * BYTES_PER_SITE / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     step_ms = ms_max / args.steps
     two = upd == 2
     roofline = {"bound": "hbm",
-                "kernel": ("k_step2_plain + k_step2 (two fused pull+collide steps per HBM sweep, temporal "
-                           "blocking; interior bands + the two wall bands)" if two else
+                "kernel": ("k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "
+                           "interior bands beside the two wall bands in one launch)" if two else
                            "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak if achieved else None,

@@ -73,6 +73,7 @@ struct d2q37_lattice {
     double* recv_hi = nullptr;
     // FUSED2 slab halos: 6 rows x 37 populations per face, [send lo, send hi, recv lo, recv hi]
     double* h6[4] = {nullptr, nullptr, nullptr, nullptr};
+    int nsm = 0;  // SM count of the device (FUSED2 CTA split)
     void* comm = nullptr;
     cudaStream_t comm_stream = nullptr;
     // NCCL slabs: pack / unpack / boundary sites run on a high-priority stream
@@ -592,13 +593,34 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
 }
 
 // Two time steps in one HBM sweep (D2Q37_FUSED2, d2q37_step2.cu).
-// Profiling: the interior-band kernel is class "fused", each face-band launch
-// class "boundary" (bench.py adds them up per sweep).
+// One sweep.  The interior bands (plain form) and the face bands (general
+// form) write disjoint rows, so on a large lattice one launch runs them side
+// by side, each face part on as many SMs as keep its items per CTA at the
+// interior's (k_step2_split).  Small lattices (a few persistent-CTA waves of
+// items) run every band in one general launch.
 int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
-    for (int part = 0; part < 3; ++part) {
-        if (!step2_part_nonempty(h->g, fc, part)) continue;
-        ProfScope ps(h, part == 0 ? kProfFused : kProfBoundary);
-        CK(launch_step2(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, h->d_flag, h->stream, part));
+    const double* src = h->buf[h->cur];
+    double* dst = h->buf[1 - h->cur];
+    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    const long long n_in = step2_items(h->g, fc, 0), n_lo = step2_items(h->g, fc, 1),
+                    n_hi = step2_items(h->g, fc, 2);
+    const long long n_faces = n_lo + n_hi;
+    if (n_faces == 0) {
+        ProfScope ps(h, kProfFused);
+        CK(launch_step2(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, 0, 0));
+    } else if (n_in + n_faces <= 256LL * h->nsm || n_in == 0) {
+        ProfScope ps(h, kProfFused);
+        CK(launch_step2(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, 3, 0));
+    } else {
+        // CTAs per face part: items per CTA no more than the interior's (+15 % for the
+        // general path's cost per iteration)
+        auto share = [&](long long n) {
+            return n == 0 ? 0 : int(std::max<long long>(1, (115 * n * h->nsm + 100 * n_in - 1) / (100 * n_in)));
+        };
+        int ctas[3] = {0, share(n_lo), share(n_hi)};
+        ctas[0] = h->nsm - ctas[1] - ctas[2];
+        ProfScope ps(h, kProfFused);
+        CK(launch_step2_split(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, ctas));
     }
     h->cur = 1 - h->cur;
     h->time_step += 2;

@@ -117,10 +117,15 @@ cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int l
 // periodic x, periodic or wall y faces, FAST math.  src and dst must differ.
 bool step2_supported(const DevGeo& g, const Faces& fc);
 // One part of a sweep: 0 = the plain (interior) bands, 1 / 2 = the low / high
-// face bands (general kernel); step2_part_nonempty says whether a part exists.
-bool step2_part_nonempty(const DevGeo& g, const Faces& fc, int part);
+// face bands, 3 = every band (the last three through the general kernel);
+// step2_items = its (band, column) items; at most max_ctas persistent CTAs
+// (0: one per SM).
+long long step2_items(const DevGeo& g, const Faces& fc, int part);
+// Parts 0, 1, 2 in one launch with ctas[part] persistent CTAs each.
+cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                               const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                         double omega, int* flag, cudaStream_t s, int part);
+                         double omega, int* flag, cudaStream_t s, int part, int max_ctas);
 // FUSED2 slab halos (deep SoA geometry): 6 rows per face and population,
 // buffers of halo6_count(g) doubles laid out [p][x][6].
 size_t halo6_count(const DevGeo& g);

@@ -77,9 +77,9 @@ __device__ __forceinline__ int wrap_mod(int v, int n) {
 // of a y-periodic lattice), lx >= 3.  Every address is per-population index
 // arithmetic with a one-step wrap; this form measured ~9 % faster than the
 // table-driven general kernel.
-__global__ void __launch_bounds__(2 * kT2Band, 1)
-    k_step2_plain(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
-                  int band0, int nbands, long long per_cta, int* __restrict__ flag) {
+__device__ __forceinline__ void sweep_plain(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
+                                            const ModelParams& mp, double omega, int band0, int nbands,
+                                            long long per_cta, int* __restrict__ flag, int cta) {
     extern __shared__ double ring[];
     const bool prod = threadIdx.x < kT2Band;
     const int tid = threadIdx.x & (kT2Band - 1);
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
     const long long total = (long long)nbands * lx;
-    long long item = (long long)blockIdx.x * per_cta;
+    long long item = (long long)cta * per_cta;
     const long long item_end = min(total, item + per_cta);
     auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
     bool bad = false;
@@ -153,9 +153,10 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
 // General sweep: any band, every face kind (periodic wrap, wall image, slab
 // ghost rows) through per-thread row tables.  Launched on the face bands only
 // (k_step2_plain covers the rest).
-__global__ void __launch_bounds__(2 * kT2Band, 1)
-    k_step2(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
-            double omega, int band0, int nbands, long long per_cta, int* __restrict__ flag) {
+__device__ __forceinline__ void sweep_general(const double* __restrict__ src, double* __restrict__ dst,
+                                              const DevGeo& g, const Faces& fc, const ModelParams& mp, double omega,
+                                              int band0, int nbands, long long per_cta, int* __restrict__ flag,
+                                              int cta) {
     extern __shared__ double ring[];
     const bool prod = threadIdx.x < kT2Band;
     const int tid = threadIdx.x & (kT2Band - 1);
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
     const long long total = (long long)nbands * lx;
-    long long item = (long long)blockIdx.x * per_cta;
+    long long item = (long long)cta * per_cta;
     const long long item_end = min(total, item + per_cta);
     bool bad = false;
     while (item < item_end) {
@@ -284,6 +285,40 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     if (bad) atomicOr(flag, 1);
 }
 
+__global__ void __launch_bounds__(2 * kT2Band, 1)
+    k_step2_plain(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
+                  int band0, int nbands, long long per_cta, int* __restrict__ flag) {
+    sweep_plain(src, dst, g, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(2 * kT2Band, 1)
+    k_step2(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
+            double omega, int band0, int nbands, long long per_cta, int* __restrict__ flag) {
+    sweep_general(src, dst, g, fc, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
+}
+
+// One launch, three CTA groups: the interior bands (plain form) beside the low
+// and high face bands (general form); every CTA runs one form throughout, so
+// an SM's instruction cache holds one loop.
+struct Step2Split {
+    int band0[3], nb[3], ctas[3];
+    long long per_cta[3];
+};
+
+__global__ void __launch_bounds__(2 * kT2Band, 1)
+    k_step2_split(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
+                  double omega, Step2Split sp, int* __restrict__ flag) {
+    int cta = blockIdx.x;
+    if (cta < sp.ctas[0]) {
+        sweep_plain(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        return;
+    }
+    cta -= sp.ctas[0];
+    const int part = cta < sp.ctas[1] ? 1 : 2;
+    if (part == 2) cta -= sp.ctas[1];
+    sweep_general(src, dst, g, fc, mp, omega, sp.band0[part], sp.nb[part], sp.per_cta[part], flag, cta);
+}
+
 // 6-row slab halos of FUSED2: rows 0..5 / ly-6..ly-1 of every physical column
 // and population -> send buffers [p][x][6]; received buffers -> ghost rows
 // -6..-1 / ly..ly+5 (a null buffer skips that face).
@@ -357,14 +392,23 @@ void step2_bands(const DevGeo& g, const Faces& fc, int* nbands, int* b_lo, int* 
 }
 }  // namespace
 
-bool step2_part_nonempty(const DevGeo& g, const Faces& fc, int part) {
-    int nb, lo, hi;
-    step2_bands(g, fc, &nb, &lo, &hi);
-    return part == 0 ? hi > lo : part == 1 ? lo > 0 : hi < nb;
+namespace {
+void part_range(const DevGeo& g, const Faces& fc, int part, int* band0, int* nb) {
+    int nbands, b_lo, b_hi;
+    step2_bands(g, fc, &nbands, &b_lo, &b_hi);
+    *band0 = part == 0 ? b_lo : part == 1 ? 0 : part == 2 ? b_hi : 0;
+    *nb = part == 0 ? b_hi - b_lo : part == 1 ? b_lo : part == 2 ? nbands - b_hi : nbands;
+}
+}  // namespace
+
+long long step2_items(const DevGeo& g, const Faces& fc, int part) {
+    int band0, nb;
+    part_range(g, fc, part, &band0, &nb);
+    return (long long)nb * g.lx;
 }
 
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                         double omega, int* flag, cudaStream_t s, int part) {
+                         double omega, int* flag, cudaStream_t s, int part, int max_ctas) {
     constexpr int kMaxDev = 64;
     static int nsm_of[kMaxDev] = {};  // per device: SM count once the attributes are set
     int dev = 0;
@@ -381,18 +425,41 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
         if (e != cudaSuccess) return e;
         if (dev < kMaxDev) nsm_of[dev] = nsm;
     }
-    int nbands, b_lo, b_hi;
-    step2_bands(g, fc, &nbands, &b_lo, &b_hi);
-    const int band0 = part == 0 ? b_lo : part == 1 ? 0 : b_hi;
-    const int nb = part == 0 ? b_hi - b_lo : part == 1 ? b_lo : nbands - b_hi;
+    int band0, nb;
+    part_range(g, fc, part, &band0, &nb);
     if (nb <= 0) return cudaSuccess;
     const long long total = (long long)nb * g.lx;
-    const int grid = (int)std::min<long long>(nsm, total);
+    const int grid = (int)std::min<long long>(max_ctas > 0 ? std::min(max_ctas, nsm) : nsm, total);
     const long long per_cta = (total + grid - 1) / grid;
     if (part == 0)
         k_step2_plain<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta, flag);
     else
         k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                               const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]) {
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 64 || !attr_set[dev]) {
+        e = cudaFuncSetAttribute(k_step2_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step2_smem_bytes());
+        if (e != cudaSuccess) return e;
+        if (dev < 64) attr_set[dev] = true;
+    }
+    Step2Split sp{};
+    int grid = 0;
+    for (int part = 0; part < 3; ++part) {
+        part_range(g, fc, part, &sp.band0[part], &sp.nb[part]);
+        const long long total = (long long)std::max(0, sp.nb[part]) * g.lx;
+        sp.ctas[part] = total > 0 ? (int)std::min<long long>(ctas[part], total) : 0;
+        sp.per_cta[part] = sp.ctas[part] ? (total + sp.ctas[part] - 1) / sp.ctas[part] : 0;
+        grid += sp.ctas[part];
+    }
+    if (grid == 0) return cudaSuccess;
+    k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, sp, flag);
     return cudaGetLastError();
 }
 
