@@ -1021,3 +1021,30 @@ def test_fp64_peak_probe_is_plausible(gpu, lbm):
     the 1.965 GHz boost clock; under the power cap the probe lands below that, never above ~40."""
     tf = lbm.fp64_peak(0)
     assert 10.0 < tf < 41.0, tf
+
+
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_fused2_split_launch_bitwise(gpu, lbm, bc):
+    """Lattices past the small-lattice threshold run one k_step2_split launch per sweep (interior
+    bands in the plain form beside the face bands in the general form): bit-identical to fused steps,
+    single domain and as two slabs with ghost faces."""
+    lx, ly = 4096, 2048
+    s2 = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused2")
+    s2.init_rt_device(99)
+    s1 = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused")
+    s1.init_rt_device(99)
+    s2.step(0.8, 4)
+    s1.step(0.8, 4)
+    want = s1.dump()
+    s1.close()
+    assert np.array_equal(s2.dump(), want)
+    init = s2.dump(which=0)
+    s2.close()
+    grp = lbm.SlabGroup("soa", lx, 2 * ly, 1, 2, bc=bc, variant="fused2")
+    ref = sim_of(lbm, "soa", lx, 2 * ly, bc=bc, variant="fused")
+    big = np.concatenate([init, init[:, :, ::-1]], axis=2)
+    grp.load(big)
+    ref.load(big)
+    grp.step(0.8, 2)
+    ref.step(0.8, 2)
+    assert np.array_equal(grp.dump(), ref.dump())
