@@ -377,6 +377,34 @@ def bench_slab_schedule_fused2(lbm, ly, warmup, steps) -> dict:
     return out
 
 
+def bench_fused2_group_emulation(lbm, nslabs, warmup, steps) -> dict:
+    """BASELINE config 4 strong (4096 x 32768) as `nslabs` FUSED2 y-slabs on ONE GPU (group transport:
+    6-row halos by device copies, each slab's sweep with its ghost-face bands), vs the same lattice
+    as one domain: the cost of the decomposition at the per-GPU slab size of the 8-GPU run."""
+    ly = STRONG_LY
+    out = {"config": f"{LX}x{ly} soa FUSED2, walls, {nslabs} slabs on one GPU (device-copy halos) vs one domain, "
+                     f"{steps} steps"}
+    sim = lbm.Simulation("soa", LX, ly, 1, device=0, bc="wall", variant="fused2")
+    sim.init_rt_device(SEED)
+    sim.step(OMEGA, warmup)
+    ms = time_stepping(sim, steps, "fused2")
+    out["single_domain"] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6}
+    init = sim.dump()
+    sim.close()
+    del sim
+    grp = lbm.SlabGroup("soa", LX, ly, 1, nslabs, bc="wall", variant="fused2")
+    grp.load(init)
+    del init
+    grp.step(OMEGA, warmup)
+    s0 = grp.slabs[0]
+    ms = time_steps(s0, steps // 2, lambda: grp.step(OMEGA, 2))
+    out[f"group_{nslabs}"] = {"ms_per_step": ms / steps, "mlups": LX * ly * steps / (ms / 1e3) / 1e6,
+                             "timing": "CUDA events on the group's shared stream"}
+    grp.close()
+    out["decomposition_overhead"] = out[f"group_{nslabs}"]["ms_per_step"] / out["single_domain"]["ms_per_step"] - 1.0
+    return out
+
+
 def bench_p2p_ring_emulation(lbm, layout, vl, nslabs, warmup, steps) -> dict:
     """BASELINE config 4 strong (4096 x 32768) as `nslabs` P2P slabs on ONE GPU, stepped in
     lockstep through the real peer-memory protocol (counters, remote stores, separate streams),
@@ -655,6 +683,10 @@ def run_b200(args, dist: Dist):
                 "weak_slab": bench_slab_schedule_fused2(lbm, LY_PER_GPU, 4, 20)}
         except Exception as e:  # noqa: BLE001
             line["slab_schedule_fused2"] = {"error": str(e)}
+        try:
+            line["fused2_group_emulation"] = bench_fused2_group_emulation(lbm, 8, 4, 20)
+        except Exception as e:  # noqa: BLE001
+            line["fused2_group_emulation"] = {"error": str(e)}
         # the single-step multi-GPU schedules (CAoSoA vl 32: NCCL columns / peer-memory push)
         try:
             line["slab_schedule"] = {
