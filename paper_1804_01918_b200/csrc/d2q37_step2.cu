@@ -77,6 +77,10 @@ __device__ __forceinline__ int wrap_mod(int v, int n) {
 // of a y-periodic lattice), lx >= 3.  Every address is per-population index
 // arithmetic with a one-step wrap; this form measured ~9 % faster than the
 // table-driven general kernel.
+// WRAPY: y-periodic lattice (rows wrap); otherwise rows are read unwrapped --
+// inside [0, ly) for bands away from the faces, and down to -6 / up to ly+5
+// (the deep ghost rows a slab's halo exchange fills) at ghost faces.
+template <bool WRAPY>
 __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
                                             const ModelParams& mp, double omega, int band0, int nbands,
                                             long long per_cta, int* __restrict__ flag, int cta) {
@@ -101,11 +105,13 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
         const int ny = min(kT2Out, ly - y0);
         const int niter = xe - xs + 7;  // producer rows t = 0 .. niter-2, consumer t = 7 .. niter-1
         if (prod) {
-            const int y1 = wrap_mod(y0 - kHalo + tid, ly);  // step-1 row of this thread
+            // step-1 row of this thread (rows past ly + 2 of the last band are never read)
+            const int y1 = WRAPY ? wrap_mod(y0 - kHalo + tid, ly) : min(y0 - kHalo + tid, ly + kHalo - 1);
             auto load = [&](double(&v)[kNpop], int r) {
 #pragma unroll
                 for (int p = 0; p < kNpop; ++p)
-                    v[p] = __ldg(sb + p * plane + (long long)wr(wr(r, lx) - cx_of(p), lx) * cs + wr(y1 - cy_of(p), ly));
+                    v[p] = __ldg(sb + p * plane + (long long)wr(wr(r, lx) - cx_of(p), lx) * cs +
+                                 (WRAPY ? wr(y1 - cy_of(p), ly) : y1 - cy_of(p)));
             };
             // the next column's loads issue before this column's collide (register double buffer)
             auto body = [&](double(&f)[kNpop], double(&fn)[kNpop], int t) {
@@ -285,10 +291,11 @@ __device__ __forceinline__ void sweep_general(const double* __restrict__ src, do
     if (bad) atomicOr(flag, 1);
 }
 
+template <bool WRAPY>
 __global__ void __launch_bounds__(2 * kT2Band, 1)
     k_step2_plain(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
                   int band0, int nbands, long long per_cta, int* __restrict__ flag) {
-    sweep_plain(src, dst, g, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
+    sweep_plain<WRAPY>(src, dst, g, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
 }
 
 __global__ void __launch_bounds__(2 * kT2Band, 1)
@@ -310,7 +317,10 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                   double omega, Step2Split sp, int* __restrict__ flag) {
     int cta = blockIdx.x;
     if (cta < sp.ctas[0]) {
-        sweep_plain(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic)
+            sweep_plain<true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        else
+            sweep_plain<false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
         return;
     }
     cta -= sp.ctas[0];
@@ -382,8 +392,10 @@ void step2_bands(const DevGeo& g, const Faces& fc, int* nbands, int* b_lo, int* 
     const bool per_lo = fc.lo == kFacePeriodic, per_hi = fc.hi == kFacePeriodic;
     int lo = 0, hi = *nbands;
     if (!(per_lo && per_hi)) {
-        lo = per_lo ? 0 : 1;
-        hi = per_hi ? *nbands : (g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0);
+        // only the wall bands need the general form: ghost faces read the deep ghost rows unwrapped
+        lo = fc.lo == kFaceWall ? 1 : 0;
+        hi = fc.hi == kFaceWall ? (g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0) : *nbands;
+        if (per_lo != per_hi) lo = 0, hi = 0;  // one periodic face with a wall / ghost one: all general
     }
     hi = std::min(hi, *nbands);
     if (g.lx < kHalo || hi <= lo) lo = hi = 0;  // degenerate: every band general
@@ -420,7 +432,10 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step2_smem_bytes());
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_step2_plain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(k_step2_plain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)step2_smem_bytes());
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_step2_plain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)step2_smem_bytes());
         if (e != cudaSuccess) return e;
         if (dev < kMaxDev) nsm_of[dev] = nsm;
@@ -431,8 +446,12 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
     const long long total = (long long)nb * g.lx;
     const int grid = (int)std::min<long long>(max_ctas > 0 ? std::min(max_ctas, nsm) : nsm, total);
     const long long per_cta = (total + grid - 1) / grid;
-    if (part == 0)
-        k_step2_plain<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta, flag);
+    if (part == 0 && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic)
+        k_step2_plain<true><<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
+                                                                          flag);
+    else if (part == 0)
+        k_step2_plain<false><<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
+                                                                           flag);
     else
         k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
     return cudaGetLastError();
