@@ -1,19 +1,21 @@
-// d2q37_step2.cu -- two D2Q37 time steps per HBM sweep (temporal blocking).
+// d2q37_step2.cu -- two D2Q37 time steps per HBM sweep (temporal blocking, FUSED2).
 //
 // The single-step kernel (k_collide<.., SHIFT>) moves the algorithmic 592 B per
 // site and step at ~105 % of the measured copy bandwidth, so past it a step
-// has to cost fewer HBM bytes.  k_step2 reads the state once and writes the
-// state two steps later: 592 B per site per TWO steps.
+// has to cost fewer HBM bytes.  A FUSED2 sweep reads the state once and writes
+// the state two steps later: 592 B per site per TWO steps.
 //
 // Storage: SoA (layout.hpp:74-75, vl = 1, x-major), the padded buffer of the
 // other kernels; physical sites only are read and written, the boundary is
-// resolved in the kernel (x periodic; y periodic or specular wall).
+// resolved in the kernel (x periodic; y periodic, specular wall, or -- on a
+// y-slab -- the 6 deep ghost rows per face that k_pack6 / NCCL / k_unpack6
+// fill before every sweep).
 //
 // Schedule (persistent CTAs, one per SM):
 //   * the lattice is cut into bands of kT2Out = 122 rows; a CTA walks a
 //     contiguous range of (band, column) items in band-major order, marching
 //     along x;
-//   * producer warps (threads 0-127) compute step 1 -- the pull of step
+//   * producer warps (threads 0-127) compute step 1 -- the pull of
 //     kernels.cpp:50-63 from HBM plus collide, model.cpp:293-298 -- for the 128
 //     rows y0-3 .. y0+124 of column r and park the result in a shared-memory
 //     ring; the next column's 37 loads are issued before this column's
@@ -25,9 +27,13 @@
 //     i.e. it lives cx_p + 4 iterations (+1: producer and consumer run
 //     concurrently), so the ring holds sum_p (cx_p + 5) = 185 population
 //     columns of 128 doubles = 185 KB.
-// Every site is updated with the same gathered values and the same
-// collide_site_sym as the single-step kernel, so two steps of k_step2 are bit
-// for bit two steps of k_collide<FAST, SHIFT> (tests/test_gpu_parity.py).
+// Two code forms of that schedule: sweep_plain (per-population index
+// arithmetic; every band of a periodic lattice, bands away from a wall, slab
+// ghost faces) and sweep_general (per-thread row tables; wall bands and
+// degenerate extents).  k_step2_split runs both in one launch, on disjoint CTA
+// groups.  Every site is updated with the same gathered values and the same
+// collide_site_sym as the single-step kernel, so a sweep is bit for bit two
+// steps of k_collide<FAST, SHIFT> (tests/test_gpu_parity.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,7 +82,7 @@ __device__ __forceinline__ int wrap_mod(int v, int n) {
 // Plain sweep: bands whose pulls stay inside the lattice rows (or any band
 // of a y-periodic lattice), lx >= 3.  Every address is per-population index
 // arithmetic with a one-step wrap; this form measured ~9 % faster than the
-// table-driven general kernel.
+// table-driven general form.
 // WRAPY: y-periodic lattice (rows wrap); otherwise rows are read unwrapped --
 // inside [0, ly) for bands away from the faces, and down to -6 / up to ly+5
 // (the deep ghost rows a slab's halo exchange fills) at ghost faces.
