@@ -59,9 +59,11 @@ enum { D2Q37_BC_PERIODIC = 0, D2Q37_BC_WALL = 1 };
  * FUSED = bc, one pull-gather + collide kernel.
  * FUSED2 = two time steps per HBM sweep (temporal blocking, csrc/d2q37_step2.cu):
  * every pair of steps is one kernel that reads the state once and writes it two
- * steps later, bit-identical to two FUSED steps.  Used on single-domain SoA
- * lattices with FAST math and periodic / wall faces; an odd last step and every
- * other case (other layouts, slabs, STRICT math) run FUSED steps. */
+ * steps later, bit-identical to two FUSED steps.  Used on SoA lattices with
+ * FAST math: single domain (periodic / wall faces), NCCL y-slabs and slab
+ * groups (6-row halos exchanged once per two steps); an odd last step and
+ * every other case (other layouts, P2P-transport slabs, STRICT math) run FUSED
+ * steps. */
 enum { D2Q37_UNFUSED = 0, D2Q37_FUSED = 1, D2Q37_FUSED2 = 2 };
 
 /* Arithmetic of the collide kernels.  FAST lets nvcc contract into DFMA (as the
