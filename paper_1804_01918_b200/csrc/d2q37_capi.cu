@@ -1367,7 +1367,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
         variant = D2Q37_FUSED;  // the odd last step, and every layout / case k_step2 does not cover
     }
-    if (!slab && !h->prof_on && nsteps >= kGraphSteps) {
+    if (!slab && !h->prof_on && nsteps - s >= kGraphSteps) {
         // Launch-bound small lattices: replay kGraphSteps steps as one CUDA graph.
         RET(ensure_step_graph(h, omega, variant, bc));
         if (h->graph.exec) {
