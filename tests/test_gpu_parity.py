@@ -280,9 +280,10 @@ def test_collide_equilibrium_fixed_point(gpu, lbm):
 
 # --------------------------------------------------------------------------- full steps
 
-@pytest.mark.parametrize("variant", ["fused", "unfused"])
+@pytest.mark.parametrize("variant", ["fused", "unfused", "fused2"])
 def test_step_vs_reference_golden(gpu, lbm, variant):
-    """10 periodic reference steps (CSoA vl=4 in the reference) within 1e-12 (1e-9 is the 100-step bar)."""
+    """10 periodic reference steps (CSoA vl=4 in the reference) within 1e-12 (1e-9 is the 100-step bar);
+    fused2 runs them as five two-step sweeps."""
     gm = golden("ref_model.npz")
     mdl = lbm.Model.from_arrays(gm["cx"], gm["cy"], gm["w"], gm["t0"], gm["eq"])
     for name in ("ref_random_16x32.npz", "ref_random_5x12.npz"):
@@ -1048,3 +1049,19 @@ def test_fused2_split_launch_bitwise(gpu, lbm, bc):
     grp.step(0.8, 2)
     ref.step(0.8, 2)
     assert np.array_equal(grp.dump(), ref.dump())
+
+
+@pytest.mark.parametrize("lx,ly", [(2, 5), (3, 6), (6, 130), (4, 250)])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+def test_fused2_degenerate_extents_bitwise(gpu, lbm, lx, ly, bc):
+    """FUSED2 on tiny extents (x wraps more than one period: lx = 2, 3; a single band; ly = 6 / 130 /
+    250 put band edges next to the walls) equals fused steps bit for bit."""
+    init = lbm.make_lattice("random", lx, ly, seed=61)
+    a = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused2")
+    b = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused")
+    a.load(init)
+    b.load(init)
+    a.step(0.9, 6)
+    b.step(0.9, 6)
+    assert np.array_equal(a.dump(), b.dump())
+
