@@ -546,7 +546,20 @@ def make_slab(lbm, args, dist: Dist, dev: int, ly_global: int):
             return sim, "p2p"
         if sim is not None:
             sim.close()
-    uid = dist.bcast_bytes(lbm.nccl_unique_id() if rank == 0 else None)
+    uid0 = None
+    if rank == 0:
+        try:
+            uid0 = lbm.nccl_unique_id()
+        except Exception as e:  # noqa: BLE001 -- every rank learns it through the broadcast
+            print(f"[rank 0] NCCL unavailable ({e})", file=sys.stderr, flush=True)
+    uid = dist.bcast_bytes(uid0)
+    if uid is None:
+        if args.variant == "fused2":  # collectively: the single-sweep slabs with the peer-memory push
+            print(f"[rank {rank}] FUSED2 slabs need NCCL; using the single-sweep CAoSoA32 P2P path",
+                  file=sys.stderr, flush=True)
+            args.layout, args.vl, args.variant, args.transport = "caosoa", 32, "fused", "p2p"
+            return make_slab(lbm, args, dist, dev, ly_global)
+        raise RuntimeError("no halo transport: P2P and NCCL both unavailable")
     sim = lbm.Simulation.slab(args.layout, LX, ly_global, args.vl, device=dev, rank=rank, nranks=n,
                               nccl_id=uid, bc="wall", variant=args.variant)
     return sim, "nccl"

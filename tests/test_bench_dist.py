@@ -34,10 +34,13 @@ class _FakeSim:
 
 
 class _FakeLbm:
-    def __init__(self, fail_rank):
+    def __init__(self, fail_rank, nccl=True):
         self.fail_rank = fail_rank
+        self.nccl = nccl
 
     def nccl_unique_id(self):
+        if not self.nccl:
+            raise OSError("libnccl.so.2 not found")
         return b"id"
 
     @property
@@ -53,7 +56,7 @@ class _FakeLbm:
         return S
 
 
-def _worker(rank, world, port, fail_rank, q, variant="fused"):
+def _worker(rank, world, port, fail_rank, q, variant="fused", nccl=True):
     sys.path.insert(0, ROOT)
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
                       MASTER_PORT=str(port), BENCH_DIST_BACKEND="gloo")
@@ -65,8 +68,8 @@ def _worker(rank, world, port, fail_rank, q, variant="fused"):
     try:
         layout, vl = ("soa", 1) if variant == "fused2" else ("caosoa", 32)
         args = argparse.Namespace(transport="p2p", layout=layout, vl=vl, variant=variant)
-        sim, transport = bench.make_slab(_FakeLbm(fail_rank), args, d, 0, 4096)
-        q.put((rank, transport, sim.transport, sim.connected))
+        sim, transport = bench.make_slab(_FakeLbm(fail_rank, nccl), args, d, 0, 4096)
+        q.put((rank, transport, sim.transport, sim.connected, args.variant, args.layout))
     finally:
         d.close()
 
@@ -105,3 +108,20 @@ def test_make_slab_fused2_uses_nccl_on_every_rank():
         assert p.exitcode == 0
     assert [got[r][0] for r in (0, 1)] == ["nccl", "nccl"]
     assert [got[r][1] for r in (0, 1)] == ["nccl", "nccl"]
+
+
+def test_make_slab_fused2_without_nccl_falls_back_to_p2p_on_every_rank():
+    """NCCL missing (rank 0 cannot make an id): every rank learns it from the broadcast and takes the
+    single-sweep CAoSoA32 P2P path -- none waits on a communicator that will not come."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, -1, q, "fused2", False)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, rest) for r, *rest in (q.get(timeout=120) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [got[r][0] for r in (0, 1)] == ["p2p", "p2p"]
+    assert [(got[r][3], got[r][4]) for r in (0, 1)] == [("fused", "caosoa")] * 2
