@@ -707,7 +707,12 @@ int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
         return D2Q37_OK;
     }
     int rc = D2Q37_OK;
-    for (int i = 0; i < kGraphSteps && rc == D2Q37_OK; ++i) rc = step_local(h, omega, variant, bc);
+    if (variant == D2Q37_FUSED2) {  // kGraphSteps two-step sweeps (an even number: cur is unchanged)
+        const Faces fc = step_faces(h, bc);
+        for (int i = 0; i < kGraphSteps && rc == D2Q37_OK; ++i) rc = step2_local(h, omega, fc);
+    } else {
+        for (int i = 0; i < kGraphSteps && rc == D2Q37_OK; ++i) rc = step_local(h, omega, variant, bc);
+    }
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
     h->cur = cur0;  // capture only recorded the launches
@@ -1357,6 +1362,19 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         const Faces fc = step_faces(h, bc);
         if (h->math == D2Q37_MATH_FAST && step2_supported(h->g, fc)) {
             if (!slab) {
+                if (!h->prof_on && nsteps - s >= 4 * kGraphSteps) {
+                    // launch-bound small lattices: one direct sweep (kernel attributes, SM
+                    // count), then graphs of kGraphSteps sweeps
+                    RET(step2_local(h, omega, fc));
+                    s += 2;
+                    RET(ensure_step_graph(h, omega, D2Q37_FUSED2, bc));
+                    if (h->graph.exec) {
+                        for (; s + 2 * kGraphSteps <= nsteps; s += 2 * kGraphSteps) {
+                            CK(cudaGraphLaunch(h->graph.exec, h->stream));
+                            h->time_step += 2 * kGraphSteps;
+                        }
+                    }
+                }
                 for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
             } else if (h->transport == kTransportNccl) {
                 for (; s + 2 <= nsteps; s += 2) {

@@ -1065,3 +1065,23 @@ def test_fused2_degenerate_extents_bitwise(gpu, lbm, lx, ly, bc):
     b.step(0.9, 6)
     assert np.array_equal(a.dump(), b.dump())
 
+
+
+def test_fused2_graph_replay_bitwise(gpu, lbm):
+    """step(n >= 40) with FUSED2 replays captured graphs of ten two-step sweeps: equal to single fused
+    steps bit for bit, across an omega / bc change (recapture) and with odd n."""
+    lx, ly = 64, 256
+    init = lbm.make_lattice("random", lx, ly, seed=4)
+    a = sim_of(lbm, "soa", lx, ly, variant="fused2", bc="wall")
+    b = sim_of(lbm, "soa", lx, ly, variant="fused", bc="wall")
+    a.load(init)
+    b.load(init)
+    a.step(1.1, 47)
+    for _ in range(47):
+        b.step(1.1, 1)
+    assert a.time_step == b.time_step == 47
+    assert np.array_equal(a.dump(), b.dump())
+    a.step(0.7, 44, bc="periodic")
+    for _ in range(44):
+        b.step(0.7, 1, bc="periodic")
+    assert np.array_equal(a.dump(), b.dump())
