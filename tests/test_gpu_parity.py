@@ -1085,3 +1085,36 @@ def test_fused2_graph_replay_bitwise(gpu, lbm):
     for _ in range(44):
         b.step(0.7, 1, bc="periodic")
     assert np.array_equal(a.dump(), b.dump())
+
+
+def test_fused2_checkpoint_restart_bitwise(gpu, lbm, tmp_path):
+    """A FUSED2 run checkpointed to LBDUMP01 (dump.cpp:44-70) after 6 steps and restarted in a fresh
+    lattice continues bit for bit like the uninterrupted run."""
+    lx, ly = 40, 300
+    init = lbm.make_lattice("random", lx, ly, seed=71)
+    full = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    full.load(init)
+    full.step(1.05, 12)
+    part = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    part.load(init)
+    part.step(1.05, 6)
+    path = str(tmp_path / "ck.lbdump")
+    part.save_dump(path)
+    part.close()
+    resumed = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    resumed.load_dump(path)
+    resumed.step(1.05, 6)
+    assert np.array_equal(resumed.dump(), full.dump())
+
+
+def test_fused2_slab_nonphysical_raises(gpu, lbm):
+    """NonPhysicalError (model.hpp:28-30) from a FUSED2 sweep of a slab group."""
+    lx, ly = 16, 96
+    bad = lbm.make_lattice("random", lx, ly, seed=72)
+    bad[:, 3, 70] = -1.0
+    grp = lbm.SlabGroup("soa", lx, ly, 1, 2, variant="fused2")
+    grp.load(bad)
+    with pytest.raises(lbm.NonPhysicalError):
+        grp.step(1.0, 2)
+        for s in grp.slabs:
+            s.sync()
