@@ -266,6 +266,16 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
  * restarts the averaging window. */
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
+/* FUSED2 tuning (no reference counterpart; process-wide).  form: how the
+ * interior bands of a two-step sweep pull step 1 -- 1 (default) bulk copies
+ * staged in shared memory (cp.async.bulk + mbarrier), 0 per-thread loads;
+ * both are bit-identical.  face_pct: items per face-band CTA relative to an
+ * interior CTA, in percent of the interior's cost (default 115 / 135 for
+ * forms 0 / 1).  A negative argument leaves a setting unchanged; the previous
+ * values are returned through prev_form / prev_face_pct when non-null.
+ * Environment: D2Q37_STEP2_FORM, D2Q37_STEP2_FACE_PCT. */
+int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct);
+
 /* Measurement helper (no reference counterpart): the achieved FP64 rate of
  * independent DFMA chains on every SM of `device`, in TFLOP/s (2 FLOP per
  * DFMA) -- the FP64 roofline denominator at the clocks the GPU holds under

@@ -142,6 +142,7 @@ def _load():
         "d2q37_p2p_connect": (i, [vp, C.c_char_p, C.c_char_p]),
         "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
         "d2q37_fp64_peak": (i, [i, P(C.c_double)]),
+        "d2q37_set_fused2_tuning": (i, [i, i, P(C.c_int), P(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -347,6 +348,16 @@ def fp64_peak(device: int = 0) -> float:
     out = C.c_double(0.0)
     _check(_load().d2q37_fp64_peak(int(device), C.byref(out)))
     return out.value
+
+
+def set_fused2_tuning(form: int = -1, face_pct: int = -1) -> tuple:
+    """Process-wide FUSED2 tuning (d2q37_set_fused2_tuning): ``form`` 1 = interior bands staged by bulk
+    copies (default), 0 = per-thread loads (bit-identical); ``face_pct`` sizes the face-band CTA
+    groups (0 = the form's default).  -1 leaves a setting unchanged.  Returns the previous
+    (form, face_pct)."""
+    pf, pp = C.c_int(0), C.c_int(0)
+    _check(_load().d2q37_set_fused2_tuning(int(form), int(face_pct), C.byref(pf), C.byref(pp)))
+    return pf.value, pp.value
 
 
 def nccl_unique_id() -> bytes:

@@ -107,7 +107,7 @@ struct d2q37_lattice {
     struct StepGraph {
         cudaGraphExec_t exec = nullptr;
         double omega = 0.0;
-        int variant = -1, bc = -1, cur = -1, math = -1;
+        int variant = -1, bc = -1, cur = -1, math = -1, form = -1;
         unsigned long model_gen = 0;
         cudaStream_t stream = nullptr;
     } graph;
@@ -605,21 +605,20 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
     const long long n_in = step2_items(h->g, fc, 0), n_lo = step2_items(h->g, fc, 1),
                     n_hi = step2_items(h->g, fc, 2);
     const long long n_faces = n_lo + n_hi;
-    if (n_faces == 0) {
-        ProfScope ps(h, kProfFused);
-        CK(launch_step2(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, 0, 0));
-    } else if (n_in + n_faces <= 256LL * h->nsm || n_in == 0) {
-        ProfScope ps(h, kProfFused);
+    // CTAs per face part: items per CTA no more than the interior's (+ the general
+    // form's extra cost per iteration, step2_face_pct)
+    const int pct = step2_face_pct();
+    auto share = [&](long long n) {
+        return n == 0 ? 0 : int(std::max<long long>(1, (pct * n * h->nsm + 100 * n_in - 1) / (100 * n_in)));
+    };
+    const int c_lo = n_in ? share(n_lo) : 0, c_hi = n_in ? share(n_hi) : 0;
+    ProfScope ps(h, kProfFused);
+    if (n_in == 0 || n_in + n_faces <= 256LL * h->nsm || c_lo + c_hi > h->nsm / 2) {
+        // small lattices (a few persistent-CTA waves of items), or face bands too large a
+        // share to split off: every band through the general form
         CK(launch_step2(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, 3, 0));
     } else {
-        // CTAs per face part: items per CTA no more than the interior's (+15 % for the
-        // general path's cost per iteration)
-        auto share = [&](long long n) {
-            return n == 0 ? 0 : int(std::max<long long>(1, (115 * n * h->nsm + 100 * n_in - 1) / (100 * n_in)));
-        };
-        int ctas[3] = {0, share(n_lo), share(n_hi)};
-        ctas[0] = h->nsm - ctas[1] - ctas[2];
-        ProfScope ps(h, kProfFused);
+        const int ctas[3] = {h->nsm - c_lo - c_hi, c_lo, c_hi};  // interior >= nsm / 2
         CK(launch_step2_split(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, ctas));
     }
     h->cur = 1 - h->cur;
@@ -697,7 +696,7 @@ void drop_step_graph(d2q37_lattice* h) {
 int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     auto& gr = h->graph;
     if (gr.exec && gr.omega == omega && gr.variant == variant && gr.bc == bc && gr.cur == h->cur &&
-        gr.math == h->math && gr.model_gen == h->model_gen && gr.stream == h->stream)
+        gr.math == h->math && gr.model_gen == h->model_gen && gr.stream == h->stream && gr.form == step2_form())
         return D2Q37_OK;
     drop_step_graph(h);
     const int cur0 = h->cur;
@@ -736,6 +735,7 @@ int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     gr.math = h->math;
     gr.model_gen = h->model_gen;
     gr.stream = h->stream;
+    gr.form = step2_form();
     return D2Q37_OK;
 }
 
@@ -1967,6 +1967,15 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
         RET(group_exchange(slabs, bc));
         for (d2q37_lattice* h : slabs) RET(slab_phase2(h, omega, variant, bc));
     }
+    return D2Q37_OK;
+}
+
+int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct) {
+    if (prev_form) *prev_form = step2_form();
+    if (prev_face_pct) *prev_face_pct = step2_face_pct();
+    if (form > 2 || face_pct > 1000) return fail(D2Q37_ERR_INVALID_ARGUMENT, "fused2 tuning: form %d, face_pct %d", form, face_pct);
+    if (form >= 0) set_step2_form(form);
+    if (face_pct >= 0) set_step2_face_pct(face_pct);
     return D2Q37_OK;
 }
 

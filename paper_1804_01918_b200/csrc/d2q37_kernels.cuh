@@ -121,7 +121,20 @@ bool step2_supported(const DevGeo& g, const Faces& fc);
 // step2_items = its (band, column) items; at most max_ctas persistent CTAs
 // (0: one per SM).
 long long step2_items(const DevGeo& g, const Faces& fc, int part);
-// Parts 0, 1, 2 in one launch with ctas[part] persistent CTAs each.
+// Interior-band code form of a FUSED2 sweep: per-thread pulls (sweep_plain) or
+// bulk copies staged in shared memory (sweep_tma).  Default: bulk; environment
+// D2Q37_STEP2_FORM=0 selects the per-thread form.  set_step2_form returns the
+// previous form.
+enum { kStep2Plain = 0, kStep2Bulk = 1, kStep2BulkEarly = 2 };
+int step2_form();
+int set_step2_form(int form);
+// percent cost of a face-band (general form) item relative to an interior item,
+// which sizes the face CTA groups of k_step2_split (0 = the form's default)
+int step2_face_pct();
+void set_step2_face_pct(int pct);
+size_t step2_smem_bytes(int form);
+// Parts 0, 1, 2 in one launch with ctas[part] persistent CTAs each (every part
+// with items needs at least one).
 cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
                                const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,

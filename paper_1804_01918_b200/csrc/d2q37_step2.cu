@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "d2q37_device.cuh"
@@ -46,8 +47,12 @@ namespace d2q37 {
 
 namespace {
 
-constexpr int kT2Band = 128;                    // step-1 rows per band column (= producer threads)
-constexpr int kT2Out = kT2Band - 2 * kHalo;     // step-2 (output) rows per band
+#ifndef D2Q37_T2_OUT
+#define D2Q37_T2_OUT 120
+#endif
+constexpr int kT2Band = 128;        // producer threads per band column (ring rows)
+constexpr int kT2Out = D2Q37_T2_OUT;  // step-2 (output) rows per band: 120 keeps every band's stores 32-byte sectors
+static_assert(kT2Out % 2 == 0 && kT2Out + 2 * kHalo <= kT2Band, "band rows");
 D2Q37_HD constexpr int t2_depth(int p) { return cx_of(p) + 5; }
 D2Q37_HD constexpr int t2_base(int p) {
     int s = 0;
@@ -76,6 +81,46 @@ __device__ __forceinline__ int wrap_mod(int v, int n) {
     }
     return v;
 }
+
+// ---- bulk-copy staging of the producer's pulls (sweep_tma) -----------------
+// Per population a 16-byte-aligned superset of the 128 source rows: 130 doubles
+// from the even row at or below y0 - 3 - cy_p (1040 B, a multiple of 16).
+constexpr int kStageRows = kT2Band + 2;
+constexpr unsigned kStageBytes = unsigned(kNpop) * kStageRows * sizeof(double);  // 38 480 B per column
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared 1-D bulk copy (SASS UBLKCP), completion counted on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+// velocity components by runtime index (the copy-issuing lanes)
+__constant__ signed char c_cx[kNpop] = {0,  -1, 0,  0,  1,  -1, -1, 1,  1,  -2, 0,  0,  2,  -2, -2, -1, -1, 1, 1,
+                                        2,  2,  -2, -2, 2,  2,  -3, 0,  0,  3,  -3, -3, -1, -1, 1,  1,  3,  3};
+__constant__ signed char c_cy[kNpop] = {0,  0,  -1, 1,  0,  -1, 1,  -1, 1,  0,  -2, 2,  0,  -1, 1,  -2, 2, -2, 2,
+                                        -1, 1,  -2, 2,  -2, 2,  0,  -3, 3,  0,  -1, 1,  -3, 3,  -3, 3,  -1, 1};
+// named barrier 1 among the 128 producer threads
+__device__ __forceinline__ void prod_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 }  // namespace
 
@@ -141,6 +186,128 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
                 body(fb, fa, t + 1);
             }
             if (t < niter) body(fa, fb, t);
+        } else {
+#pragma unroll 1
+            for (int t = 0; t < niter; ++t) {
+                if (t >= 7 && tid < ny) {
+                    double v[kNpop];
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2_base(p), dp = t2_depth(p);
+                        v[p] = ring[(rb + (t + 1) % dp) * kT2Band + tid + kHalo - cy_of(p)];
+                    });
+                    bad |= collide_site_sym(v, omega, mp);
+                    const long long e = (long long)(xs - 7 + t) * cs + y0 + tid;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(db + p * plane + e, v[p]);
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
+// Bulk-copy sweep: the plain form's schedule with the producer's 37 pulls of
+// a column staged in shared memory by the copy engine instead of per-thread
+// loads.  After the producers have consumed column r's stage (its moments
+// need all 37 values), the four producer warps issue the 37 one-dimensional
+// bulk copies of column r + 1 (cp.async.bulk, 1040 B each: rows y0-3-cy_p ..
+// y0+124-cy_p of source column r - cx_p, 16-byte aligned) into the single
+// stage, completion counted on one mbarrier; the copies are in flight during
+// column r's relaxation, ring stores and barrier.  No per-thread address
+// arithmetic, no register double buffer, no L1 for the pulls.
+// Rows are read unwrapped: bands whose pull rows y0-6 .. y0+127 lie inside
+// the stored rows (the lattice, or the deep ghost rows of a slab face).
+// GHOST: the band may reach a slab ghost face; step-1 rows past ly + 2 are
+// never read, so those threads collide row ly + 2 (finite) instead.
+template <bool GHOST, bool EARLY>
+__device__ __forceinline__ void sweep_tma(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
+                                          const ModelParams& mp, double omega, int band0, int nbands,
+                                          long long per_cta, int* __restrict__ flag, int cta) {
+    extern __shared__ double ring[];
+    double* stage = ring + kT2RingCols * kT2Band;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(stage + kNpop * kStageRows);
+    const bool prod = threadIdx.x < kT2Band;
+    const int tid = threadIdx.x & (kT2Band - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = g.lx, ly = g.ly;
+    const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
+    double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
+    const long long plane = g.pstride, cs = g.cstride;
+    const long long total = (long long)nbands * lx;
+    long long item = (long long)cta * per_cta;
+    const long long item_end = min(total, item + per_cta);
+    auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    // copy issue: producer warp w, lane l < 10 -> population 10 w + l
+    const int ip = warp * 10 + lane;
+    const bool issuer = prod && lane < 10 && ip < kNpop;
+    const int icx = issuer ? c_cx[ip] : 0, icy = issuer ? c_cy[ip] : 0;
+    double* const idst = stage + (issuer ? ip : 0) * kStageRows;
+    unsigned phase = 0;
+    bool bad = false;
+    while (item < item_end) {
+        const int band = band0 + (int)(item / lx);
+        const int xs = (int)(item % lx);
+        const int xe = (int)min((long long)lx, xs + (item_end - item));
+        item += xe - xs;
+        const int y0 = band * kT2Out;
+        const int ny = min(kT2Out, ly - y0);
+        const int niter = xe - xs + 7;  // producer rows t = 0 .. niter-2, consumer t = 7 .. niter-1
+        if (prod) {
+            const double* const isrc = sb + ip * plane + ((y0 - kHalo - icy) & ~1);
+            auto issue = [&](int r) {
+                if (issuer) {
+                    const int col = wr(wr(r, lx) - icx, lx);
+                    bulk_g2s(idst, isrc + (long long)col * cs, kStageRows * sizeof(double), full);
+                }
+                if (threadIdx.x == 0) mbar_arrive_expect_tx(full, kStageBytes);
+            };
+            if (issuer || threadIdx.x == 0) issue(xs - kHalo);
+            // stage offset of this thread's step-1 row (y1 - cy_p - row0_p = yo + ((y0-3-cy_p) & 1))
+            const int yo = GHOST ? min(tid, ly + kHalo - 1 - (y0 - kHalo)) : tid;
+            const int par = (y0 - kHalo) & 1;
+#pragma unroll 1
+            for (int t = 0; t < niter; ++t) {
+                if (t < niter - 1) {
+                    mbar_wait(full, phase);
+                    phase ^= 1;
+                    double f[kNpop];
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value;
+                        f[p] = stage[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
+                    });
+                    if (EARLY) {
+                        // the 37 values are in registers (an empty asm consumes them): refill the stage now
+#pragma unroll
+                        for (int p = 0; p < kNpop; p += 6)
+                            asm volatile("" ::"d"(f[p]), "d"(f[min(p + 1, kNpop - 1)]), "d"(f[min(p + 2, kNpop - 1)]),
+                                         "d"(f[min(p + 3, kNpop - 1)]), "d"(f[min(p + 4, kNpop - 1)]),
+                                         "d"(f[min(p + 5, kNpop - 1)]));
+                        if (t < niter - 2) {
+                            prod_bar_sync();
+                            issue(xs - kHalo + t + 1);
+                        }
+                    }
+                    SymMoments m;
+                    bad |= sym_moments(f, mp, m);
+                    // every producer has its 37 values (the moments consumed them): refill the stage
+                    if (!EARLY && t < niter - 2) {
+                        prod_bar_sync();
+                        issue(xs - kHalo + t + 1);
+                    }
+                    sym_relax(f, m, omega, mp);
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2_base(p), dp = t2_depth(p);
+                        ring[(rb + t % dp) * kT2Band + tid] = f[p];
+                    });
+                }
+                __syncthreads();
+            }
         } else {
 #pragma unroll 1
             for (int t = 0; t < niter; ++t) {
@@ -310,12 +477,13 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     sweep_general(src, dst, g, fc, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
 }
 
-// One launch, three CTA groups: the interior bands (plain form) beside the low
-// and high face bands (general form); every CTA runs one form throughout, so
-// an SM's instruction cache holds one loop.
+// One launch, three CTA groups: the interior bands (plain form, or the
+// bulk-copy form) beside the low and high face bands (general form); every
+// CTA runs one form throughout, so an SM's instruction cache holds one loop.
 struct Step2Split {
     int band0[3], nb[3], ctas[3];
     long long per_cta[3];
+    int form;  // interior bands: 0 = sweep_plain, 1 = sweep_tma
 };
 
 __global__ void __launch_bounds__(2 * kT2Band, 1)
@@ -323,10 +491,21 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                   double omega, Step2Split sp, int* __restrict__ flag) {
     int cta = blockIdx.x;
     if (cta < sp.ctas[0]) {
-        if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic)
+        if (sp.form == kStep2Bulk) {
+            if (fc.hi == kFaceGhost)
+                sweep_tma<true, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+            else
+                sweep_tma<false, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        } else if (sp.form == kStep2BulkEarly) {
+            if (fc.hi == kFaceGhost)
+                sweep_tma<true, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+            else
+                sweep_tma<false, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        } else if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic) {
             sweep_plain<true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
-        else
+        } else {
             sweep_plain<false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+        }
         return;
     }
     cta -= sp.ctas[0];
@@ -387,20 +566,61 @@ bool step2_supported(const DevGeo& g, const Faces& fc) {
            (long long)(g.lx + 2 * kHalo) * g.cstride < 0x7fffffffLL;  // 32-bit offsets inside a plane
 }
 
-size_t step2_smem_bytes() { return (size_t)kT2RingCols * kT2Band * sizeof(double); }
+size_t step2_smem_bytes(int form) {
+    const size_t ring = (size_t)kT2RingCols * kT2Band * sizeof(double);
+    return form != kStep2Plain ? ring + kStageBytes + 16 : ring;  // + the stage and its mbarrier
+}
+
+namespace {
+int g_form = -1;  // interior-band form of every FUSED2 sweep (step2_form)
+}  // namespace
+
+int step2_form() {
+    if (g_form < 0) {
+        const char* v = std::getenv("D2Q37_STEP2_FORM");
+        g_form = v && *v ? std::min(2, std::max(0, std::atoi(v))) : kStep2Bulk;
+    }
+    return g_form;
+}
+
+int set_step2_form(int form) {
+    const int prev = step2_form();
+    g_form = std::min(2, std::max(0, form));
+    return prev;
+}
+
+namespace {
+int g_face_pct = -1;  // 0: the form's default
+}  // namespace
+
+int step2_face_pct() {
+    if (g_face_pct < 0) {
+        const char* v = std::getenv("D2Q37_STEP2_FACE_PCT");
+        g_face_pct = v ? std::max(0, std::atoi(v)) : 0;
+    }
+    return g_face_pct > 0 ? g_face_pct : (step2_form() != kStep2Plain ? 135 : 115);
+}
+
+void set_step2_face_pct(int pct) { g_face_pct = std::max(0, pct); }
 
 namespace {
 // Band split of one sweep: plain bands [b_lo, b_hi) -- every pull row (y0 - 6 ..
-// y0 + 127) inside [0, ly), or any band of a y-periodic lattice -- and the face
-// bands [0, b_lo) / [b_hi, nbands), which take the general kernel.
-void step2_bands(const DevGeo& g, const Faces& fc, int* nbands, int* b_lo, int* b_hi) {
+// y0 + 127) inside the stored rows [0, ly) (or, at a slab ghost face, the deep
+// ghost rows), or with the per-thread form any band of a y-periodic lattice --
+// and the face bands [0, b_lo) / [b_hi, nbands), which take the general kernel.
+// The bulk-copy form reads rows unwrapped, so the wrapping first and last bands
+// of a y-periodic lattice are face bands for it.
+void step2_bands(const DevGeo& g, const Faces& fc, int form, int* nbands, int* b_lo, int* b_hi) {
     *nbands = (g.ly + kT2Out - 1) / kT2Out;
     const bool per_lo = fc.lo == kFacePeriodic, per_hi = fc.hi == kFacePeriodic;
     int lo = 0, hi = *nbands;
-    if (!(per_lo && per_hi)) {
-        // only the wall bands need the general form: ghost faces read the deep ghost rows unwrapped
+    const int inside_hi = g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0;  // bands with rows < ly
+    if (per_lo && per_hi) {
+        if (form == kStep2Bulk) lo = 1, hi = inside_hi;
+    } else {
+        // ghost faces read the deep ghost rows unwrapped; wall bands need the general form
         lo = fc.lo == kFaceWall ? 1 : 0;
-        hi = fc.hi == kFaceWall ? (g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0) : *nbands;
+        hi = fc.hi == kFaceWall ? inside_hi : *nbands;
         if (per_lo != per_hi) lo = 0, hi = 0;  // one periodic face with a wall / ghost one: all general
     }
     hi = std::min(hi, *nbands);
@@ -408,83 +628,83 @@ void step2_bands(const DevGeo& g, const Faces& fc, int* nbands, int* b_lo, int* 
     *b_lo = lo;
     *b_hi = hi;
 }
-}  // namespace
 
-namespace {
-void part_range(const DevGeo& g, const Faces& fc, int part, int* band0, int* nb) {
+void part_range(const DevGeo& g, const Faces& fc, int form, int part, int* band0, int* nb) {
     int nbands, b_lo, b_hi;
-    step2_bands(g, fc, &nbands, &b_lo, &b_hi);
+    step2_bands(g, fc, form, &nbands, &b_lo, &b_hi);
     *band0 = part == 0 ? b_lo : part == 1 ? 0 : part == 2 ? b_hi : 0;
     *nb = part == 0 ? b_hi - b_lo : part == 1 ? b_lo : part == 2 ? nbands - b_hi : nbands;
+}
+
+// per-device SM count, set once with the kernels' shared-memory attributes
+int device_nsm(cudaError_t* err) {
+    constexpr int kMaxDev = 64;
+    static int nsm_of[kMaxDev] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    int nsm = (e == cudaSuccess && dev < kMaxDev) ? nsm_of[dev] : 0;
+    if (e == cudaSuccess && nsm == 0) {
+        e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int ring = (int)step2_smem_bytes(kStep2Plain), bulk = (int)step2_smem_bytes(kStep2Bulk);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_step2_plain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_step2_plain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_step2_split, cudaFuncAttributeMaxDynamicSharedMemorySize, bulk);
+        if (e == cudaSuccess && dev < kMaxDev) nsm_of[dev] = nsm;
+    }
+    *err = e;
+    return e == cudaSuccess ? nsm : 0;
 }
 }  // namespace
 
 long long step2_items(const DevGeo& g, const Faces& fc, int part) {
     int band0, nb;
-    part_range(g, fc, part, &band0, &nb);
+    part_range(g, fc, step2_form(), part, &band0, &nb);
     return (long long)nb * g.lx;
 }
 
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                          double omega, int* flag, cudaStream_t s, int part, int max_ctas) {
-    constexpr int kMaxDev = 64;
-    static int nsm_of[kMaxDev] = {};  // per device: SM count once the attributes are set
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    cudaError_t e;
+    const int nsm = device_nsm(&e);
     if (e != cudaSuccess) return e;
-    int nsm = dev < kMaxDev ? nsm_of[dev] : 0;
-    if (nsm == 0) {
-        e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step2_smem_bytes());
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_step2_plain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)step2_smem_bytes());
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_step2_plain<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)step2_smem_bytes());
-        if (e != cudaSuccess) return e;
-        if (dev < kMaxDev) nsm_of[dev] = nsm;
-    }
     int band0, nb;
-    part_range(g, fc, part, &band0, &nb);
+    part_range(g, fc, kStep2Plain, part, &band0, &nb);
     if (nb <= 0) return cudaSuccess;
     const long long total = (long long)nb * g.lx;
     const int grid = (int)std::min<long long>(max_ctas > 0 ? std::min(max_ctas, nsm) : nsm, total);
     const long long per_cta = (total + grid - 1) / grid;
+    const size_t smem = step2_smem_bytes(kStep2Plain);
     if (part == 0 && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic)
-        k_step2_plain<true><<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
-                                                                          flag);
+        k_step2_plain<true><<<grid, 2 * kT2Band, smem, s>>>(src, dst, g, mp, omega, band0, nb, per_cta, flag);
     else if (part == 0)
-        k_step2_plain<false><<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
-                                                                           flag);
+        k_step2_plain<false><<<grid, 2 * kT2Band, smem, s>>>(src, dst, g, mp, omega, band0, nb, per_cta, flag);
     else
-        k_step2<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
+        k_step2<<<grid, 2 * kT2Band, smem, s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
     return cudaGetLastError();
 }
 
 cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
                                const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]) {
-    static bool attr_set[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    cudaError_t e;
+    device_nsm(&e);
     if (e != cudaSuccess) return e;
-    if (dev >= 64 || !attr_set[dev]) {
-        e = cudaFuncSetAttribute(k_step2_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step2_smem_bytes());
-        if (e != cudaSuccess) return e;
-        if (dev < 64) attr_set[dev] = true;
-    }
     Step2Split sp{};
+    sp.form = step2_form();
     int grid = 0;
     for (int part = 0; part < 3; ++part) {
-        part_range(g, fc, part, &sp.band0[part], &sp.nb[part]);
+        part_range(g, fc, sp.form, part, &sp.band0[part], &sp.nb[part]);
         const long long total = (long long)std::max(0, sp.nb[part]) * g.lx;
         sp.ctas[part] = total > 0 ? (int)std::min<long long>(ctas[part], total) : 0;
+        if (total > 0 && sp.ctas[part] < 1) return cudaErrorInvalidValue;  // a part with items and no CTA
         sp.per_cta[part] = sp.ctas[part] ? (total + sp.ctas[part] - 1) / sp.ctas[part] : 0;
         grid += sp.ctas[part];
     }
     if (grid == 0) return cudaSuccess;
-    k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(), s>>>(src, dst, g, fc, mp, omega, sp, flag);
+    k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(sp.form), s>>>(src, dst, g, fc, mp, omega, sp, flag);
     return cudaGetLastError();
 }
 

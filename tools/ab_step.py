@@ -12,7 +12,7 @@ lib = C.CDLL(sys.argv[1])
 layout = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}[sys.argv[2] if len(sys.argv) > 2 else "caosoa"]
 vl = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 mode = sys.argv[4] if len(sys.argv) > 4 else "fused"  # fused | unfused | propagate (config 1 verb)
-variant = {"unfused": 0, "fused": 1, "propagate": 1}[mode]
+variant = {"unfused": 0, "fused": 1, "propagate": 1, "fused2": 2}[mode]
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 200
 lx = int(sys.argv[6]) if len(sys.argv) > 6 else 4096
 ly = int(sys.argv[7]) if len(sys.argv) > 7 else 16384
