@@ -46,8 +46,16 @@ enum {
 };
 
 /* LayoutKind numbering of layout.hpp:12 {AoS, SoA, CSoA, CAoSoA}; all four are
- * device layouts (the reference's element order, with a device column pitch). */
-enum { D2Q37_AOS = 0, D2Q37_SOA = 1, D2Q37_CSOA = 2, D2Q37_CAOSOA = 3 };
+ * device layouts (the reference's element order, with a device column pitch).
+ * BANDED (no reference counterpart) is the device store of the two-step sweep:
+ * per column, bands of 120 rows with the 37 populations of a band contiguous
+ * (csrc/d2q37_banded.cu).  It supports load / dump (canonical order), the
+ * device initialisers, moments, LBDUMP01 files, convert, and step() with
+ * FUSED2 (FUSED = one step per sweep) in FAST math, single domain and NCCL /
+ * group y-slabs; the padded-buffer verbs (bc, propagate, collide,
+ * read/write_padded), UNFUSED steps, STRICT math and P2P slabs return
+ * D2Q37_ERR_UNSUPPORTED.  Requires ly >= 12 (per slab). */
+enum { D2Q37_AOS = 0, D2Q37_SOA = 1, D2Q37_CSOA = 2, D2Q37_CAOSOA = 3, D2Q37_BANDED = 4 };
 
 /* Boundary condition of the y faces.  PERIODIC is the reference
  * halo_exchange (kernels.cpp:197-234); WALL is the specular top/bottom wall

@@ -44,7 +44,7 @@ HALO = 3
 COLLIDE_FLOPS_PER_SITE = 1522  # VelocityModel::kCollideFlopsPerSite (model.hpp:74-78)
 
 OK, ERR_INVALID, ERR_NON_PHYSICAL, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(6)
-LAYOUTS = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}
+LAYOUTS = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3, "banded": 4}  # banded: the FUSED2 device store
 BCS = {"periodic": 0, "wall": 1}
 VARIANTS = {"unfused": 0, "fused": 1, "fused2": 2}
 MATHS = {"fast": 0, "strict": 1}

@@ -160,9 +160,15 @@ bool clustered(int layout) { return layout == D2Q37_CSOA || layout == D2Q37_CAOS
 bool site_major(int layout) { return layout == D2Q37_AOS || layout == D2Q37_CAOSOA; }
 
 int make_geometry(int layout, int lx, int ly, int vl, DevGeo* g) {
-    if (layout < D2Q37_AOS || layout > D2Q37_CAOSOA) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown layout %d", layout);
+    if (layout < D2Q37_AOS || layout > D2Q37_BANDED) return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown layout %d", layout);
     if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");
     if (lx > 65535) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lx > 65535 not supported");
+    if (layout == D2Q37_BANDED) {
+        // halo slots hold single periodic images: 12 rows at least
+        if (ly < 4 * kHalo) return fail(D2Q37_ERR_INVALID_ARGUMENT, "banded store needs ly >= 12 (per slab)");
+        band_geometry(lx, ly, g);
+        return D2Q37_OK;
+    }
     if (!clustered(layout)) vl = 1;  // Descriptor::evl (layout.cpp:55)
     if (clustered(layout)) {
         if (!is_pow2(vl)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "vl must be a power of two");
@@ -287,7 +293,8 @@ int new_stream(d2q37_lattice* h) {
 int alloc_lattice(d2q37_lattice* h) {
     DeviceGuard dg(h->device);
     const DevGeo& g = h->g;
-    h->buf_elems = size_t(g.lead + (site_major(h->layout) ? g.px * g.cstride : kNpop * g.pstride) + 32);
+    h->buf_elems = g.band ? band_elems(g)
+                          : size_t(g.lead + (site_major(h->layout) ? g.px * g.cstride : kNpop * g.pstride) + 32);
     for (int b = 0; b < 2; ++b) {
         CK(cudaMalloc(&h->buf[b], h->buf_elems * sizeof(double)));
         CK(cudaMemset(h->buf[b], 0, h->buf_elems * sizeof(double)));  // AlignedBuffer is zeroed (layout.cpp:101)
@@ -369,6 +376,8 @@ int check_handle(const d2q37_lattice* h) {
 // The padded-buffer verbs (halo_exchange, propagate-after-halo, Field::data())
 // speak the reference's x-major element order; y-major slab storage has none.
 int padded_verbs_ok(const d2q37_lattice* h, const char* verb) {
+    if (h->g.band)
+        return fail(D2Q37_ERR_UNSUPPORTED, "%s: not available on the banded store (use FUSED2 steps / load / dump)", verb);
     if (h->g.tr)
         return fail(D2Q37_ERR_UNSUPPORTED, "%s: not available on y-major slab storage (use step / load / dump)", verb);
     return D2Q37_OK;
@@ -580,6 +589,16 @@ int propagate_launch(d2q37_lattice* h, const Offsets& off, const Faces& fc) {
 // the boundary is resolved inside the pull, no bc pass.
 int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
     const Faces fc = step_faces(h, bc);
+    if (h->g.band) {  // one step = a one-step sweep of the banded store
+        {
+            ProfScope ps(h, kProfFused);
+            CK(launch_band_sweep(h->buf[h->cur], h->buf[1 - h->cur], h->g, fc, h->mp, omega, false, h->d_flag,
+                                 h->stream));
+        }
+        h->cur = 1 - h->cur;
+        ++h->time_step;
+        return D2Q37_OK;
+    }
     const Segments all = all_sites(h->g);
     if (variant == D2Q37_FUSED) {
         RET(collide_launch(h, h->cur, 1 - h->cur, omega, true, all, 1, fc));
@@ -601,6 +620,15 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
 int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
     const double* src = h->buf[h->cur];
     double* dst = h->buf[1 - h->cur];
+    if (h->g.band) {
+        {
+            ProfScope ps(h, kProfFused);
+            CK(launch_band_sweep(src, dst, h->g, fc, h->mp, omega, true, h->d_flag, h->stream));
+        }
+        h->cur = 1 - h->cur;
+        h->time_step += 2;
+        return D2Q37_OK;
+    }
     if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
     const long long n_in = step2_items(h->g, fc, 0), n_lo = step2_items(h->g, fc, 1),
                     n_hi = step2_items(h->g, fc, 2);
@@ -1341,6 +1369,7 @@ int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
 
 int d2q37_collide(d2q37_lattice* h, double omega) {
     RET(check_handle(h));
+    if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "collide: not available on the banded store (use FUSED2 steps)");
     DeviceGuard dg(h->device);
     return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1, ghost_faces(h));
 }
@@ -1351,6 +1380,8 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
     if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
         return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    if (h->g.band && (variant == D2Q37_UNFUSED || h->math != D2Q37_MATH_FAST))
+        return fail(D2Q37_ERR_UNSUPPORTED, "banded store: FUSED2 / FUSED steps in FAST math only");
     DeviceGuard dg(h->device);
     if (h->transport == kTransportGroup) {
         d2q37_lattice** slabs = h->group.data();
@@ -1396,7 +1427,10 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
     }
     for (; s < nsteps; ++s) {
-        if (slab && h->transport == kTransportP2P) {
+        if (slab && h->g.band) {  // 6-row halos, then a one-step sweep
+            RET(step2_slab_exchange_nccl(h, bc));
+            RET(step_local(h, omega, variant, bc));
+        } else if (slab && h->transport == kTransportP2P) {
             RET(p2p_step(h, omega, variant, bc));
         } else if (slab && h->g.tr) {
             RET(variant == D2Q37_FUSED ? ymajor_step_nccl(h, omega, bc) : ymajor_step_nccl_unfused(h, omega, bc));
@@ -1547,6 +1581,7 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
     if (h) h->p2p_dirty = true;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
+    if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "fill_philox: not available on the banded store");
     DeviceGuard dg(h->device);
     CK(launch_philox(h->buf[which == 0 ? h->cur : 1 - h->cur], h->g, seed, h->y0, h->ly_global, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -1739,6 +1774,7 @@ constexpr uint32_t kP2PMagic = 0x50373344u;  // "D37P"
 
 int d2q37_create_slab_p2p(int layout, int lx, int ly, int vl, int device, int rank, int nranks,
                           d2q37_lattice** out) {
+    if (layout == D2Q37_BANDED) return fail(D2Q37_ERR_UNSUPPORTED, "p2p slabs: not available on the banded store");
     // site-major layouts slab in y-major storage (faces = contiguous columns), the others x-major
     if (!site_major(layout) && nranks > 0 && ly % nranks == 0 && !clustered(layout) && ly / nranks < 2 * kHalo)
         return fail(D2Q37_ERR_INVALID_ARGUMENT, "p2p SoA slab needs at least 6 rows per slab");
@@ -1938,6 +1974,8 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
     }
     if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
         return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    if (slabs[0]->g.band && (variant == D2Q37_UNFUSED || slabs[0]->math != D2Q37_MATH_FAST))
+        return fail(D2Q37_ERR_UNSUPPORTED, "banded store: FUSED2 / FUSED steps in FAST math only");
     DeviceGuard dg(slabs[0]->device);
     int s = 0;
     if (variant == D2Q37_FUSED2) {
@@ -1954,6 +1992,11 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
     }
     for (; s < nsteps; ++s) {
         if (nslabs == 1 || !remote_faces(slabs[0], bc)) {
+            for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
+            continue;
+        }
+        if (slabs[0]->g.band) {  // 6-row halos, then one-step sweeps
+            RET(step2_group_exchange(slabs, bc));
             for (d2q37_lattice* h : slabs) RET(step_local(h, omega, variant, bc));
             continue;
         }

@@ -37,6 +37,9 @@ struct DevGeo {
     long long pstride;  // between populations of one site: plane (SoA/CSoA) or vl (AoS/CAoSoA)
     long long rstride;  // between padded rows j of a lane: vl (SoA/CSoA) or 37*vl (AoS/CAoSoA)
     long long cstride;  // between padded columns X: pitch * rstride
+    // band-blocked store (layout D2Q37_BANDED, d2q37_banded.cu): band = 1; nbt
+    // bands of kBandRows rows
+    int band, nbt;
 };
 
 // Reference Descriptor::elem (layout.hpp:67-79) for all four layouts.

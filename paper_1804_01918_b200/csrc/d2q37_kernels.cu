@@ -750,6 +750,7 @@ cudaError_t preload_kernels() {
     load_kernel(k_scalar_propagate);
     load_kernel(k_scalar_collide<false>);
     load_kernel(k_scalar_collide<true>);
+    preload_band_kernels();
     return cudaGetLastError();
 }
 
@@ -821,6 +822,7 @@ cudaError_t launch_pack(const double* buf, const DevGeo& g, const PackParams& pp
 }
 
 cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_plane, int p, cudaStream_t s) {
+    if (g.band) return launch_band_scatter(buf, g, canon_plane, p, s);
     const long long n = (long long)g.lx * g.ly;
     (void)cudaGetLastError();
     k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf, g, canon_plane, p);
@@ -828,6 +830,7 @@ cudaError_t launch_scatter(double* buf, const DevGeo& g, const double* canon_pla
 }
 
 cudaError_t launch_gather(const double* buf, const DevGeo& g, double* canon_plane, int p, cudaStream_t s) {
+    if (g.band) return launch_band_gather(buf, g, canon_plane, p, s);
     const long long n = (long long)g.lx * g.ly;
     (void)cudaGetLastError();
     k_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(buf, g, canon_plane, p);
@@ -843,6 +846,7 @@ cudaError_t launch_philox(double* buf, const DevGeo& g, unsigned long long seed,
 
 cudaError_t launch_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, unsigned long long seed, int y0,
                            int ly_global, cudaStream_t s) {
+    if (g.band) return launch_band_init_rt(buf, g, mp, seed, y0, ly_global, s);
     (void)cudaGetLastError();
     k_init_rt<<<dim3((g.ly + 127) / 128, g.lx), 128, 0, s>>>(buf, g, mp, seed, y0, ly_global);
     return cudaGetLastError();
@@ -862,6 +866,7 @@ cudaError_t launch_scalar_step(const double* in, double* tmp, double* out, int l
 }
 
 cudaError_t launch_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s) {
+    if (g.band) return launch_band_moments(buf, g, part, s);
     (void)cudaGetLastError();
     k_moments<<<g.lx, 256, 0, s>>>(buf, g, part);
     return cudaGetLastError();

@@ -139,6 +139,26 @@ cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, 
                                const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                          double omega, int* flag, cudaStream_t s, int part, int max_ctas);
+// Band-blocked store (layout D2Q37_BANDED, d2q37_banded.cu): FUSED2 sweeps on
+// blocks of 37 populations x (kBandRows + 2 kBandHalo) rows per (column, band),
+// the halo rows kept as copies.  band_geometry fills a DevGeo (band = 1), band_elems its buffer size.
+constexpr int kBandRows = 120;
+constexpr int kBandHalo = 8;
+void band_geometry(int lx, int ly, DevGeo* g);
+size_t band_elems(const DevGeo& g);
+size_t band_smem_bytes();
+// one sweep: two steps (two = true) or one
+cudaError_t launch_band_sweep(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                              double omega, bool two, int* flag, cudaStream_t s);
+cudaError_t launch_band_scatter(double* buf, const DevGeo& g, const double* canon_plane, int p, cudaStream_t s);
+cudaError_t launch_band_gather(const double* buf, const DevGeo& g, double* canon_plane, int p, cudaStream_t s);
+cudaError_t launch_band_init_rt(double* buf, const DevGeo& g, const ModelParams& mp, unsigned long long seed, int y0,
+                                int ly_global, cudaStream_t s);
+cudaError_t launch_band_moments(const double* buf, const DevGeo& g, double* part, cudaStream_t s);
+cudaError_t launch_band_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s);
+cudaError_t launch_band_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
+                                cudaStream_t s);
+cudaError_t preload_band_kernels();
 // FUSED2 slab halos (deep SoA geometry): 6 rows per face and population,
 // buffers of halo6_count(g) doubles laid out [p][x][6].
 size_t halo6_count(const DevGeo& g);
