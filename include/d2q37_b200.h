@@ -275,13 +275,15 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
 /* FUSED2 tuning (no reference counterpart; process-wide).  form: how the
- * interior bands of a two-step sweep pull step 1 -- 1 (default) bulk copies
- * staged in shared memory (cp.async.bulk + mbarrier), 0 per-thread loads;
- * both are bit-identical.  face_pct: items per face-band CTA relative to an
- * interior CTA, in percent of the interior's cost (default 115 / 135 for
- * forms 0 / 1).  A negative argument leaves a setting unchanged; the previous
- * values are returned through prev_form / prev_face_pct when non-null.
- * Environment: D2Q37_STEP2_FORM, D2Q37_STEP2_FACE_PCT. */
+ * interior bands of a two-step sweep on the SoA store pull step 1 --
+ * 0 (default, measured fastest) per-thread loads, 1 bulk copies staged in
+ * shared memory (cp.async.bulk + mbarrier) issued after the moments, 2 the
+ * same issued as soon as the stage is in registers; all bit-identical.
+ * face_pct: items per face-band CTA relative to an interior CTA, in percent
+ * of the interior's cost (0 = the form's default: 115 / 135 for forms 0 / 1-2).
+ * A negative argument leaves a setting unchanged; the previous values are
+ * returned through prev_form / prev_face_pct when non-null.  Environment:
+ * D2Q37_STEP2_FORM, D2Q37_STEP2_FACE_PCT. */
 int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct);
 
 /* Measurement helper (no reference counterpart): the achieved FP64 rate of

@@ -351,8 +351,8 @@ def fp64_peak(device: int = 0) -> float:
 
 
 def set_fused2_tuning(form: int = -1, face_pct: int = -1) -> tuple:
-    """Process-wide FUSED2 tuning (d2q37_set_fused2_tuning): ``form`` 1 = interior bands staged by bulk
-    copies (default), 0 = per-thread loads (bit-identical); ``face_pct`` sizes the face-band CTA
+    """Process-wide FUSED2 tuning (d2q37_set_fused2_tuning): ``form`` 0 = per-thread loads (default),
+    1 / 2 = interior bands staged by bulk copies (bit-identical); ``face_pct`` sizes the face-band CTA
     groups (0 = the form's default).  -1 leaves a setting unchanged.  Returns the previous
     (form, face_pct)."""
     pf, pp = C.c_int(0), C.c_int(0)

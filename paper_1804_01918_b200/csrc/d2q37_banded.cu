@@ -118,6 +118,19 @@ __constant__ signed char c_slot[kNpop] = {
     slot_of(24), slot_of(25), slot_of(26), slot_of(27), slot_of(28), slot_of(29), slot_of(30), slot_of(31),
     slot_of(32), slot_of(33), slot_of(34), slot_of(35), slot_of(36)};
 __device__ __forceinline__ int slot_of_rt(int p) { return c_slot[p]; }
+// cx of the population in storage slot s
+D2Q37_HD constexpr int cx_of_slot(int s) {
+    for (int p = 0; p < kNpop; ++p)
+        if (slot_of(p) == s) return cx_of(p);
+    return 0;
+}
+__constant__ signed char c_cx_slot[kNpop] = {
+    cx_of_slot(0),  cx_of_slot(1),  cx_of_slot(2),  cx_of_slot(3),  cx_of_slot(4),  cx_of_slot(5),  cx_of_slot(6),
+    cx_of_slot(7),  cx_of_slot(8),  cx_of_slot(9),  cx_of_slot(10), cx_of_slot(11), cx_of_slot(12), cx_of_slot(13),
+    cx_of_slot(14), cx_of_slot(15), cx_of_slot(16), cx_of_slot(17), cx_of_slot(18), cx_of_slot(19), cx_of_slot(20),
+    cx_of_slot(21), cx_of_slot(22), cx_of_slot(23), cx_of_slot(24), cx_of_slot(25), cx_of_slot(26), cx_of_slot(27),
+    cx_of_slot(28), cx_of_slot(29), cx_of_slot(30), cx_of_slot(31), cx_of_slot(32), cx_of_slot(33), cx_of_slot(34),
+    cx_of_slot(35), cx_of_slot(36)};
 
 }  // namespace
 
@@ -137,6 +150,11 @@ D2Q37_HD constexpr int b2_base(int p) {
     return s;
 }
 constexpr int kB2RingCols = b2_base(kNpop);  // 148
+// timing probes (tools/gpu_g8.sh; results are garbage): 1 / 2 / 3 no consumer / producer / any collide,
+// 4 no stores, 5 no bulk copies, 6 one copy per population instead of per cx group
+#ifndef D2Q37_BAND_PROBE
+#define D2Q37_BAND_PROBE 0
+#endif
 constexpr int kBandStages = 2;
 
 // named barriers (256 threads): 2 = consumers -> producers "this iteration's ring slots are read",
@@ -164,12 +182,23 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+#if D2Q37_BAND_PROBE == 6 || D2Q37_BAND_PROBE == 7
+    // probe: one copy per population (slot 10 w + lane), block rows 2 .. 135
+    const int isl = 10 * warp + lane;
+    const bool issuer = prod && lane < 10 && isl < kNpop;
+    const int gs = issuer ? isl : 0;
+    const unsigned ibytes = unsigned((kBS - 2) * sizeof(double));
+    const int icx = issuer ? c_cx_slot[isl] : 0;
+    constexpr int kIoff = 2;
+#else
     // copy issue: producer warp w, lanes 0-1 -> cx group 2 w + lane (7 groups, one contiguous run each)
     const int igr = 2 * warp + lane;
     const bool issuer = prod && lane < 2 && igr < 2 * kHalo + 1;
     const int gs = issuer ? c_gstart[igr] : 0, gn = issuer ? c_gstart[igr + 1] - gs : 0;
     const unsigned ibytes = unsigned(gn * kBS * sizeof(double));
     const int icx = igr - kHalo;
+    constexpr int kIoff = 0;
+#endif
     unsigned issued = 0, used = 0;  // stage columns issued / consumed by this CTA (stage = n % 2)
     bool bad = false;
     while (item < item_end) {
@@ -185,12 +214,15 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
         if (prod) {
             auto issue = [&](int r) {  // stage the column of producer row r
                 const unsigned st = issued % kBandStages;
-                if (issuer) {
+                if (issuer && D2Q37_BAND_PROBE != 5) {
                     const int col = wrap_mod(wrap_mod(r, lx) - icx, lx);
-                    bulk_g2s(stage0 + st * kBlk + gs * kBS, src + g.lead + ((long long)col * nbt + band) * kBlk + gs * kBS,
-                             ibytes, full + st);
+                    bulk_g2s(stage0 + st * kBlk + gs * kBS + kIoff,
+                             src + g.lead + ((long long)col * nbt + band) * kBlk + gs * kBS + kIoff, ibytes, full + st);
                 }
-                if (threadIdx.x == 0) mbar_arrive_expect_tx(full + st, kBandStageBytes);
+                if (threadIdx.x == 0 && D2Q37_BAND_PROBE != 5)
+                    mbar_arrive_expect_tx(full + st, D2Q37_BAND_PROBE == 6 || D2Q37_BAND_PROBE == 7
+                                                         ? unsigned(kNpop * (kBS - 2) * sizeof(double))
+                                                         : kBandStageBytes);
                 ++issued;
             };
             for (int k = 0; k < kBandStages && k < niter - 1; ++k) issue(xs - kHalo + k);
@@ -204,7 +236,7 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
 #pragma unroll 1
             for (int t = 0; t < niter - 1; ++t) {
                 const unsigned st = used % kBandStages;
-                mbar_wait(full + st, (used / kBandStages) & 1);
+                if (D2Q37_BAND_PROBE != 5) mbar_wait(full + st, (used / kBandStages) & 1);  // probe 5: no copies
                 ++used;
                 const double* const sg = stage0 + st * kBlk;
                 double f[kNpop];
@@ -243,7 +275,8 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                     prod_bar_sync();
                     issue(xs - kHalo + t + kBandStages);
                 }
-                bad |= collide_site_sym(f, omega, mp);
+                if (D2Q37_BAND_PROBE != 2 && D2Q37_BAND_PROBE != 3 && D2Q37_BAND_PROBE != 7)
+                    bad |= collide_site_sym(f, omega, mp);  // probes 2, 3: no producer collide
                 nb_sync(2);  // the consumers have read this iteration's slots
                 for_pops([&](auto P) {
                     constexpr int p = decltype(P)::value, rb = b2_base(p), dp = b2_depth(p);
@@ -307,8 +340,10 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                 }
                 nb_arrive(2);
                 if (work) {
-                    if (TWO) bad |= collide_site_sym(v, omega, mp);
+                    if (TWO && D2Q37_BAND_PROBE != 1 && D2Q37_BAND_PROBE != 3 && D2Q37_BAND_PROBE != 7)
+                        bad |= collide_site_sym(v, omega, mp);  // probes 1, 3: no consumer collide
                     double* __restrict__ o = dst + band_base(g, c, band, tid);
+                    if (D2Q37_BAND_PROBE == 4) continue;  // probe 4: no stores
                     for_pops([&](auto P) {
                         constexpr int p = decltype(P)::value;
                         __stcs(o + slot_of(p) * kBS, v[p]);

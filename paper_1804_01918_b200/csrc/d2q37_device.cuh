@@ -264,7 +264,31 @@ struct SymMoments {
     double mom[kNmom];
 };
 
+#ifndef D2Q37_SPLIT_MOMENTS
+#define D2Q37_SPLIT_MOMENTS 0
+#endif
 __device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const ModelParams& mp, SymMoments& m) {
+#if D2Q37_SPLIT_MOMENTS
+    // four interleaved partial sums per moment: 10-deep dependency chains instead of 37
+    double r4[4] = {0.0, 0.0, 0.0, 0.0}, x4[4] = {0.0, 0.0, 0.0, 0.0}, y4[4] = {0.0, 0.0, 0.0, 0.0},
+           e4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i) r4[i & 3] += f[i];
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cx_of(i) != 0) x4[i & 3] = fma((double)cx_of(i), f[i], x4[i & 3]);
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cy_of(i) != 0) y4[i & 3] = fma((double)cy_of(i), f[i], y4[i & 3]);
+#pragma unroll
+    for (int i = 0; i < kNpop; ++i)
+        if (cx_of(i) != 0 || cy_of(i) != 0)
+            e4[i & 3] = fma((double)(cx_of(i) * cx_of(i) + cy_of(i) * cy_of(i)), f[i], e4[i & 3]);
+    const double rho = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+    const bool bad = !(rho > 0.0);
+    const double jx = (x4[0] + x4[1]) + (x4[2] + x4[3]), jy = (y4[0] + y4[1]) + (y4[2] + y4[3]);
+    const double e2 = (e4[0] + e4[1]) + (e4[2] + e4[3]);
+#else
     double rho = 0.0;
 #pragma unroll
     for (int i = 0; i < kNpop; ++i) rho += f[i];
@@ -280,6 +304,7 @@ __device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const Mode
     for (int i = 0; i < kNpop; ++i)
         if (cx_of(i) != 0 || cy_of(i) != 0)
             e2 = fma((double)(cx_of(i) * cx_of(i) + cy_of(i) * cy_of(i)), f[i], e2);
+#endif
     const double inv_rho = 1.0 / rho;
     const double ux = jx * inv_rho;
     const double uy = jy * inv_rho;

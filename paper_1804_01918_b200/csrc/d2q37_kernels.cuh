@@ -121,10 +121,10 @@ bool step2_supported(const DevGeo& g, const Faces& fc);
 // step2_items = its (band, column) items; at most max_ctas persistent CTAs
 // (0: one per SM).
 long long step2_items(const DevGeo& g, const Faces& fc, int part);
-// Interior-band code form of a FUSED2 sweep: per-thread pulls (sweep_plain) or
-// bulk copies staged in shared memory (sweep_tma).  Default: bulk; environment
-// D2Q37_STEP2_FORM=0 selects the per-thread form.  set_step2_form returns the
-// previous form.
+// Interior-band code form of a FUSED2 sweep: per-thread pulls (sweep_plain, the
+// default: measured fastest) or bulk copies staged in shared memory (sweep_tma;
+// 1 = issued after the moments, 2 = as soon as the stage is in registers).
+// Environment D2Q37_STEP2_FORM selects one.  set_step2_form returns the previous form.
 enum { kStep2Plain = 0, kStep2Bulk = 1, kStep2BulkEarly = 2 };
 int step2_form();
 int set_step2_form(int form);

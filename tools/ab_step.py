@@ -9,7 +9,7 @@ import threading
 import time
 
 lib = C.CDLL(sys.argv[1])
-layout = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3}[sys.argv[2] if len(sys.argv) > 2 else "caosoa"]
+layout = {"aos": 0, "soa": 1, "csoa": 2, "caosoa": 3, "banded": 4}[sys.argv[2] if len(sys.argv) > 2 else "caosoa"]
 vl = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 mode = sys.argv[4] if len(sys.argv) > 4 else "fused"  # fused | unfused | propagate (config 1 verb)
 variant = {"unfused": 0, "fused": 1, "propagate": 1, "fused2": 2}[mode]

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 #define CK(x)                                                                              \
@@ -25,16 +26,22 @@
         }                                                                                  \
     } while (0)
 
-constexpr int kNpop = 37, kBand = 128, kRows = 130;
+constexpr int kNpop = 37, kBand = 128, kRows = 136;
 __constant__ signed char c_cx[kNpop] = {0, -1, 0, 0, 1, -1, -1, 1, 1, -2, 0, 0, 2, -2, -2, -1, -1, 1, 1,
                                         2, 2, -2, -2, 2, 2, -3, 0, 0, 3, -3, -3, -1, -1, 1, 1, 3, 3};
 __constant__ signed char c_cy[kNpop] = {0, 0, -1, 1, 0, -1, 1, -1, 1, 0, -2, 2, 0, -1, 1, -2, 2, -2, 2,
                                         -1, 1, -2, 2, -2, 2, 0, -3, 3, 0, -1, 1, -3, 3, -3, 3, -1, 1};
 
 __device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__constant__ int c_gs[8] = {0, 3, 8, 15, 22, 29, 34, 37};
 
 // MODE 0: SoA planes (the library's FUSED2 store): element (p, x, y) at p*plane + x*cs + y.
 // MODE 2: SoA reads, band-blocked writes.  MODE 3: band-blocked reads, SoA writes.
+// MODE 8: exact 120-row blocks plus separate halo arrays LO/HI[x][b][s][8] (contiguous per column):
+//         21 copies per column (main, lo, hi of each cx group), halo copies written as contiguous runs.
+// MODE 5: MODE 4 without the halo copies.  MODE 6: MODE 4 reads, MODE 1 writes.
+// MODE 4: the library's banded store (csrc/d2q37_banded.cu): blocks of 37 x 136 rows, 7 copies per
+//         column (one per cx group), writes of the 120 own rows plus 8-row halo copies.
 // MODE 1: band-blocked: element (p, x, y) of band b at ((x*nb + b)*37 + p)*kOut + y - y0 -- one
 //         column's 37 populations x kOut rows contiguous (reads approximate: each population's
 //         1040 B taken from inside its own block).
@@ -49,9 +56,12 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
     if (threadIdx.x < NST) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + threadIdx.x)));
     asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    const int ip = warp * 10 + lane;
-    const bool issuer = prod && lane < 10 && ip < kNpop;
-    const int icx = issuer ? c_cx[ip] : 0, icy = issuer ? c_cy[ip] : 0;
+    const int ip = MODE == 8 ? lane : (MODE >= 4) ? 2 * warp + lane : warp * 10 + lane;
+    const bool issuer = MODE == 8 ? (prod && warp < 3 && lane < 7)
+                                  : (MODE >= 4) ? (prod && lane < 2 && ip < 7) : (prod && lane < 10 && ip < kNpop);
+    const long long hsz = (long long)(lx + 8) * nbands * kNpop * 8;  // one halo array (doubles)
+    const long long mainsz = (long long)(lx + 8) * nbands * kNpop * 120;
+    const int icx = (MODE >= 4) ? ip - 3 : (issuer ? c_cx[ip] : 0), icy = (MODE >= 4) ? 0 : (issuer ? c_cy[ip] : 0);
     long long item = (long long)blockIdx.x * per_cta;
     const long long end = min((long long)nbands * lx, item + per_cta);
     unsigned ph[NST > 0 ? NST : 1] = {};
@@ -67,7 +77,28 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
         auto wr = [&](int v) { return v < 0 ? v + lx : (v >= lx ? v - lx : v); };
         auto issue = [&](int t) {
             const int st = issued % NST;
-            if (issuer) {
+            if (issuer && MODE == 8) {
+                const int col = wr(wr(xs - 3 + t) - icx);
+                const int gs = c_gs[ip], gn = c_gs[ip + 1] - gs;
+                const long long blk = (long long)col * nbands + band;
+                const double* s = warp == 0 ? src + (blk * kNpop + gs) * 120
+                                            : src + mainsz + (warp - 1) * hsz + (blk * kNpop + gs) * 8;
+                double* d = sm + st * kNpop * kRows + (warp == 0 ? gs * 120 : kNpop * 120 + (warp - 1) * kNpop * 8 + gs * 8);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sa(d)),
+                    "l"(s), "r"(gn * (warp == 0 ? 120 : 8) * 8), "r"(sa(bar + st))
+                    : "memory");
+            } else if (issuer && MODE >= 4) {
+                const int col = wr(wr(xs - 3 + t) - icx);
+                const int gs = c_gs[ip], gn = c_gs[ip + 1] - gs;
+                const double* s = src + (((long long)col * nbands + band) * kNpop + gs) * 136;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sa(sm + st * kNpop * kRows + gs * 136)),
+                    "l"(s), "r"(gn * 136 * 8), "r"(sa(bar + st))
+                    : "memory");
+            } else if (issuer) {
                 const int col = wr(wr(xs - 3 + t) - icx);
                 const double* s = (MODE == 0 || MODE == 2) ? src + ip * plane + col * cs + ((y0 + 3 - icy) & ~1)
                                             : src + (((long long)col * nbands + band) * kNpop + ip) * kOut;
@@ -79,7 +110,7 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
             }
             if (threadIdx.x == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar + st)),
-                             "r"(kNpop * kRows * 8)
+                             "r"((MODE >= 4) ? kNpop * 136 * 8 : kNpop * kRows * 8)
                              : "memory");
             ++issued;
         };
@@ -109,6 +140,26 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
                     double* o = dst + (long long)(xs - 7 + t) * cs + y0 + (kOut == 120 ? 4 : 6) + tid;
 #pragma unroll
                     for (int p = 0; p < kNpop; ++p) __stcs(o + p * plane, acc + p);
+                } else if (MODE == 8) {
+                    const long long blk = (long long)(xs - 7 + t) * nbands + band;
+                    double* o = dst + blk * kNpop * 120 + tid;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(o + p * 120, acc + p);
+                    if ((tid < 8 && band > 0) || (tid >= 112 && band + 1 < nbands)) {
+                        double* oo = tid < 8 ? dst + mainsz + hsz + ((blk - 1) * kNpop) * 8 + tid
+                                             : dst + mainsz + ((blk + 1) * kNpop) * 8 + tid - 112;
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) __stcs(oo + p * 8, acc + p);
+                    }
+                } else if (MODE == 4 || MODE == 5) {  // 5: no halo copies
+                    double* o = dst + ((long long)(xs - 7 + t) * nbands + band) * kNpop * 136 + 8 + tid;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(o + p * 136, acc + p);
+                    if (MODE == 4 && ((tid < 8 && band > 0) || (tid >= 112 && band + 1 < nbands))) {
+                        double* oo = o + (tid < 8 ? -kNpop * 136 + 120 : kNpop * 136 - 120);
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) __stcs(oo + p * 136, acc + p);
+                    }
                 } else {
                     double* o = dst + ((long long)(xs - 7 + t) * nbands + band) * kNpop * kOut + tid;
 #pragma unroll
@@ -128,7 +179,7 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
 int main(int argc, char** argv) {
     const int lx = argc > 1 ? atoi(argv[1]) : 4096, ly = argc > 2 ? atoi(argv[2]) : 16384;
     const long long cs = ly + 12 + 128, plane = (long long)(lx + 8) * cs;  // padded like the lattice
-    const size_t bytes = (size_t)plane * kNpop * 8;
+    const size_t bytes = std::max((size_t)plane * kNpop * 8, (size_t)(lx + 8) * (ly / 120 + 2) * kNpop * 136 * 8);
     double *a, *b;
     CK(cudaMalloc(&a, bytes));
     CK(cudaMalloc(&b, bytes));
@@ -166,14 +217,10 @@ int main(int argc, char** argv) {
                100.0 * w / (double)nsm / ((double)best * 1e-3 * 1.9e9));
     };
     for (int delay : {0}) {
-        run(k_mem<2, 0, 122>, 2, delay, 122, 0);
-        run(k_mem<2, 0, 120>, 2, delay, 120, 0);
         run(k_mem<2, 1, 120>, 2, delay, 120, 1);
-        run(k_mem<2, 2, 120>, 2, delay, 120, 2);
-        run(k_mem<2, 3, 120>, 2, delay, 120, 3);
-        run(k_mem<1, 2, 120>, 1, delay, 120, 2);
-        run(k_mem<1, 3, 120>, 1, delay, 120, 3);
-        run(k_mem<2, 2, 122>, 2, delay, 122, 2);
+        run(k_mem<2, 4, 120>, 2, delay, 120, 4);
+        run(k_mem<2, 8, 120>, 2, delay, 120, 8);
+        run(k_mem<1, 8, 120>, 1, delay, 120, 8);
     }
     return 0;
 }
