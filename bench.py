@@ -127,7 +127,7 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.backend = backend or os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        self.backend = backend or os.environ.get("BENCH_DIST_BACKEND", "gloo" if STUB else "nccl")
         self.pg = False
         if self.world > 1:
             import torch
@@ -187,6 +187,68 @@ class Dist:
             dist.destroy_process_group()
 
 
+# --------------------------------------------------------------------------- stub backend (host-logic tests)
+
+STUB = False  # --stub: a no-op lattice timed on the host, gloo collectives (tests/test_bench_launch.py)
+
+
+class _StubSim:
+    """Stands in for paper_1804_01918_b200.Simulation in --stub runs: every verb is a no-op, a step
+    sleeps 50 microseconds so the timing path has something to measure."""
+
+    host_timed = True
+    stream = 0
+
+    def __init__(self, layout, lx, ly, vl=1, *, variant="fused2", **_):
+        self.layout, self.lx, self.ly, self.vl, self.variant = layout, lx, ly, vl, variant
+        self._launches = 0
+
+    def init_rt_device(self, seed):
+        pass
+
+    def step(self, omega, n=1, sync=True, **_):
+        time.sleep(5e-5 * n)
+        self._launches += max(1, n // 2)
+
+    def sync(self):
+        pass
+
+    def set_profiling(self, on=True):
+        pass
+
+    def kernel_times(self):
+        n, self._launches = self._launches, 0
+        return {"edge": (0.0, 0), "propagate": (0.0, 0), "collide": (0.0, 0), "fused": (0.1 * n, n),
+                "pack": (0.0, 0), "boundary": (0.0, 0)}
+
+    def exposed_halo_ms(self):
+        return 0.0
+
+    def close(self):
+        pass
+
+
+class _StubLbm:
+    class Simulation(_StubSim):
+        @classmethod
+        def slab(cls, layout, lx, ly_global, vl=1, *, rank=0, nranks=1, **kw):
+            return cls(layout, lx, ly_global // nranks, vl, **kw)
+
+    @staticmethod
+    def nccl_unique_id():
+        return b"stub"
+
+    @staticmethod
+    def fp64_peak(dev):
+        raise RuntimeError("stub")
+
+
+def cuda_sync():
+    if not STUB:
+        import torch
+        torch.cuda.synchronize()
+
+
 # --------------------------------------------------------------------------- GPU helpers
 
 def cuda_events():
@@ -209,6 +271,11 @@ def time_stepping(sim, steps: int, variant: str) -> float:
 
 def time_steps(sim, steps: int, fn) -> float:
     """Device time (ms) of `steps` calls of fn on the lattice stream (CUDA events)."""
+    if getattr(sim, "host_timed", False):  # --stub
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        return 1e3 * (time.perf_counter() - t0)
     import torch
     s = torch.cuda.ExternalStream(sim.stream)
     a, b = cuda_events()
@@ -474,6 +541,28 @@ def bench_variant(lbm, ly, layout, vl, variant, warmup, steps, hbm_peak: float =
 
 # --------------------------------------------------------------------------- CPU baseline / reference arm
 
+def physical_cores():
+    """Physical cores of this host (psutil, else /proc/cpuinfo core ids), for the cpu_baseline record."""
+    try:
+        import psutil
+        n = psutil.cpu_count(logical=False)
+        if n:
+            return int(n)
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        cores, phys = set(), None
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("physical id"):
+                    phys = ln.split(":")[1].strip()
+                elif ln.startswith("core id"):
+                    cores.add((phys, ln.split(":")[1].strip()))
+        return len(cores) or None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def reference_step_rate(lx=LX, ly=1024, iterations=3, warmup=1, workers=None):
     """The unmodified reference step (oracle/_ref) on a bounded sample of the lattice."""
     from oracle import pyoracle as po
@@ -512,6 +601,7 @@ def run_reference(args, dist):
             "config": {"workload": f"c3/c4-weak sample: {lx}x{ly} (RT init, omega {OMEGA})", "lx": lx,
                        "ly_sample": ly, "layout": "aos", "workers": workers},
             "cpu_baseline": {"value": value, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                             "hardware_threads": os.cpu_count(), "physical_cores": physical_cores(),
                              "sample": sample},
             "e2e": {"value": value, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "step_ms_median": 1e3 * statistics.median(times)}
@@ -565,37 +655,28 @@ def make_slab(lbm, args, dist: Dist, dev: int, ly_global: int):
     return sim, "nccl"
 
 
-def run_b200(args, dist: Dist):
-    import torch
-    import paper_1804_01918_b200 as lbm
-
-    dev = dist.local
-    torch.cuda.set_device(dev)
-    hbm_peak, peak_src = peaks()
-    n = dist.world
-    # weak (default): 4096 x 16384 per GPU; strong: BASELINE config 4's 4096 x 32768 split over N
-    ly_local = args.ly if args.scaling == "weak" else STRONG_LY // dist.world
+def measure(lbm, args, dist: Dist, scaling: str) -> dict:
+    """This rank's lattice for `scaling` (weak: --ly rows per GPU; strong: BASELINE config 4's
+    4096 x 32768 split over the ranks), `--warmup` untimed steps, then exactly `--steps` timed
+    steps between a barrier and a device sync on both sides; max over ranks."""
+    n, dev = dist.world, dist.local
+    ly_local = args.ly if scaling == "weak" else STRONG_LY // n
     ly_global = ly_local * n
-    sites_local = LX * ly_local
-    rank = dist.rank
-
-    # ---- lattice + init: each rank generates its slab of the RT state on the device
     transport = None
     if n == 1:
         sim = lbm.Simulation(args.layout, LX, ly_local, args.vl, device=dev, bc="wall", variant=args.variant)
     else:
         sim, transport = make_slab(lbm, args, dist, dev, ly_global)
-    sim.init_rt_device(SEED)
-
+    sim.init_rt_device(SEED)  # each rank generates its slab of the global RT state on the device
     clocks = ClockSampler(dev)
     clocks.start()
     sim.step(OMEGA, args.warmup)
     sim.set_profiling(True)
     sim.kernel_times()
     dist.barrier()
-    torch.cuda.synchronize()
+    cuda_sync()
     ms = time_stepping(sim, args.steps, args.variant)
-    torch.cuda.synchronize()
+    cuda_sync()
     dist.barrier()
     kt = sim.kernel_times()
     sim.set_profiling(False)
@@ -604,7 +685,45 @@ def run_b200(args, dist: Dist):
     if n > 1 and args.variant == "fused2":
         halo_ms /= 2  # one 6-row exchange per two-step sweep
     ms_max = dist.max(ms)
-    value = n * sites_local * args.steps / (ms_max / 1e3) / 1e6
+    return {"sim": sim, "transport": transport, "ly_local": ly_local, "ly_global": ly_global, "ms_max": ms_max,
+            "value": n * LX * ly_local * args.steps / (ms_max / 1e3) / 1e6, "kt": kt, "clk": clk,
+            "halo_ms": halo_ms}
+
+
+def single_gpu_rate(lbm, args, dist: Dist, ly: int):
+    """Rank 0 alone, after the multi-GPU runs: the single-domain lattice of `ly` rows -- the 1-GPU
+    point the N-GPU value is compared with (the other ranks wait at the barrier)."""
+    val = None
+    if dist.rank == 0:
+        sim = lbm.Simulation(args.layout, LX, ly, args.vl, device=dist.local, bc="wall", variant=args.variant)
+        sim.init_rt_device(SEED)
+        sim.step(OMEGA, args.warmup)
+        cuda_sync()
+        ms = time_stepping(sim, args.steps, args.variant)
+        cuda_sync()
+        sim.close()
+        val = LX * ly * args.steps / (ms / 1e3) / 1e6
+    dist.barrier()
+    return val
+
+
+def run_b200(args, dist: Dist):
+    if STUB:
+        lbm = _StubLbm()
+    else:
+        import torch
+
+        import paper_1804_01918_b200 as lbm
+        torch.cuda.set_device(dist.local)
+    dev = dist.local
+    hbm_peak, peak_src = peaks()
+    n = dist.world
+    rank = dist.rank
+    main = measure(lbm, args, dist, args.scaling)
+    sim, transport, kt, clk = main["sim"], main["transport"], main["kt"], main["clk"]
+    ly_local, ly_global, ms_max, value, halo_ms = (main["ly_local"], main["ly_global"], main["ms_max"],
+                                                   main["value"], main["halo_ms"])
+    sites_local = LX * ly_local
     launches = sum(c for _, c in kt.values())
     if transport == "p2p":  # + the one-thread step-counter wait and signal kernels of every step
         launches += 2 * args.steps
@@ -642,11 +761,11 @@ def run_b200(args, dist: Dist):
 
     # ---- e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not STUB:
         e2e = run_e2e(lbm, sim, args, dist)
 
     try:  # after the timed region: the FP64 denominator at the clocks this GPU holds under load
-        fp64_meas = lbm.fp64_peak(dev)
+        fp64_meas = None if STUB else lbm.fp64_peak(dev)
     except Exception:  # noqa: BLE001
         fp64_meas = None
     if fp64_meas and roofline.get("fp64_tflops_reference_count"):
@@ -664,10 +783,35 @@ def run_b200(args, dist: Dist):
                        "halo_transport": transport},
             "roofline": roofline, "gpu_launches": launches, "clocks": clk, "e2e": e2e,
             "exposed_halo_ms_per_step": halo_ms}
+    if STUB:
+        line["stub"] = "host-logic run: no-op lattice, host timers, gloo (not a measurement)"
+    sim.close()
+    del sim, main
 
-    if n == 1 and not args.no_extras:
-        sim.close()
-        del sim
+    # ---- the other BASELINE config-4 scaling mode, same ranks (weak <-> strong)
+    if not args.no_other_scaling:
+        other = "strong" if args.scaling == "weak" else "weak"
+        o = measure(lbm, args, dist, other)
+        o["sim"].close()
+        line[f"scaling_{other}"] = {
+            "value": o["value"], "unit": "MLUPS", "n_gpus": n, "ms_per_step": o["ms_max"] / args.steps,
+            "exposed_halo_ms_per_step": o["halo_ms"], "clocks": o["clk"], "halo_transport": o["transport"],
+            "config": f"c4-{other}: {LX}x{o['ly_local']} per GPU (global {LX}x{o['ly_global']})"}
+        del o
+    # ---- the 1-GPU points (rank 0 alone), for the scaling efficiency of this run
+    if n > 1 and not args.no_single:
+        one_weak = single_gpu_rate(lbm, args, dist, args.ly)
+        one_strong = single_gpu_rate(lbm, args, dist, STRONG_LY)
+        ones = {"weak": one_weak, "strong": one_strong}
+        line["single_gpu_mlups"] = ones
+        if rank == 0:  # whole-job MLUPS / (N x the 1-GPU MLUPS of the same lattice per GPU / in total)
+            eff = {args.scaling: value / (n * ones[args.scaling])}
+            other = "strong" if args.scaling == "weak" else "weak"
+            if f"scaling_{other}" in line:
+                eff[other] = line[f"scaling_{other}"]["value"] / (n * ones[other])
+            line["efficiency_vs_1gpu_same_run"] = eff
+
+    if n == 1 and not args.no_extras and not STUB:
         kernels = {}
         for lay, vl in (("soa", 1), ("csoa", 32), ("caosoa", 32), ("aos", 1)):
             tag = f"{lay}{vl if vl > 1 else ''}"
@@ -680,6 +824,21 @@ def run_b200(args, dist: Dist):
                     v["frac_of_fp64_measured"] = v["GFLOP_per_s"] / (fp64_meas * 1e3)
             kernels["fp64_peak_measured_tflops"] = fp64_meas
         line["kernels"] = kernels
+        # the other two BASELINE metrics, in the roofline record itself (propagate GB/s on config 1,
+        # collide FP64 GFLOP/s on config 2 with the reference FLOP count), SoA and CAoSoA32
+        roofline["propagate_c1"] = {
+            tag: {"GB_per_s": kernels[f"propagate_c1_{tag}"]["GB_per_s"],
+                  "frac_of_hbm": kernels[f"propagate_c1_{tag}"]["frac_of_hbm"], "unit": "GB/s",
+                  "bytes_per_site": BYTES_PER_SITE}
+            for tag in ("soa", "caosoa32")}
+        roofline["collide_c2"] = {
+            tag: {"GFLOP_per_s": kernels[f"collide_c2_{tag}"]["GFLOP_per_s"],
+                  "frac_of_fp64_nominal": kernels[f"collide_c2_{tag}"]["frac_of_fp64_nominal"],
+                  "frac_of_fp64_measured": kernels[f"collide_c2_{tag}"].get("frac_of_fp64_measured"),
+                  "frac_of_attainable": kernels[f"collide_c2_{tag}"]["frac_of_attainable"],
+                  "frac_of_hbm": kernels[f"collide_c2_{tag}"]["frac_of_hbm"],
+                  "flop_per_site": FLOPS_PER_SITE, "unit": "GFLOP/s"}
+            for tag in ("soa", "caosoa32")}
         variants = {}
         for lay, vl, var in (("soa", 1, "fused2"), ("soa", 1, "fused"), ("soa", 1, "unfused"), ("csoa", 32, "fused"),
                              ("csoa", 32, "unfused"), ("aos", 1, "fused"), ("caosoa", 32, "fused"),
@@ -706,15 +865,17 @@ def run_b200(args, dist: Dist):
                 "weak_slab": bench_slab_schedule(lbm, "caosoa", 32, LY_PER_GPU, 3, 20)}
         except Exception as e:  # NCCL unavailable must not sink the line
             line["slab_schedule"] = {"error": str(e)}
-        try:
-            line["p2p_ring_emulation"] = bench_p2p_ring_emulation(lbm, "caosoa", 32, 8, 3, 20)
-        except Exception as e:  # noqa: BLE001
-            line["p2p_ring_emulation"] = {"error": str(e)}
-    if n == 1 and not args.no_cpu:
+        if args.p2p_extras:  # slabs on one GPU waiting on each other's counters: not on the default path
+            try:
+                line["p2p_ring_emulation"] = bench_p2p_ring_emulation(lbm, "caosoa", 32, 8, 3, 20)
+            except Exception as e:  # noqa: BLE001
+                line["p2p_ring_emulation"] = {"error": str(e)}
+    if n == 1 and not args.no_cpu and not STUB:
         try:
             v, med, workers = reference_step_rate()
             line["cpu_baseline"] = {
                 "value": v, "unit": "MLUPS", "cores": workers, "kind": "reference",
+                "hardware_threads": os.cpu_count(), "physical_cores": physical_cores(),
                 "sample": f"{LX}x1024 rows of the {LX}x{LY_PER_GPU} lattice, unmodified reference step "
                           f"(oracle/_ref, AoS, periodic halo_exchange + propagate + collide), median of 3 steps"}
         except Exception as e:  # the CPU baseline must not sink the GPU line
@@ -775,6 +936,30 @@ def load_ncu_traffic(layout: str, ly: int, variant: str = "fused"):
     return rec["dram_bytes_per_launch"] * (LX * ly) / (4096 * 16384)
 
 
+def launch_ranks(args):
+    """`--gpus N` without a launcher: start N ranks (one per GPU) through torch.distributed.run on
+    127.0.0.1 and exit with their status.  Fails loudly -- never a silent 1-GPU line -- when this
+    host has fewer than N GPUs."""
+    import socket
+    if not STUB:
+        try:
+            import torch
+            have = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            have = 0
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but this host has {have} CUDA device(s)")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -796,6 +981,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-other-scaling", action="store_true",
+                    help="skip the second config-4 measurement (strong when --scaling weak and vice versa)")
+    ap.add_argument("--no-single", action="store_true", help="N > 1: skip the 1-GPU points of the efficiency")
+    ap.add_argument("--p2p-extras", action="store_true",
+                    help="also run the 8-slab P2P ring emulation on one GPU (slabs spin on each other)")
+    ap.add_argument("--stub", action="store_true",
+                    help="host-logic test mode: no-op lattice, host timers, gloo (tests/test_bench_launch.py)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: at least 3 warm-up steps
     multi = int(os.environ.get("WORLD_SIZE", "1")) > 1
@@ -806,11 +998,18 @@ def main():
     if args.variant is None:
         args.variant = "fused2"
     del multi
+    global STUB
+    STUB = args.stub
     if args.impl == "reference":
         # rank 0 alone runs the CPU reference; other ranks exit 0 without work
         if int(os.environ.get("RANK", "0")) == 0:
             run_reference(args, None)
         return
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        launch_ranks(args)  # re-executes this script as args.gpus ranks; does not return
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report a mismatched run")
     dist = Dist()
     try:
         run_b200(args, dist)
