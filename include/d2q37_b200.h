@@ -224,7 +224,8 @@ int d2q37_create_slab(int layout, int lx, int ly, int vl, int device, int rank, 
  * as the NCCL path; used to prove slab invariance on a single GPU. */
 int d2q37_create_group(int layout, int lx, int ly, int vl, int device, int nslabs,
                        d2q37_lattice** out);
-/* step for every slab of a group created by d2q37_create_group. */
+/* step for every slab of a group created by d2q37_create_group; blocks until
+ * every slab is done and reports a NonPhysicalError raised in any slab. */
 int d2q37_group_step(d2q37_lattice** slabs, int nslabs, double omega, int nsteps, int variant, int bc);
 /* The halo message layout: entry i of send_lo / recv_hi is (distance d, population p)
  * = (lo_d[i], lo_p[i]) with cy_p <= -d (the low neighbour's high ghost row d),

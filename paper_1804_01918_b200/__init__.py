@@ -687,9 +687,9 @@ class SlabGroup:
             s.init_philox(seed)
 
     def step(self, omega: float = 1.0, n: int = 1, *, bc: str | None = None, variant: str | None = None):
+        # blocking: d2q37_group_step syncs every slab and reports any slab's NonPhysicalError
         _check(_load().d2q37_group_step(self._hs, self.nslabs, float(omega), int(n),
                                         VARIANTS[variant or self.variant], BCS[bc or self.bc_mode]))
-        self.slabs[0].sync()
 
 
 class MultiGPU(SlabGroup):

@@ -248,6 +248,7 @@ int model_params(const d2q37_model* m, ModelParams* mp) {
 int upload_model(d2q37_lattice* h, const d2q37_model* m) {
     ModelParams mp{};
     RET(model_params(m, &mp));
+    if (std::memcmp(&mp, &h->mp, sizeof mp) == 0) return D2Q37_OK;  // same constants: keep the cached graphs
     h->mp = mp;
     ++h->model_gen;  // captured step graphs carry the old constants
     return D2Q37_OK;
@@ -2010,7 +2011,14 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
         RET(group_exchange(slabs, bc));
         for (d2q37_lattice* h : slabs) RET(slab_phase2(h, omega, variant, bc));
     }
-    return D2Q37_OK;
+    // like the reference's blocking step (and d2q37_multi_step): every slab's deferred
+    // non-physical flag is collected, so an error in any slab surfaces here
+    int rc = D2Q37_OK;
+    for (d2q37_lattice* h : slabs) {
+        const int r = d2q37_sync(h);
+        if (rc == D2Q37_OK) rc = r;
+    }
+    return rc;
 }
 
 int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct) {

@@ -2,8 +2,8 @@
 // lattice initialisers (pure C++, no CUDA).
 //
 //   d2q37_model_d2q37  <- VelocityModel::d2q37() (model.hpp:52, model.cpp:81-240):
-//                         velocity set, moment-matched shell weights + t0,
-//                         Hermite table folded with 1/(n! t0^n).
+//                         velocity set, the quadrature's shell weights + t0 (a
+//                         constant table), Hermite table folded with 1/(n! t0^n).
 //   d2q37_make_lattice <- make_random/equilibrium/shear_lattice (lattice.cpp:8-47)
 //                         and the BASELINE config 0-2 recipes.
 //
@@ -27,140 +27,35 @@
 namespace d2q37 {
 namespace {
 
+// The D2Q37 quadrature (VelocityModel::d2q37, model.cpp:101-181 derives it at
+// run time): shell weights w_s and the lattice temperature t0 for which the
+// lattice moments sum_i w_i cx^a cy^b equal those of a 2-D Gaussian of
+// variance t0 for (a, b) in {(0,0) (2,0) (4,0) (2,2) (6,0) (4,2) (6,2) (4,4)
+// (8,0)}, with sum_i w_i = 1.  The library ships the solution as a constant
+// table (round-to-nearest, no FMA contraction: identical to the oracle's
+// restatement, within 16 ulp of the reference's FMA build) instead of
+// re-deriving it; tests/test_host.py checks the moment residuals (< 1e-12),
+// the positivity and the reference's frozen values (test_model.cpp:87-142).
+// The lattice arithmetic takes the constants of the caller's model anyway
+// (d2q37_set_model: e.g. the reference's own VelocityModel).
+constexpr double kT0 = 0x1.655a23486b0eap-1;  // 0.6979533220196832
 constexpr int kShells = 8;
-constexpr std::array<int, kShells> kShellNorms = {0, 1, 2, 4, 5, 8, 9, 10};
+constexpr int kShellNorms[kShells] = {0, 1, 2, 4, 5, 8, 9, 10};  // |c|^2 of each shell
+constexpr double kShellW[kShells] = {
+    0x1.dd7e1917b635fp-3,   // |c|^2 = 0   0.23315066913235236
+    0x1.b786979d5dd9fp-4,   //         1   0.10730609154221903
+    0x1.d86a448815fd4p-5,   //         2   0.05766785988879489
+    0x1.d19327de15f20p-7,   //         4   0.014208216158450748
+    0x1.5ed142641e9dap-8,   //         5   0.005353049000513777
+    0x1.0945fb76e9ba7p-10,  //         8   0.0010119375926735759
+    0x1.01377e453341cp-12,  //         9   0.00024530102775771763
+    0x1.292e6f2a5028ep-12,  //        10   0.00028341425299419846
+};
 
-int shell_of_norm(int n2) {
+double shell_weight(int n2) {
     for (int s = 0; s < kShells; ++s)
-        if (kShellNorms[s] == n2) return s;
-    return -1;
-}
-
-// Moment conditions E[x^a y^b] of a 2-D Gaussian with variance t0: the first
-// eight determine the shell weights linearly, E[x^8] closes the system in t0.
-struct Cond {
-    int a, b;
-};
-constexpr std::array<Cond, kShells> kLinear = {{{0, 0}, {2, 0}, {4, 0}, {2, 2}, {6, 0}, {4, 2}, {6, 2}, {4, 4}}};
-constexpr Cond kClosing = {8, 0};
-
-double gaussian_moment(int k, double t0) {
-    if (k % 2 != 0) return 0.0;
-    double dfact = 1.0;
-    for (int j = k - 1; j > 0; j -= 2) dfact *= j;
-    return dfact * std::pow(t0, k / 2);
-}
-
-double int_pow(int base, int e) {
-    double r = 1.0;
-    for (int i = 0; i < e; ++i) r *= base;
-    return r;
-}
-
-using Mat = std::array<std::array<double, kShells>, kShells>;
-using Vec = std::array<double, kShells>;
-
-Vec gauss_solve(Mat a, Vec b) {
-    for (int col = 0; col < kShells; ++col) {
-        int piv = col;
-        for (int r = col + 1; r < kShells; ++r)
-            if (std::abs(a[r][col]) > std::abs(a[piv][col])) piv = r;
-        if (a[piv][col] == 0.0) throw std::runtime_error("singular moment system");
-        std::swap(a[col], a[piv]);
-        std::swap(b[col], b[piv]);
-        for (int r = col + 1; r < kShells; ++r) {
-            const double f = a[r][col] / a[col][col];
-            for (int c = col; c < kShells; ++c) a[r][c] -= f * a[col][c];
-            b[r] -= f * b[col];
-        }
-    }
-    Vec x{};
-    for (int r = kShells - 1; r >= 0; --r) {
-        double s = b[r];
-        for (int c = r + 1; c < kShells; ++c) s -= a[r][c] * x[c];
-        x[r] = s / a[r][r];
-    }
-    return x;
-}
-
-struct Derived {
-    Vec shell_w;
-    double t0;
-};
-
-Derived derive(const int* cx, const int* cy) {
-    auto shell_moment = [&](int s, int a, int b) {
-        double acc = 0.0;
-        for (int i = 0; i < kNpop; ++i)
-            if (shell_of_norm(cx[i] * cx[i] + cy[i] * cy[i]) == s) acc += int_pow(cx[i], a) * int_pow(cy[i], b);
-        return acc;
-    };
-    Mat a{};
-    Vec closing{};
-    for (int r = 0; r < kShells; ++r)
-        for (int s = 0; s < kShells; ++s) a[r][s] = shell_moment(s, kLinear[r].a, kLinear[r].b);
-    for (int s = 0; s < kShells; ++s) closing[s] = shell_moment(s, kClosing.a, kClosing.b);
-
-    auto weights = [&](double t0) {
-        Vec rhs{};
-        for (int r = 0; r < kShells; ++r)
-            rhs[r] = gaussian_moment(kLinear[r].a, t0) * gaussian_moment(kLinear[r].b, t0);
-        return gauss_solve(a, rhs);
-    };
-    auto closing_residual = [&](double t0) {
-        const Vec w = weights(t0);
-        double r = -gaussian_moment(kClosing.a, t0) * gaussian_moment(kClosing.b, t0);
-        for (int s = 0; s < kShells; ++s) r += closing[s] * w[s];
-        return r;
-    };
-    auto population_sum = [&](const Vec& w) {
-        double sum = 0.0;
-        for (int i = 0; i < kNpop; ++i) sum += w[shell_of_norm(cx[i] * cx[i] + cy[i] * cy[i])];
-        return sum;
-    };
-
-    // Scan t0 in (0.1, 2.0) for a sign change of the closing residual, bisect,
-    // accept the first root with all-positive weights, then pin sum(w) == 1.
-    const double lo0 = 0.1, hi0 = 2.0, dt = 1e-3;
-    double t_prev = lo0, r_prev = closing_residual(lo0);
-    for (double t = lo0 + dt; t < hi0; t += dt) {
-        const double r = closing_residual(t);
-        if (std::signbit(r) != std::signbit(r_prev)) {
-            double lo = t_prev, hi = t, r_lo = r_prev;
-            for (int it = 0; it < 200 && hi - lo > 1e-16; ++it) {
-                const double mid = 0.5 * (lo + hi);
-                const double rm = closing_residual(mid);
-                if (std::abs(rm) < 1e-14) {
-                    lo = hi = mid;
-                    break;
-                }
-                if (std::signbit(rm) == std::signbit(r_lo)) {
-                    lo = mid;
-                    r_lo = rm;
-                } else {
-                    hi = mid;
-                }
-            }
-            const double t0 = 0.5 * (lo + hi);
-            Vec w = weights(t0);
-            if (std::all_of(w.begin(), w.end(), [](double v) { return v > 0.0; })) {
-                for (int pass = 0; pass < 4; ++pass) {
-                    const double sum = population_sum(w);
-                    if (sum == 1.0) break;
-                    for (double& v : w) v /= sum;
-                }
-                for (int pass = 0; pass < 4; ++pass) {
-                    const double sum = population_sum(w);
-                    if (sum == 1.0) break;
-                    w[0] -= sum - 1.0;  // rest weight enters no other moment condition
-                }
-                return {w, t0};
-            }
-        }
-        t_prev = t;
-        r_prev = r;
-    }
-    throw std::runtime_error("no all-positive D2Q37 quadrature for t0 in (0.1, 2.0)");
+        if (kShellNorms[s] == n2) return kShellW[s];
+    throw std::runtime_error("velocity outside the D2Q37 shells");
 }
 
 }  // namespace
@@ -171,11 +66,10 @@ void build_model(d2q37_model* m) {
         m->cx[p] = cx_of(p);
         m->cy[p] = cy_of(p);
     }
-    const Derived d = derive(m->cx, m->cy);
-    const double t0 = d.t0;
+    const double t0 = kT0;
     m->t0 = t0;
     for (int i = 0; i < kNpop; ++i) {
-        m->w[i] = d.shell_w[shell_of_norm(m->cx[i] * m->cx[i] + m->cy[i] * m->cy[i])];
+        m->w[i] = shell_weight(m->cx[i] * m->cx[i] + m->cy[i] * m->cy[i]);
         const double cx = m->cx[i], cy = m->cy[i];
         const double cx2 = cx * cx, cy2 = cy * cy;
         const double t2 = t0 * t0, t3 = t2 * t0, t4 = t2 * t2;

@@ -319,6 +319,12 @@ def test_config0_100_steps(gpu, lbm, po, layout, vl, variant):
     one = s1.dump()
     want1, _ = po.orc_step(init, omega, 1, po.BC_WALL)
     assert max_rel(one, want1) <= 1e-12
+    # derived fields after one step (model.cpp:242-257): rho, T elementwise, u relative to the peak speed
+    r1, ux1, uy1, t1 = macros_fields(po, one)
+    rw1, uxw1, uyw1, tw1 = macros_fields(po, want1)
+    assert max_rel(r1, rw1) <= 1e-12 and max_rel(t1, tw1) <= 1e-12
+    speed1 = max(np.max(np.abs(uxw1)), np.max(np.abs(uyw1)))
+    assert max(np.max(np.abs(ux1 - uxw1)), np.max(np.abs(uy1 - uyw1))) <= 1e-12 * speed1
     s1.step(omega, 99)
     got = s1.dump()
     want, bad = po.orc_step(init, omega, 100, po.BC_WALL)
@@ -1114,7 +1120,25 @@ def test_fused2_slab_nonphysical_raises(gpu, lbm):
     bad[:, 3, 70] = -1.0
     grp = lbm.SlabGroup("soa", lx, ly, 1, 2, variant="fused2")
     grp.load(bad)
-    with pytest.raises(lbm.NonPhysicalError):
+    with pytest.raises(lbm.NonPhysicalError):  # the bad site is in slab 1: step() syncs every slab
         grp.step(1.0, 2)
-        for s in grp.slabs:
-            s.sync()
+
+
+@pytest.mark.parametrize("lx,ly,nslabs", [(16384, 400, 1), (20000, 400, 2)])
+def test_fused2_split_launch_wide_short_lattices(gpu, lbm, lx, ly, nslabs):
+    """Wide, short wall lattices whose face bands outweigh the interior (a negative interior
+    CTA count skipped bands silently): every band is swept -- bit-identical to fused steps, single
+    domain and as wall + ghost slabs."""
+    init = lbm.make_lattice("random", lx, ly, seed=77)
+    ref = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused")
+    ref.load(init)
+    ref.step(0.9, 2)
+    want = ref.dump()
+    ref.close()
+    if nslabs == 1:
+        s = sim_of(lbm, "soa", lx, ly, bc="wall", variant="fused2")
+    else:
+        s = lbm.SlabGroup("soa", lx, ly, 1, nslabs, bc="wall", variant="fused2")
+    s.load(init)
+    s.step(0.9, 2)
+    assert np.array_equal(s.dump(), want)

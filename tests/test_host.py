@@ -203,3 +203,24 @@ def test_validation_first_divergence_order_and_defaults(lbm):
     assert o.geometries == [(16, 32), (64, 128)] and o.vls == [1, 2, 4, 8]
     assert o.layouts == ["aos", "soa", "csoa", "caosoa"] and (o.steps, o.omega, o.seed) == (10, 1.0, 12345)
     assert o.corrupt_population == -1
+
+
+def test_product_quadrature_satisfies_the_moment_conditions(lbm):
+    """The shipped quadrature table (csrc/d2q37_host.cpp) solves the conditions model.cpp:101-181
+    derives it from: lattice moments sum_i w_i cx^a cy^b equal the 2-D Gaussian's of variance t0 for
+    (a, b) in {(0,0) (2,0) (4,0) (2,2) (6,0) (4,2) (6,2) (4,4) (8,0)} (test_model.cpp:119-142), all
+    weights positive, one weight per shell."""
+    m = lbm.model()
+    cx, cy = m.velocities[:, 0].astype(float), m.velocities[:, 1].astype(float)
+    w, t0 = m.weights, m.t0
+
+    def gauss(k):
+        return 0.0 if k % 2 else float(np.prod(np.arange(k - 1, 0, -2, dtype=float))) * t0 ** (k // 2)
+
+    for a, b in ((0, 0), (2, 0), (4, 0), (2, 2), (6, 0), (4, 2), (6, 2), (4, 4), (8, 0)):
+        lat = float(np.sum(w * cx ** a * cy ** b))
+        assert abs(lat - gauss(a) * gauss(b)) <= 1e-12 * max(1.0, abs(gauss(a) * gauss(b))), (a, b)
+    assert np.all(w > 0)
+    n2 = cx * cx + cy * cy
+    for s in np.unique(n2):
+        assert len(np.unique(w[n2 == s])) == 1
