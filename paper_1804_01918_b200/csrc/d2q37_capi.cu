@@ -1,5 +1,6 @@
 // d2q37_capi.cu -- the C-ABI of include/d2q37_b200.h: device lattice handle,
 // storage, the per-step schedule (single domain and y-slab), load/dump.
+#include <cuda.h>  // CUresult / CUstream for the driver's stream wait-value operation
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -103,6 +104,9 @@ struct d2q37_lattice {
     unsigned long long p2p_seq = 0;             // steps (and primes) issued
     bool p2p_connected = false;
     bool p2p_dirty = true;  // prv changed outside a step: ghost columns must be re-primed
+    bool h6_valid = false;  // FUSED2 slab: prv's 6-row ghost rows hold the neighbours' current rows
+    unsigned* d_sweep_counter = nullptr;  // overlapped FUSED2 slab sweeps: face CTAs done (k_step2_slab)
+    unsigned sweep_target = 0;            // its value once the last queued sweep's face CTAs are done
     // cached CUDA graph of kGraphSteps single-domain steps (d2q37_step)
     struct StepGraph {
         cudaGraphExec_t exec = nullptr;
@@ -344,6 +348,7 @@ void free_lattice(d2q37_lattice* h) {
         if (e) cudaEventDestroy(e);
     if (h->d_flag) cudaFree(h->d_flag);
     if (h->d_seq) cudaFree(h->d_seq);
+    if (h->d_sweep_counter) cudaFree(h->d_sweep_counter);
     for (void* p : h->ipc_mapped) cudaIpcCloseMemHandle(p);
     if (h->h_flag) cudaFreeHost(h->h_flag);
     if (h->ev_pack) cudaEventDestroy(h->ev_pack);
@@ -399,17 +404,18 @@ cudaEvent_t prof_event(d2q37_lattice* h) {
 struct ProfScope {
     d2q37_lattice* h;
     int cls;
+    cudaStream_t st;
     cudaEvent_t a = nullptr;
-    ProfScope(d2q37_lattice* h_, int cls_) : h(h_), cls(cls_) {
+    ProfScope(d2q37_lattice* h_, int cls_, cudaStream_t st_ = nullptr) : h(h_), cls(cls_), st(st_ ? st_ : h_->stream) {
         if (h->prof_on) {
             a = prof_event(h);
-            cudaEventRecord(a, h->stream);
+            cudaEventRecord(a, st);
         }
     }
     ~ProfScope() {
         if (a) {
             cudaEvent_t b = prof_event(h);
-            cudaEventRecord(b, h->stream);
+            cudaEventRecord(b, st);
             h->prof_pending.push_back({cls, a, b});
         }
     }
@@ -689,6 +695,112 @@ int step2_slab_exchange_nccl(d2q37_lattice* h, int bc) {
     }
     CK(cudaEventRecord(h->ev_wait[h->ev_count % kEventRing], h->stream));
     ++h->ev_count;
+    return D2Q37_OK;
+}
+
+// SMs the interior launch of an overlapped FUSED2 slab sweep leaves to the halo
+// pipeline (pack, NCCL, unpack on the comm stream): the persistent interior
+// CTAs take every register and all shared memory of their SM, so the halo
+// kernels only run beside them on SMs left free.  D2Q37_STEP2_HALO_SMS.
+// D2Q37_STEP2_OVERLAP=0 selects the serial exchange-then-sweep schedule (A/B).
+bool step2_overlap() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("D2Q37_STEP2_OVERLAP");
+        v = (e && *e == '0') ? 0 : 1;
+    }
+    return v != 0;
+}
+
+int step2_halo_sms() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("D2Q37_STEP2_HALO_SMS");
+        v = e ? std::max(0, std::atoi(e)) : 1;
+    }
+    return v;
+}
+
+// The driver's cuStreamWaitValue32 (stream memory operation; 32-bit waits need
+// no device attribute), looked up once through the runtime.
+using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32 wait_value32() {
+    static WaitValue32 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WaitValue32>(p);
+        (void)cudaGetLastError();
+    }
+    return fn;
+}
+
+// One FUSED2 sweep of an NCCL y-slab with its 6-row halo exchange overlapped
+// (north_star: "overlapped with interior compute"); prv's ghost rows are
+// current (h6_valid).  One launch (k_step2_slab): a few CTAs sweep the face
+// bands first and pack the new state's 6 edge rows into the send buffers as
+// they write them, then bump a device counter; all CTAs then sweep the
+// interior.  On the comm stream a wait on that counter gates the NCCL
+// exchange and the unpack into the new state's ghost rows, which run on the
+// step2_halo_sms() SMs the sweep leaves free (its persistent CTAs take every
+// register and all shared memory of their SM) while the interior is swept.
+// The lattice stream waits for the exchange before the next sweep.  Every
+// band sees the same inputs as in the serial exchange-then-sweep schedule, so
+// the two are bit-identical.
+int step2_sweep_overlapped(d2q37_lattice* h, double omega, int bc, const Faces& fc) {
+    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    WaitValue32 wait = wait_value32();
+    RET(ensure_halo6(h));
+    if (!h->d_sweep_counter) {
+        CK(cudaMalloc(&h->d_sweep_counter, sizeof(unsigned)));
+        CK(cudaMemset(h->d_sweep_counter, 0, sizeof(unsigned)));
+        h->sweep_target = 0;
+    }
+    const double* src = h->buf[h->cur];
+    double* dst = h->buf[1 - h->cur];
+    const int grid = h->nsm - std::min(step2_halo_sms(), h->nsm / 4);
+    int nsig = 0;
+    if (wait) {
+        ProfScope ps(h, kProfFused);
+        cudaError_t err;
+        nsig = launch_step2_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid, h->d_sweep_counter,
+                                 h->h6[0], h->h6[1], &err);
+        CK(err);
+    }
+    if (nsig == 0) {  // no overlapped form for this slab (small, periodic face): the serial schedule
+        RET(step2_local(h, omega, fc));
+        h->h6_valid = false;
+        return D2Q37_OK;
+    }
+    h->sweep_target += unsigned(nsig);
+    {  // the halo pipeline of the new state, beside the interior
+        const int lo = lo_peer_of(h, bc), hi = hi_peer_of(h, bc);
+        if (wait(reinterpret_cast<CUstream>(h->comm_stream), reinterpret_cast<CUdeviceptr>(h->d_sweep_counter),
+                 h->sweep_target, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return fail(D2Q37_ERR_CUDA, "cuStreamWaitValue32 failed");
+        std::string why;
+        const int rc = nccl_exchange(h->comm, h->comm_stream, h->h6[0], h->h6[2], lo, h->h6[1], h->h6[3], hi,
+                                     halo6_count(h->g), &why);
+        if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+        {
+            ProfScope ps(h, kProfEdge, h->comm_stream);
+            CK(launch_unpack6(dst, h->g, lo >= 0 ? h->h6[2] : nullptr, hi >= 0 ? h->h6[3] : nullptr,
+                              h->comm_stream));
+        }
+        CK(cudaEventRecord(h->ev_recv, h->comm_stream));
+    }
+    // exposed halo: from the end of the sweep to the end of the exchange
+    CK(cudaEventRecord(h->ev_int[h->ev_count % kEventRing], h->stream));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_recv, 0));
+    CK(cudaEventRecord(h->ev_wait[h->ev_count % kEventRing], h->stream));
+    ++h->ev_count;
+    h->cur = 1 - h->cur;
+    h->time_step += 2;
+    h->h6_valid = true;
     return D2Q37_OK;
 }
 
@@ -1077,7 +1189,7 @@ int ensure_io_pipeline(d2q37_lattice* h, size_t plane_vals) {
 }
 
 int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n, bool src_device) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 (prv) or 1 (nxt)");
     if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "from_canonical: dimension mismatch");
@@ -1317,7 +1429,7 @@ int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
 }
 
 int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     RET(padded_verbs_ok(h, "write_padded"));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
@@ -1338,6 +1450,7 @@ int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n
 
 int d2q37_bc(d2q37_lattice* h, int bc) {
     RET(check_handle(h));
+    h->h6_valid = false;  // the reference's 3 ghost rows share storage with the 6-row FUSED2 ghosts
     RET(padded_verbs_ok(h, "bc"));
     RET(validate_bc(h, bc));
     DeviceGuard dg(h->device);
@@ -1359,6 +1472,7 @@ int d2q37_propagate(d2q37_lattice* h) { return d2q37_propagate_corrupt(h, -1); }
 
 int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
     RET(check_handle(h));
+    h->h6_valid = false;
     RET(padded_verbs_ok(h, "propagate"));
     DeviceGuard dg(h->device);
     if (corrupt_population >= kNpop) return fail(D2Q37_ERR_INVALID_ARGUMENT, "corrupt_population out of range");
@@ -1370,6 +1484,7 @@ int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
 
 int d2q37_collide(d2q37_lattice* h, double omega) {
     RET(check_handle(h));
+    h->h6_valid = false;
     if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "collide: not available on the banded store (use FUSED2 steps)");
     DeviceGuard dg(h->device);
     return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1, ghost_faces(h));
@@ -1408,6 +1523,11 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
                     }
                 }
                 for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
+            } else if (h->transport == kTransportNccl && h->comm_stream && step2_overlap()) {
+                for (; s + 2 <= nsteps; s += 2) {
+                    if (!h->h6_valid) RET(step2_slab_exchange_nccl(h, bc));
+                    RET(step2_sweep_overlapped(h, omega, bc, fc));
+                }
             } else if (h->transport == kTransportNccl) {
                 for (; s + 2 <= nsteps; s += 2) {
                     RET(step2_slab_exchange_nccl(h, bc));
@@ -1417,6 +1537,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
         }
         variant = D2Q37_FUSED;  // the odd last step, and every layout / case k_step2 does not cover
     }
+    if (s < nsteps) h->h6_valid = false;  // the remaining steps change prv without refreshing its 6-row ghosts
     if (!slab && !h->prof_on && nsteps - s >= kGraphSteps) {
         // Launch-bound small lattices: replay kGraphSteps steps as one CUDA graph.
         RET(ensure_step_graph(h, omega, variant, bc));
@@ -1449,7 +1570,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
 }
 
 int d2q37_swap_buffers(d2q37_lattice* h) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     h->cur = 1 - h->cur;
     return D2Q37_OK;
@@ -1556,6 +1677,7 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst) {
     CK(cudaStreamSynchronize(src->stream));
     dst->time_step = src->time_step;
     dst->p2p_dirty = true;
+    dst->h6_valid = false;
     return D2Q37_OK;
 }
 
@@ -1579,7 +1701,7 @@ int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* pa
 }
 
 int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
     if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "fill_philox: not available on the banded store");
@@ -1590,7 +1712,7 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
 }
 
 int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     DeviceGuard dg(h->device);
     CK(launch_init_rt(h->buf[h->cur], h->g, h->mp, seed, h->y0, h->ly_global, h->stream));
@@ -1677,7 +1799,7 @@ int d2q37_save_dump(d2q37_lattice* h, const char* path) {
 }
 
 int d2q37_load_dump(d2q37_lattice* h, const char* path) {
-    if (h) h->p2p_dirty = true;
+    if (h) h->p2p_dirty = true, h->h6_valid = false;
     RET(check_handle(h));
     if (!path) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null path");
     DeviceGuard dg(h->device);
@@ -1888,6 +2010,7 @@ int d2q37_p2p_connect(d2q37_lattice* h, const unsigned char lo[D2Q37_P2P_BLOB_BY
     }
     h->p2p_connected = true;
     h->p2p_dirty = true;
+    h->h6_valid = false;
     return D2Q37_OK;
 }
 

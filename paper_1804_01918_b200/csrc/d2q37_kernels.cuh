@@ -139,6 +139,22 @@ cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, 
                                const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                          double omega, int* flag, cudaStream_t s, int part, int max_ctas);
+// Slab sweeps split in time (the overlapped FUSED2 slab schedule): bands
+// [b_lo, b_hi) pull only rows inside [0, ly); the others reach a face.
+void step2_interior_bands(const DevGeo& g, int* nbands, int* b_lo, int* b_hi);
+// One overlapped FUSED2 slab sweep on `grid` CTAs (k_step2_slab): face bands
+// first on a few CTAs, which write the 6-row halos of the new state into
+// send_lo / send_hi and add one each to *counter; then the interior.  Returns
+// the number of CTAs that signal (0: not launched -- no interior band, a
+// periodic face, or a launch error in *err).
+int launch_step2_slab(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                      double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
+                      double* send_hi, cudaError_t* err);
+// Explicit band ranges per part: part 0 in the per-thread plain form (rows read
+// unwrapped: not for y-periodic faces), parts 1 and 2 in the general form.
+cudaError_t launch_step2_parts(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                               const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int band0[3],
+                               const int nb[3], const int ctas[3]);
 // Band-blocked store (layout D2Q37_BANDED, d2q37_banded.cu): FUSED2 sweeps on
 // blocks of 37 populations x (kBandRows + 2 kBandHalo) rows per (column, band),
 // the halo rows kept as copies.  band_geometry fills a DevGeo (band = 1), band_elems its buffer size.

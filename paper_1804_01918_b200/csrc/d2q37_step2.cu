@@ -37,7 +37,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
+#include <vector>
 #include <utility>
 
 #include "d2q37_device.cuh"
@@ -57,7 +59,9 @@ namespace d2q37 {
 template <bool WRAPY>
 __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
                                             const ModelParams& mp, double omega, int band0, int nbands,
-                                            long long per_cta, int* __restrict__ flag, int cta) {
+                                            long long item_begin, long long item_end_, int* __restrict__ flag,
+                                            double* __restrict__ send_lo = nullptr,
+                                            double* __restrict__ send_hi = nullptr) {
     extern __shared__ double ring[];
     const bool prod = threadIdx.x < kT2Band;
     const int tid = threadIdx.x & (kT2Band - 1);
@@ -66,8 +70,8 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
     const long long total = (long long)nbands * lx;
-    long long item = (long long)cta * per_cta;
-    const long long item_end = min(total, item + per_cta);
+    long long item = item_begin;
+    const long long item_end = min(total, item_end_);
     auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
     bool bad = false;
     while (item < item_end) {
@@ -122,6 +126,18 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
                     const long long e = (long long)(xs - 7 + t) * cs + y0 + tid;
 #pragma unroll
                     for (int p = 0; p < kNpop; ++p) __stcs(db + p * plane + e, v[p]);
+                    // fused pack of a slab's 6-row halos ([p][x][6], the k_pack6 layout)
+                    const int y = y0 + tid;
+                    if (send_lo && y < 2 * kHalo) {
+                        double* __restrict__ sl = send_lo + (long long)(xs - 7 + t) * (2 * kHalo) + y;
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) sl[(long long)p * lx * (2 * kHalo)] = v[p];
+                    }
+                    if (send_hi && y >= ly - 2 * kHalo) {
+                        double* __restrict__ sh = send_hi + (long long)(xs - 7 + t) * (2 * kHalo) + y - (ly - 2 * kHalo);
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) sh[(long long)p * lx * (2 * kHalo)] = v[p];
+                    }
                 }
                 __syncthreads();
             }
@@ -146,7 +162,7 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
 template <bool GHOST, bool EARLY>
 __device__ __forceinline__ void sweep_tma(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
                                           const ModelParams& mp, double omega, int band0, int nbands,
-                                          long long per_cta, int* __restrict__ flag, int cta) {
+                                          long long item_begin, long long item_end_, int* __restrict__ flag) {
     extern __shared__ double ring[];
     double* stage = ring + kT2RingCols * kT2Band;
     unsigned long long* full = reinterpret_cast<unsigned long long*>(stage + kNpop * kStageRows);
@@ -158,8 +174,8 @@ __device__ __forceinline__ void sweep_tma(const double* __restrict__ src, double
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
     const long long total = (long long)nbands * lx;
-    long long item = (long long)cta * per_cta;
-    const long long item_end = min(total, item + per_cta);
+    long long item = item_begin;
+    const long long item_end = min(total, item_end_);
     auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
     if (threadIdx.x == 0) {
         mbar_init(full, 1);
@@ -257,8 +273,9 @@ __device__ __forceinline__ void sweep_tma(const double* __restrict__ src, double
 // (k_step2_plain covers the rest).
 __device__ __forceinline__ void sweep_general(const double* __restrict__ src, double* __restrict__ dst,
                                               const DevGeo& g, const Faces& fc, const ModelParams& mp, double omega,
-                                              int band0, int nbands, long long per_cta, int* __restrict__ flag,
-                                              int cta) {
+                                              int band0, int nbands, long long item_begin, long long item_end_,
+                                              int* __restrict__ flag, double* __restrict__ send_lo = nullptr,
+                                              double* __restrict__ send_hi = nullptr) {
     extern __shared__ double ring[];
     const bool prod = threadIdx.x < kT2Band;
     const int tid = threadIdx.x & (kT2Band - 1);
@@ -271,8 +288,8 @@ __device__ __forceinline__ void sweep_general(const double* __restrict__ src, do
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
     const long long total = (long long)nbands * lx;
-    long long item = (long long)cta * per_cta;
-    const long long item_end = min(total, item + per_cta);
+    long long item = item_begin;
+    const long long item_end = min(total, item_end_);
     bool bad = false;
     while (item < item_end) {
         const int band = band0 + (int)(item / lx);
@@ -379,6 +396,17 @@ __device__ __forceinline__ void sweep_general(const double* __restrict__ src, do
                     double* __restrict__ o = db + (long long)(xs - 7 + t) * cs + y;
 #pragma unroll
                     for (int p = 0; p < kNpop; ++p) __stcs(o + p * plane, v[p]);
+                    // fused pack of a slab's 6-row halos ([p][x][6], the k_pack6 layout)
+                    if (send_lo && y < 2 * kHalo) {
+                        double* __restrict__ sl = send_lo + (long long)(xs - 7 + t) * (2 * kHalo) + y;
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) sl[(long long)p * lx * (2 * kHalo)] = v[p];
+                    }
+                    if (send_hi && y >= ly - 2 * kHalo) {
+                        double* __restrict__ sh = send_hi + (long long)(xs - 7 + t) * (2 * kHalo) + y - (ly - 2 * kHalo);
+#pragma unroll
+                        for (int p = 0; p < kNpop; ++p) sh[(long long)p * lx * (2 * kHalo)] = v[p];
+                    }
                 }
                 __syncthreads();
             }
@@ -391,13 +419,13 @@ template <bool WRAPY>
 __global__ void __launch_bounds__(2 * kT2Band, 1)
     k_step2_plain(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
                   int band0, int nbands, long long per_cta, int* __restrict__ flag) {
-    sweep_plain<WRAPY>(src, dst, g, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
+    sweep_plain<WRAPY>(src, dst, g, mp, omega, band0, nbands, blockIdx.x * per_cta, (blockIdx.x + 1) * per_cta, flag);
 }
 
 __global__ void __launch_bounds__(2 * kT2Band, 1)
     k_step2(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
             double omega, int band0, int nbands, long long per_cta, int* __restrict__ flag) {
-    sweep_general(src, dst, g, fc, mp, omega, band0, nbands, per_cta, flag, blockIdx.x);
+    sweep_general(src, dst, g, fc, mp, omega, band0, nbands, blockIdx.x * per_cta, (blockIdx.x + 1) * per_cta, flag);
 }
 
 // One launch, three CTA groups: the interior bands (plain form, or the
@@ -416,25 +444,64 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
     if (cta < sp.ctas[0]) {
         if (sp.form == kStep2Bulk) {
             if (fc.hi == kFaceGhost)
-                sweep_tma<true, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+                sweep_tma<true, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
             else
-                sweep_tma<false, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+                sweep_tma<false, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
         } else if (sp.form == kStep2BulkEarly) {
             if (fc.hi == kFaceGhost)
-                sweep_tma<true, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+                sweep_tma<true, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
             else
-                sweep_tma<false, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+                sweep_tma<false, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
         } else if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic) {
-            sweep_plain<true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+            sweep_plain<true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
         } else {
-            sweep_plain<false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], sp.per_cta[0], flag, cta);
+            sweep_plain<false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
         }
         return;
     }
     cta -= sp.ctas[0];
     const int part = cta < sp.ctas[1] ? 1 : 2;
     if (part == 2) cta -= sp.ctas[1];
-    sweep_general(src, dst, g, fc, mp, omega, sp.band0[part], sp.nb[part], sp.per_cta[part], flag, cta);
+    sweep_general(src, dst, g, fc, mp, omega, sp.band0[part], sp.nb[part], cta * sp.per_cta[part],
+                  (cta + 1) * sp.per_cta[part], flag);
+}
+
+// One overlapped sweep of a FUSED2 y-slab (k_step2_slab): the first nf_lo +
+// nf_hi CTAs sweep the face bands first -- the bands whose pulls reach the
+// ghost rows or a wall -- writing the slab's 6 edge rows of the new state into
+// the send buffers as they go (fused pack), then bump the sweep counter; every
+// CTA then sweeps its share of the interior bands.  The host queues the halo
+// exchange on the comm stream behind a stream wait on that counter, so the
+// exchange runs while the interior is being swept.
+constexpr int kSlabMaxCtas = 256;
+struct SlabPlan {
+    int nf_lo, nf_hi;  // CTAs [0, nf_lo): the low face bands; [nf_lo, nf_lo + nf_hi): the high ones
+    int lo_band0, lo_nb, hi_band0, hi_nb, in_band0, in_nb;
+    long long lo_per, hi_per;
+    long long in_off[kSlabMaxCtas + 1];  // interior items of CTA c: [in_off[c], in_off[c + 1])
+};
+
+__global__ void __launch_bounds__(2 * kT2Band, 1)
+    k_step2_slab(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, Faces fc, ModelParams mp,
+                 double omega, SlabPlan sp, int* __restrict__ flag, unsigned* __restrict__ counter,
+                 double* __restrict__ send_lo, double* __restrict__ send_hi) {
+    const int cta = blockIdx.x;
+    if (cta < sp.nf_lo + sp.nf_hi) {
+        const bool lo = cta < sp.nf_lo;
+        const long long c = lo ? cta : cta - sp.nf_lo, per = lo ? sp.lo_per : sp.hi_per;
+        const int b0 = lo ? sp.lo_band0 : sp.hi_band0, nb = lo ? sp.lo_nb : sp.hi_nb;
+        if ((lo ? fc.lo : fc.hi) == kFaceWall)  // a global wall: the general form mirrors
+            sweep_general(src, dst, g, fc, mp, omega, b0, nb, c * per, (c + 1) * per, flag, send_lo, send_hi);
+        else  // ghost rows: read unwrapped by the plain form
+            sweep_plain<false>(src, dst, g, mp, omega, b0, nb, c * per, (c + 1) * per, flag, send_lo, send_hi);
+        __syncthreads();  // every consumer's face rows (lattice and send buffers) are stored
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            atomicAdd(counter, 1u);
+        }
+    }
+    if (sp.in_off[cta] < sp.in_off[cta + 1])
+        sweep_plain<false>(src, dst, g, mp, omega, sp.in_band0, sp.in_nb, sp.in_off[cta], sp.in_off[cta + 1], flag);
 }
 
 // 6-row slab halos of FUSED2: rows 0..5 / ly-6..ly-1 of every physical column
@@ -611,6 +678,98 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
     else
         k_step2<<<grid, 2 * kT2Band, smem, s>>>(src, dst, g, fc, mp, omega, band0, nb, per_cta, flag);
     return cudaGetLastError();
+}
+
+void step2_interior_bands(const DevGeo& g, int* nbands, int* b_lo, int* b_hi) {
+    *nbands = (g.ly + kT2Out - 1) / kT2Out;
+    *b_lo = 1;  // band 0 pulls rows down to -6
+    *b_hi = std::min(*nbands, g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0);  // pulls stay below ly
+    if (g.lx < kHalo || *b_hi <= *b_lo) *b_lo = *b_hi = 0;
+}
+
+cudaError_t launch_step2_parts(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                               const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int band0[3],
+                               const int nb[3], const int ctas[3]) {
+    cudaError_t e;
+    device_nsm(&e);
+    if (e != cudaSuccess) return e;
+    Step2Split sp{};
+    sp.form = kStep2Plain;  // part 0 reads rows unwrapped (slab interiors): the per-thread form
+    int grid = 0;
+    for (int part = 0; part < 3; ++part) {
+        sp.band0[part] = band0[part];
+        sp.nb[part] = nb[part];
+        const long long total = (long long)std::max(0, nb[part]) * g.lx;
+        sp.ctas[part] = total > 0 ? (int)std::min<long long>(ctas[part], total) : 0;
+        if (total > 0 && sp.ctas[part] < 1) return cudaErrorInvalidValue;
+        sp.per_cta[part] = sp.ctas[part] ? (total + sp.ctas[part] - 1) / sp.ctas[part] : 0;
+        grid += sp.ctas[part];
+    }
+    if (grid == 0) return cudaSuccess;
+    if (nb[0] > 0 && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic) return cudaErrorInvalidValue;  // nowrap only
+    k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(sp.form), s>>>(src, dst, g, fc, mp, omega, sp, flag);
+    return cudaGetLastError();
+}
+
+int launch_step2_slab(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                      double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
+                      double* send_hi, cudaError_t* err) {
+    *err = cudaSuccess;
+    int nbands, b_lo, b_hi;
+    step2_interior_bands(g, &nbands, &b_lo, &b_hi);
+    if (b_hi - b_lo < 1 || grid < 8 || grid > kSlabMaxCtas || fc.lo == kFacePeriodic || fc.hi == kFacePeriodic)
+        return 0;  // no overlapped form: the caller runs the serial schedule
+    static bool attr = false;
+    if (!attr) {
+        *err = cudaFuncSetAttribute(k_step2_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)step2_smem_bytes(kStep2Plain));
+        if (*err != cudaSuccess) return 0;
+        attr = true;
+    }
+    SlabPlan sp{};
+    sp.lo_band0 = 0;
+    sp.lo_nb = b_lo;
+    sp.hi_band0 = b_hi;
+    sp.hi_nb = nbands - b_hi;
+    sp.in_band0 = b_lo;
+    sp.in_nb = b_hi - b_lo;
+    // cost per item relative to the plain interior form: the general form at a wall
+    const double cfl = fc.lo == kFaceWall ? step2_face_pct() / 100.0 : 1.0;
+    const double cfh = fc.hi == kFaceWall ? step2_face_pct() / 100.0 : 1.0;
+    const double lo_items = double(sp.lo_nb) * g.lx, hi_items = double(sp.hi_nb) * g.lx;
+    const long long in_items = (long long)sp.in_nb * g.lx;
+    const double per = (cfl * lo_items + cfh * hi_items + double(in_items)) / grid;  // work per CTA
+    // face CTAs: enough that a face share is at most half of a CTA's work (the exchange then has
+    // the other half of the sweep to hide under)
+    auto nface = [&](double items, double cf) {
+        if (items <= 0) return 0;
+        return std::max(1, std::min(grid / 4, int(std::ceil(2.0 * cf * items / per))));
+    };
+    sp.nf_lo = nface(lo_items, cfl);
+    sp.nf_hi = nface(hi_items, cfh);
+    sp.lo_per = sp.nf_lo ? (long long)std::ceil(lo_items / sp.nf_lo) : 0;
+    sp.hi_per = sp.nf_hi ? (long long)std::ceil(hi_items / sp.nf_hi) : 0;
+    // interior shares: what is left of each CTA's work, scaled to the interior items
+    std::vector<double> share(grid);
+    double tot = 0.0;
+    for (int c = 0; c < grid; ++c) {
+        double face = 0.0;
+        if (c < sp.nf_lo) face = cfl * std::min<double>(sp.lo_per, std::max(0.0, lo_items - double(c) * sp.lo_per));
+        else if (c < sp.nf_lo + sp.nf_hi)
+            face = cfh * std::min<double>(sp.hi_per, std::max(0.0, hi_items - double(c - sp.nf_lo) * sp.hi_per));
+        share[c] = std::max(0.0, per - face);
+        tot += share[c];
+    }
+    double acc = 0.0;
+    sp.in_off[0] = 0;
+    for (int c = 0; c < grid; ++c) {
+        acc += share[c];
+        sp.in_off[c + 1] = c + 1 == grid ? in_items : std::min<long long>(in_items, llround(acc / tot * in_items));
+    }
+    k_step2_slab<<<grid, 2 * kT2Band, step2_smem_bytes(kStep2Plain), s>>>(src, dst, g, fc, mp, omega, sp, flag,
+                                                                         counter, send_lo, send_hi);
+    *err = cudaGetLastError();
+    return *err == cudaSuccess ? sp.nf_lo + sp.nf_hi : 0;
 }
 
 cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,

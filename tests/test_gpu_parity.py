@@ -1142,3 +1142,29 @@ def test_fused2_split_launch_wide_short_lattices(gpu, lbm, lx, ly, nslabs):
     s.load(init)
     s.step(0.9, 2)
     assert np.array_equal(s.dump(), want)
+
+
+@pytest.mark.parametrize("lx,ly", [(256, 1024), (300, 1205)])
+def test_fused2_nccl_self_ring_overlapped_bitwise(gpu, lbm, lx, ly):
+    """The overlapped FUSED2 slab schedule (face bands, then the interior beside the 6-row halo
+    pipeline on the comm stream: pack, ncclSend/Recv, unpack) through a real 1-rank NCCL ring, on
+    slabs large enough to take it: bit-identical to single-domain fused steps -- across calls (the
+    ghost rows stay valid between step() calls), after a load (invalidated, re-exchanged) and with
+    odd step counts."""
+    import torch  # noqa: F401  (torch's libnccl.so.2 is the one the library binds to)
+
+    init = lbm.make_lattice("random", lx, ly, seed=48)
+    ref = sim_of(lbm, "soa", lx, ly, variant="fused")
+    ref.load(init)
+    s = lbm.Simulation.slab("soa", lx, ly, 1, rank=0, nranks=1, nccl_id=lbm.nccl_unique_id(), variant="fused2")
+    s.load(init)
+    for n in (2, 4, 3, 6):
+        s.step(1.2, n)
+        ref.step(1.2, n)
+        assert np.array_equal(s.dump(), ref.dump()), n
+    assert s.exposed_halo_ms() >= 0.0
+    mid = ref.dump()
+    s.load(mid)  # a load invalidates the exchanged ghost rows
+    s.step(1.2, 4)
+    ref.step(1.2, 4)
+    assert np.array_equal(s.dump(), ref.dump())
