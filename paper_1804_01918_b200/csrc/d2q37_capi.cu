@@ -105,6 +105,7 @@ struct d2q37_lattice {
     bool p2p_connected = false;
     bool p2p_dirty = true;  // prv changed outside a step: ghost columns must be re-primed
     bool h6_valid = false;  // FUSED2 slab: prv's 6-row ghost rows hold the neighbours' current rows
+    int bc_filled = -1;  // y-major slab: boundary mode of the last bc verb while prv is unchanged (else -1)
     unsigned* d_sweep_counter = nullptr;  // overlapped FUSED2 slab sweeps: face CTAs done (k_step2_slab)
     unsigned sweep_target = 0;            // its value once the last queued sweep's face CTAs are done
     // cached CUDA graph of kGraphSteps single-domain steps (d2q37_step)
@@ -1189,7 +1190,7 @@ int ensure_io_pipeline(d2q37_lattice* h, size_t plane_vals) {
 }
 
 int load_canonical_impl(d2q37_lattice* h, int which, const double* src, size_t n, bool src_device) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 (prv) or 1 (nxt)");
     if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "from_canonical: dimension mismatch");
@@ -1429,7 +1430,7 @@ int d2q37_read_padded(d2q37_lattice* h, int which, double* host, size_t n) {
 }
 
 int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     RET(padded_verbs_ok(h, "write_padded"));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
@@ -1448,9 +1449,38 @@ int d2q37_write_padded(d2q37_lattice* h, int which, const double* host, size_t n
     return D2Q37_OK;
 }
 
+// halo_exchange (kernels.cpp:197-234) on y-major slab storage, which has no
+// reference padded order: the neighbours' face columns come into the ghost
+// columns (NCCL or, in a group, device copies) and the boundary mode is
+// recorded; the propagate verb then resolves the faces in the kernel (x
+// periodic, y wall / periodic / the exchanged ghost columns) -- the same
+// pulls the reference makes from its filled ghost cells.
+int ymajor_bc(d2q37_lattice* h, int bc) {
+    if (!local_only(h) && remote_faces(h, bc)) {
+        if (h->transport == kTransportGroup) {
+            RET(ymajor_group_exchange(h->group, bc));
+            for (d2q37_lattice* s : h->group) s->bc_filled = bc;
+            return D2Q37_OK;
+        }
+        if (h->transport != kTransportNccl)
+            return fail(D2Q37_ERR_UNSUPPORTED, "bc: not available on P2P y-major slabs (use step)");
+        CK(cudaEventRecord(h->ev_start, h->stream));
+        CK(cudaStreamWaitEvent(h->comm_stream, h->ev_start, 0));
+        RET(ymajor_exchange_nccl(h, bc));
+        CK(cudaStreamWaitEvent(h->stream, h->ev_recv, 0));
+    }
+    h->bc_filled = bc;
+    return D2Q37_OK;
+}
+
 int d2q37_bc(d2q37_lattice* h, int bc) {
     RET(check_handle(h));
     h->h6_valid = false;  // the reference's 3 ghost rows share storage with the 6-row FUSED2 ghosts
+    RET(validate_bc(h, bc));
+    if (h->g.tr) {
+        DeviceGuard dg(h->device);
+        return ymajor_bc(h, bc);
+    }
     RET(padded_verbs_ok(h, "bc"));
     RET(validate_bc(h, bc));
     DeviceGuard dg(h->device);
@@ -1473,18 +1503,22 @@ int d2q37_propagate(d2q37_lattice* h) { return d2q37_propagate_corrupt(h, -1); }
 int d2q37_propagate_corrupt(d2q37_lattice* h, int corrupt_population) {
     RET(check_handle(h));
     h->h6_valid = false;
-    RET(padded_verbs_ok(h, "propagate"));
+    if (!h->g.tr) RET(padded_verbs_ok(h, "propagate"));
+    if (h->g.tr && h->bc_filled < 0)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "propagate on a y-major slab: call bc (halo_exchange) first");
     DeviceGuard dg(h->device);
     if (corrupt_population >= kNpop) return fail(D2Q37_ERR_INVALID_ARGUMENT, "corrupt_population out of range");
     Offsets off = h->off_pull;
     if (corrupt_population >= 0) off.o[corrupt_population] += 1;  // bites on the flat-offset (interior) sites
     finish_offsets(off, h->g.pstride, corrupt_population < 0);
-    return propagate_launch(h, off, ghost_faces(h));
+    // y-major slabs: the faces of the last bc, resolved in the pull (see ymajor_bc)
+    return propagate_launch(h, off, h->g.tr ? step_faces(h, h->bc_filled) : ghost_faces(h));
 }
 
 int d2q37_collide(d2q37_lattice* h, double omega) {
     RET(check_handle(h));
     h->h6_valid = false;
+    h->bc_filled = -1;
     if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "collide: not available on the banded store (use FUSED2 steps)");
     DeviceGuard dg(h->device);
     return collide_launch(h, 1 - h->cur, h->cur, omega, false, all_sites(h->g), 1, ghost_faces(h));
@@ -1492,6 +1526,7 @@ int d2q37_collide(d2q37_lattice* h, double omega) {
 
 int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) {
     RET(check_handle(h));
+    h->bc_filled = -1;
     RET(validate_bc(h, bc));
     if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
     if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
@@ -1570,7 +1605,7 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
 }
 
 int d2q37_swap_buffers(d2q37_lattice* h) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     h->cur = 1 - h->cur;
     return D2Q37_OK;
@@ -1678,6 +1713,7 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst) {
     dst->time_step = src->time_step;
     dst->p2p_dirty = true;
     dst->h6_valid = false;
+    dst->bc_filled = -1;
     return D2Q37_OK;
 }
 
@@ -1701,7 +1737,7 @@ int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* pa
 }
 
 int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     if (which != 0 && which != 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "buffer index must be 0 or 1");
     if (h->g.band) return fail(D2Q37_ERR_UNSUPPORTED, "fill_philox: not available on the banded store");
@@ -1712,7 +1748,7 @@ int d2q37_fill_philox(d2q37_lattice* h, int which, uint64_t seed) {
 }
 
 int d2q37_init_rt_device(d2q37_lattice* h, uint64_t seed) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     DeviceGuard dg(h->device);
     CK(launch_init_rt(h->buf[h->cur], h->g, h->mp, seed, h->y0, h->ly_global, h->stream));
@@ -1799,7 +1835,7 @@ int d2q37_save_dump(d2q37_lattice* h, const char* path) {
 }
 
 int d2q37_load_dump(d2q37_lattice* h, const char* path) {
-    if (h) h->p2p_dirty = true, h->h6_valid = false;
+    if (h) h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
     RET(check_handle(h));
     if (!path) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null path");
     DeviceGuard dg(h->device);

@@ -580,12 +580,11 @@ def test_nccl_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, varia
     s.step(1.2, 6)
     assert np.array_equal(s.dump(), ref.dump())
     assert s.exposed_halo_ms() >= 0.0
-    if layout in ("aos", "caosoa"):  # y-major storage: no padded-buffer verbs
+    if layout in ("aos", "caosoa"):  # y-major storage: no padded element order ...
         with pytest.raises(ValueError, match="y-major"):
-            s.bc("periodic")
-        return
-    # the bc verb through NCCL fills only the 26 planned ghost pop-rows, which is
-    # everything propagate reads: halo + propagate must still equal the single domain
+            s.read_padded()
+    # ... but bc (halo_exchange through NCCL: 26 planned ghost pop-rows, or whole face columns in
+    # y-major storage) followed by propagate equals the single domain
     s.bc("periodic")
     s.propagate_only()
     ref.bc("periodic")
@@ -1168,3 +1167,24 @@ def test_fused2_nccl_self_ring_overlapped_bitwise(gpu, lbm, lx, ly):
     s.step(1.2, 4)
     ref.step(1.2, 4)
     assert np.array_equal(s.dump(), ref.dump())
+
+
+@pytest.mark.parametrize("layout,vl", [("aos", 1), ("caosoa", 8), ("caosoa", 32)])
+@pytest.mark.parametrize("bc", ["periodic", "wall"])
+@pytest.mark.parametrize("nslabs", [2, 3])
+def test_ymajor_slab_bc_propagate_bitwise_vs_oracle(gpu, lbm, po, layout, vl, bc, nslabs):
+    """halo_exchange + propagate (kernels.cpp:197-258) on site-major y-slabs, whose storage is y-major:
+    bc brings the neighbours' face columns into the ghost columns and propagate pulls with the faces
+    resolved in the kernel -- bit-exact against the oracle's propagate of the whole lattice (VERDICT r1:
+    these verbs used to return UNSUPPORTED); propagate without a preceding bc is refused."""
+    lx, ly = 128, 96 * nslabs  # y-major storage: lx / vl >= 3
+    init = lbm.make_lattice("random", lx, ly, seed=91)
+    grp = lbm.SlabGroup(layout, lx, ly, vl, nslabs, bc=bc)
+    grp.load(init)
+    with pytest.raises(ValueError, match="bc"):
+        grp.slabs[-1].propagate_only()
+    grp.slabs[0].bc(bc)  # one group-wide exchange fills every slab's ghost columns
+    for s in grp.slabs:
+        s.propagate_only()
+    got = np.concatenate([s.dump(which=1) for s in grp.slabs], axis=2)
+    assert np.array_equal(got, po.orc_propagate(init, po.BC_WALL if bc == "wall" else po.BC_PERIODIC))
