@@ -19,6 +19,12 @@ LAYOUTS = [("aos", 1), ("soa", 1), ("csoa", 1), ("csoa", 2), ("csoa", 4), ("csoa
            ("caosoa", 2), ("caosoa", 4), ("caosoa", 8)]
 
 
+P2P_EMULATION = pytest.mark.skipif(
+    not __import__("os").environ.get("D2Q37_P2P_EMULATION"),
+    reason="several P2P slabs on ONE GPU spin on each other's counters (nothing guarantees co-scheduling, "
+           "B200_PROFILING.md): opt in with D2Q37_P2P_EMULATION=1; the 1-rank self rings stay on")
+
+
 def sim_of(lbm, layout, lx, ly, vl=1, **kw):
     return lbm.Simulation(layout, lx, ly, vl, device=0, **kw)
 
@@ -677,6 +683,7 @@ def test_p2p_self_ring_bitwise_equals_single_domain(gpu, lbm, layout, vl, varian
     assert s.exposed_halo_ms() >= 0.0
 
 
+@P2P_EMULATION
 @pytest.mark.parametrize("nslabs", [2, 4])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 @pytest.mark.parametrize("layout,vl,variant", [("caosoa", 8, "fused"), ("caosoa", 32, "fused"),
@@ -747,6 +754,7 @@ def test_p2p_connect_across_processes_maps_ipc(gpu, lbm, tmp_path):
     a.close()
 
 
+@P2P_EMULATION
 @pytest.mark.slow
 def test_p2p_ring_full_size_bitwise(gpu, lbm):
     """The bench lattice (4096 x 16384, CAoSoA32, walls) as a 2-slab P2P ring in one process:
@@ -838,6 +846,7 @@ def test_run_validation_same_seed_same_report(gpu, lbm):
     assert a == b and not a.passed
 
 
+@P2P_EMULATION
 @pytest.mark.parametrize("layout,vl", [("caosoa", 32), ("csoa", 8)])
 def test_create_multi_bitwise_equals_single_domain(gpu, lbm, layout, vl):
     """d2q37_create_multi / d2q37_multi_step (single-process multi-GPU): 3 slabs, here all on
@@ -854,6 +863,7 @@ def test_create_multi_bitwise_equals_single_domain(gpu, lbm, layout, vl):
     m.close()
 
 
+@P2P_EMULATION
 def test_p2p_missing_neighbour_reports_instead_of_hanging(gpu, lbm):
     """Failure detection: slab 0 of a 2-slab ring steps while slab 1 never does; with
     D2Q37_P2P_TIMEOUT_S=1 the wait gives up and sync raises instead of hanging."""
