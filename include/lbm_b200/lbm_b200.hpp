@@ -50,7 +50,9 @@ inline void check(int rc) {
     }
 }
 
-enum class LayoutKind { AoS = D2Q37_AOS, SoA = D2Q37_SOA, CSoA = D2Q37_CSOA, CAoSoA = D2Q37_CAOSOA };
+// Banded: the device store of the two-step sweep (no reference counterpart; FUSED2 / FUSED steps,
+// load / dump / files / convert only -- see d2q37_b200.h).
+enum class LayoutKind { AoS = D2Q37_AOS, SoA = D2Q37_SOA, CSoA = D2Q37_CSOA, CAoSoA = D2Q37_CAOSOA, Banded = D2Q37_BANDED };
 enum class Boundary { Periodic = D2Q37_BC_PERIODIC, Wall = D2Q37_BC_WALL };
 enum class StepVariant { Unfused = D2Q37_UNFUSED, Fused = D2Q37_FUSED, Fused2 = D2Q37_FUSED2 };
 enum class Math { Fast = D2Q37_MATH_FAST, Strict = D2Q37_MATH_STRICT };
