@@ -184,6 +184,16 @@ int d2q37_scalar_steps(const d2q37_model* m, int lx, int ly, const double* host_
  * for a given geometry.  Conservation checks at full size. */
 int d2q37_moments(d2q37_lattice* h, double out[4]);
 
+/* Per-site host verbs of VelocityModel (model.hpp:60-72), in the reference's
+ * operation order on the host (no FMA contraction): macros_of -> {rho, ux,
+ * uy, temp} (model.cpp:242-257; D2Q37_ERR_NON_PHYSICAL when !(rho > 0)),
+ * equilibrium from {rho, ux, uy, temp} (model.cpp:259-291), collide_site
+ * (model.cpp:293-298).  m = NULL uses d2q37_model_d2q37.  Inspection / test
+ * helpers; the lattice-wide arithmetic runs on the GPU. */
+int d2q37_macros_of(const d2q37_model* m, const double f[37], double out[4]);
+int d2q37_equilibrium(const d2q37_model* m, const double macros[4], double f_eq[37]);
+int d2q37_collide_site(const d2q37_model* m, const double f[37], double omega, double out[37]);
+
 /* Host initialisers -> canonical array (n = 37*lx*ly); params per kind above;
  * nthreads host threads for the equilibrium evaluation (<= 0: all cores). */
 int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* params,

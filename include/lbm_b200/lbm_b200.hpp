@@ -16,6 +16,7 @@
 // ThreadPool / KernelOptions arguments of the reference have no counterpart.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <stdexcept>
@@ -62,6 +63,14 @@ struct IVec2 {
     int y = 0;
 };
 
+/// Per-site macroscopic fields (model.hpp:21-26).
+struct Macros {
+    double rho = 0.0;
+    double ux = 0.0;
+    double uy = 0.0;
+    double temp = 0.0;
+};
+
 /// VelocityModel (model.hpp:50-100): the constants the kernels need.
 class VelocityModel {
   public:
@@ -81,10 +90,34 @@ class VelocityModel {
     }
     IVec2 velocity(int i) const { return {raw_.cx[i], raw_.cy[i]}; }
     double weight(int i) const { return raw_.w[i]; }
+    std::array<IVec2, kNpop> velocities() const {
+        std::array<IVec2, kNpop> v{};
+        for (int i = 0; i < kNpop; ++i) v[i] = velocity(i);
+        return v;
+    }
+    std::array<double, kNpop> weights() const {
+        std::array<double, kNpop> w{};
+        for (int i = 0; i < kNpop; ++i) w[i] = raw_.w[i];
+        return w;
+    }
     double t0() const { return raw_.t0; }
     int halo_extent() const { return kHaloExtent; }
     const d2q37_model& raw() const { return raw_; }
+    /// Per-site verbs (model.hpp:60-72), host arithmetic in the reference's order.
+    Macros macros_of(const double* f) const {
+        double m[4];
+        check(d2q37_macros_of(&raw_, f, m));
+        return {m[0], m[1], m[2], m[3]};
+    }
+    void equilibrium(const Macros& m, double* f_eq) const {
+        const double mac[4] = {m.rho, m.ux, m.uy, m.temp};
+        check(d2q37_equilibrium(&raw_, mac, f_eq));
+    }
+    void collide_site(const double* f, double omega, double* out) const {
+        check(d2q37_collide_site(&raw_, f, omega, out));
+    }
     static constexpr int kCollideFlopsPerSite = 1522;
+    static constexpr int kEqMoments = D2Q37_NMOM;
 
   private:
     d2q37_model raw_{};

@@ -1717,6 +1717,36 @@ int d2q37_convert(d2q37_lattice* src, d2q37_lattice* dst) {
     return D2Q37_OK;
 }
 
+namespace {
+const d2q37_model& model_or_default(const d2q37_model* m) {
+    static const d2q37_model def = [] {
+        d2q37_model d;
+        build_model(&d);
+        return d;
+    }();
+    return m ? *m : def;
+}
+}  // namespace
+
+int d2q37_macros_of(const d2q37_model* m, const double f[37], double out[4]) {
+    if (!f || !out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "macros_of: null array");
+    if (!host_macros(model_or_default(m), f, out)) return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
+    return D2Q37_OK;
+}
+
+int d2q37_equilibrium(const d2q37_model* m, const double macros[4], double f_eq[37]) {
+    if (!macros || !f_eq) return fail(D2Q37_ERR_INVALID_ARGUMENT, "equilibrium: null array");
+    host_equilibrium(model_or_default(m), macros[0], macros[1], macros[2], macros[3], f_eq);
+    return D2Q37_OK;
+}
+
+int d2q37_collide_site(const d2q37_model* m, const double f[37], double omega, double out[37]) {
+    if (!f || !out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "collide_site: null array");
+    if (!host_collide_site(model_or_default(m), f, omega, out))
+        return fail(D2Q37_ERR_NON_PHYSICAL, "non-positive density");
+    return D2Q37_OK;
+}
+
 int d2q37_make_lattice(int kind, int lx, int ly, uint64_t seed, const double* params, const d2q37_model* m,
                        double* out, size_t n, int nthreads) {
     if (lx < 1 || ly < 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "lattice extents must be positive");

@@ -124,6 +124,35 @@ void host_equilibrium(const d2q37_model& m, double rho, double ux, double uy, do
     }
 }
 
+// Host per-site verbs of VelocityModel (model.hpp:60-72) in the reference's
+// operation order: macros_of (model.cpp:242-257: four separate reductions in
+// population order) and collide_site (model.cpp:293-298).  Returns false when
+// !(rho > 0) (NonPhysicalError).
+bool host_macros(const d2q37_model& m, const double* f, double out[4]) {
+    double rho = 0.0;
+    for (int i = 0; i < kNpop; ++i) rho += f[i];
+    if (!(rho > 0.0)) return false;
+    double jx = 0.0, jy = 0.0, e2 = 0.0;
+    for (int i = 0; i < kNpop; ++i) jx += double(m.cx[i]) * f[i];
+    for (int i = 0; i < kNpop; ++i) jy += double(m.cy[i]) * f[i];
+    for (int i = 0; i < kNpop; ++i) e2 += double(m.cx[i] * m.cx[i] + m.cy[i] * m.cy[i]) * f[i];
+    const double inv_rho = 1.0 / rho;
+    const double ux = jx * inv_rho, uy = jy * inv_rho;
+    out[0] = rho;
+    out[1] = ux;
+    out[2] = uy;
+    out[3] = 0.5 * (e2 * inv_rho - (ux * ux + uy * uy));
+    return true;
+}
+
+bool host_collide_site(const d2q37_model& m, const double* f, double omega, double* out) {
+    double mac[4], feq[kNpop];
+    if (!host_macros(m, f, mac)) return false;
+    host_equilibrium(m, mac[0], mac[1], mac[2], mac[3], feq);
+    for (int i = 0; i < kNpop; ++i) out[i] = f[i] + omega * (feq[i] - f[i]);
+    return true;
+}
+
 void philox4x32_10(const uint32_t in[4], const uint32_t key[2], uint32_t out[4]) {
     uint32_t c[4] = {in[0], in[1], in[2], in[3]};
     uint32_t k0 = key[0], k1 = key[1];

@@ -12,6 +12,8 @@ constexpr int kHostNpop = D2Q37_NPOP;
 
 void build_model(d2q37_model* m);
 void host_equilibrium(const d2q37_model& m, double rho, double ux, double uy, double temp, double* f_eq);
+bool host_macros(const d2q37_model& m, const double* f, double out[4]);
+bool host_collide_site(const d2q37_model& m, const double* f, double omega, double* out);
 void philox4x32_10(const uint32_t in[4], const uint32_t key[2], uint32_t out[4]);
 double philox_u01(uint64_t seed, uint64_t counter);
 void make_lattice(int kind, int lx, int ly, uint64_t seed, const double* params, const d2q37_model& m,

@@ -18,13 +18,20 @@
 //   G8  run_validation's scalar device reference <= 1e-12 vs the reference's
 //       oracle_propagate + oracle_collide (5 steps); convert between device
 //       layouts preserves every physical site                           (validation.cpp, layout.cpp:105-116)
-//   G9  a 4-slab MultiGpuLattice (P2P halos; all slabs on device 0 here)
-//       <= 1e-12 vs the reference lbm::step over 6 periodic steps
+//   G9  a MultiGpuLattice (P2P halos) <= 1e-12 vs the reference lbm::step over
+//       6 periodic steps: one slab per device listed in D2Q37_G9_DEVICES
+//       (default "0": a 1-slab ring that waits only on its own stream --
+//       several slabs on one GPU would spin on each other's counters)
 //   G10 StepVariant::Fused2 (two steps per HBM sweep) on SoA: 10 steps
 //       <= 1e-12 vs the reference lbm::step, and bit for bit == 10 fused steps
+//   G11 VelocityModel per-site verbs (model.hpp:60-72): macros_of,
+//       equilibrium and collide_site <= 1e-14 vs the reference's on random
+//       sites; macros_of of a non-positive density throws NonPhysicalError
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -263,16 +270,49 @@ bool g9() {
     ref.load(init);
     lbm::ThreadPool pool(4);
     for (int n = 0; n < 6; ++n) lbm::step(ref, m, 1.05, pool);
-    lbm_b200::MultiGpuLattice gpu(B::CAoSoA, lbm_b200::Geometry{96, 256, 3, 3, 8}, {0, 0, 0, 0});
+    std::vector<int> devs;
+    const char* env = std::getenv("D2Q37_G9_DEVICES");
+    for (const char* c = env ? env : "0"; *c; ++c)
+        if (*c >= '0' && *c <= '9') devs.push_back(*c - '0');
+    lbm_b200::MultiGpuLattice gpu(B::CAoSoA, lbm_b200::Geometry{96, 256, 3, 3, 8}, devs);
     gpu.load(to_gpu(init));
     gpu.step(reference_model(), 1.05, 6);
     return max_rel(gpu.dump().values, ref.dump().values) <= 1e-12;
 }
 
+bool g11() {
+    const lbm::VelocityModel& r = lbm::VelocityModel::d2q37();
+    const lbm_b200::VelocityModel& d = lbm_b200::VelocityModel::d2q37();
+    const lbm::CanonicalLattice lat = lbm::make_random_lattice(8, 16, 1111);
+    auto rel = [](double a, double b) { return std::abs(a - b) / std::max(std::abs(b), 1e-300); };
+    for (int site = 0; site < 8 * 16; ++site) {
+        double f[37], outr[37], outd[37], feqr[37], feqd[37];
+        for (int p = 0; p < 37; ++p) f[p] = lat.values[size_t(p) * 8 * 16 + site];
+        const lbm::Macros mr = r.macros_of(f);
+        const lbm_b200::Macros md = d.macros_of(f);
+        if (rel(md.rho, mr.rho) > 1e-14 || rel(md.temp, mr.temp) > 1e-14) return false;
+        if (std::abs(md.ux - mr.ux) > 1e-14 || std::abs(md.uy - mr.uy) > 1e-14) return false;
+        r.equilibrium(mr, feqr);
+        d.equilibrium(md, feqd);
+        r.collide_site(f, 1.3, outr);
+        d.collide_site(f, 1.3, outd);
+        for (int p = 0; p < 37; ++p)
+            if (rel(feqd[p], feqr[p]) > 1e-14 || rel(outd[p], outr[p]) > 1e-14) return false;
+    }
+    double bad[37] = {};
+    bad[0] = -1.0;
+    try {
+        (void)d.macros_of(bad);
+        return false;
+    } catch (const lbm_b200::NonPhysicalError&) {
+    }
+    return true;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::array<std::pair<const char*, bool (*)()>, 10> all = {{{"G1", g1},
+    const std::array<std::pair<const char*, bool (*)()>, 11> all = {{{"G1", g1},
                                                                      {"G2", g2},
                                                                      {"G3", g3},
                                                                      {"G4", g4},
@@ -281,7 +321,8 @@ int main(int argc, char** argv) {
                                                                      {"G7", g7},
                                                                      {"G8", g8},
                                                                      {"G9", g9},
-                                                                     {"G10", g10}}};
+                                                                     {"G10", g10},
+                                                                     {"G11", g11}}};
     int failures = 0;
     for (const auto& [name, fn] : all) {
         if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;

@@ -27,10 +27,19 @@ def test_metric_criterion_runs_without_gpu():
     assert r.returncode == 0 and "G6 PASS" in r.stdout, r.stdout + r.stderr
 
 
+def test_per_site_verbs_without_gpu():
+    """G11 (host arithmetic): VelocityModel::macros_of / equilibrium / collide_site of the drop-in
+    header against the reference's own (model.hpp:60-72), and NonPhysicalError."""
+    if not os.access(EXE, os.X_OK):
+        pytest.skip("parity program not built")
+    r = subprocess.run([EXE, "G11"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "G11 PASS" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.gpu
 def test_cpp_parity_all_criteria(gpu):
     assert os.access(EXE, os.X_OK), "tests/cpp/_build/parity missing: run __graft_entry__.build() in the build container"
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 10
+    assert r.stdout.count("PASS") == 11

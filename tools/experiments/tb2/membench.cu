@@ -37,6 +37,8 @@ __constant__ int c_gs[8] = {0, 3, 8, 15, 22, 29, 34, 37};
 
 // MODE 0: SoA planes (the library's FUSED2 store): element (p, x, y) at p*plane + x*cs + y.
 // MODE 2: SoA reads, band-blocked writes.  MODE 3: band-blocked reads, SoA writes.
+// MODE 9: exact 120-row blocks; the 6-row halos read straight from the neighbouring blocks (per
+//         population, 48 B each: 7 group copies + 74 small copies per column), exact writes.
 // MODE 8: exact 120-row blocks plus separate halo arrays LO/HI[x][b][s][8] (contiguous per column):
 //         21 copies per column (main, lo, hi of each cx group), halo copies written as contiguous runs.
 // MODE 5: MODE 4 without the halo copies.  MODE 6: MODE 4 reads, MODE 1 writes.
@@ -56,8 +58,9 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
     if (threadIdx.x < NST) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + threadIdx.x)));
     asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    const int ip = MODE == 8 ? lane : (MODE >= 4) ? 2 * warp + lane : warp * 10 + lane;
-    const bool issuer = MODE == 8 ? (prod && warp < 3 && lane < 7)
+    const int ip = MODE == 9 ? warp * 32 + lane : MODE == 8 ? lane : (MODE >= 4) ? 2 * warp + lane : warp * 10 + lane;
+    const bool issuer = MODE == 9 ? (prod && ip < 7 + 2 * kNpop)
+                      : MODE == 8 ? (prod && warp < 3 && lane < 7)
                                   : (MODE >= 4) ? (prod && lane < 2 && ip < 7) : (prod && lane < 10 && ip < kNpop);
     const long long hsz = (long long)(lx + 8) * nbands * kNpop * 8;  // one halo array (doubles)
     const long long mainsz = (long long)(lx + 8) * nbands * kNpop * 120;
@@ -77,7 +80,32 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
         auto wr = [&](int v) { return v < 0 ? v + lx : (v >= lx ? v - lx : v); };
         auto issue = [&](int t) {
             const int st = issued % NST;
-            if (issuer && MODE == 8) {
+            if (issuer && MODE == 9) {
+                const int k = ip < 7 ? ip : (ip - 7) % kNpop;  // group (main) or population (halo)
+                const int cxk = ip < 7 ? k - 3 : c_cx[k];
+                const int col = wr(wr(xs - 3 + t) - cxk);
+                const long long blk = (long long)col * nbands + band;
+                const double* s;
+                double* d;
+                unsigned bytes;
+                if (ip < 7) {
+                    const int gs = c_gs[k], gn = c_gs[k + 1] - gs;
+                    s = src + (blk * kNpop + gs) * 120;
+                    d = sm + st * kNpop * kRows + gs * 120;
+                    bytes = gn * 120 * 8;
+                } else {
+                    const bool lo = ip - 7 < kNpop;
+                    const long long nb = lo ? (band > 0 ? blk - 1 : blk) : (band + 1 < nbands ? blk + 1 : blk);
+                    s = src + (nb * kNpop + k) * 120 + (lo ? 114 : 0);
+                    d = sm + st * kNpop * kRows + kNpop * 120 + (lo ? 0 : kNpop * 6) + k * 6;
+                    bytes = 48;
+                }
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sa(d)),
+                    "l"(s), "r"(bytes), "r"(sa(bar + st))
+                    : "memory");
+            } else if (issuer && MODE == 8) {
                 const int col = wr(wr(xs - 3 + t) - icx);
                 const int gs = c_gs[ip], gn = c_gs[ip + 1] - gs;
                 const long long blk = (long long)col * nbands + band;
@@ -110,7 +138,7 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
             }
             if (threadIdx.x == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar + st)),
-                             "r"((MODE >= 4) ? kNpop * 136 * 8 : kNpop * kRows * 8)
+                             "r"(MODE == 9 ? kNpop * 132 * 8 : (MODE >= 4) ? kNpop * 136 * 8 : kNpop * kRows * 8)
                              : "memory");
             ++issued;
         };
@@ -218,9 +246,10 @@ int main(int argc, char** argv) {
     };
     for (int delay : {0}) {
         run(k_mem<2, 1, 120>, 2, delay, 120, 1);
-        run(k_mem<2, 4, 120>, 2, delay, 120, 4);
         run(k_mem<2, 8, 120>, 2, delay, 120, 8);
-        run(k_mem<1, 8, 120>, 1, delay, 120, 8);
+        run(k_mem<2, 9, 120>, 2, delay, 120, 9);
+        run(k_mem<1, 9, 120>, 1, delay, 120, 9);
+        run(k_mem<2, 0, 120>, 2, delay, 120, 0);
     }
     return 0;
 }
