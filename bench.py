@@ -731,19 +731,26 @@ def run_b200(args, dist: Dist):
     fused_ms, fused_n = kt["fused"]
     dom = "fused" if fused_n else "collide"
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
-    # FUSED2: one launch per sweep (k_step2_split: interior bands beside the face bands)
+    form = None if STUB else lbm.set_fused2_tuning(-1, -1)[0]
+    pair = args.variant == "fused2" and args.layout == "soa" and form == 4 and transport is None
+    if pair:  # two launches per sweep: k_step2_pair (interior) beside k_step2_split (the two wall bands)
+        launches += fused_n
+    # FUSED2: one sweep per timed "fused" interval (k_step2_pair + the face bands' k_step2_split beside it)
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
     upd = steps_per_call(args.variant) if dom == "fused" else 1
     achieved = sites_local * BYTES_PER_SITE / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
     step_ms = ms_max / args.steps
     two = upd == 2
     roofline = {"bound": "hbm",
-                "kernel": ("k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "
-                           "interior bands beside the two wall bands in one launch)" if two else
+                "kernel": (("k_step2_pair (two fused pull+collide steps per HBM sweep, temporal blocking; two "
+                            "threads per site, 512-thread CTAs, lockstep band schedule) beside k_step2_split on "
+                            "the two wall bands; the sweep interval covers both" if pair else
+                            "k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "
+                            "interior bands beside the two wall bands in one launch)") if two else
                            "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak if achieved else None,
-                "traffic": load_ncu_traffic(args.layout, ly_local, args.variant),
+                "traffic": load_ncu_traffic(args.layout, ly_local, args.variant, pair),
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": sites_local * BYTES_PER_SITE,
                 "time_steps_per_launch": upd,
@@ -921,12 +928,12 @@ def run_e2e(lbm, sim, args, dist: Dist):
             "call": f"Simulation.load(host canonical) + step(0.8, n, {sim.variant}, wall) + dump(host canonical)"}
 
 
-def load_ncu_traffic(layout: str, ly: int, variant: str = "fused"):
+def load_ncu_traffic(layout: str, ly: int, variant: str = "fused", pair: bool = False):
     """DRAM bytes/launch of the step kernel from the committed ncu capture (profiles/), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_fused_traffic.json")
     key = {"csoa": "prof_fused_csoa", "caosoa": "prof_fused_caosoa"}.get(layout, "prof_fused")
     if variant == "fused2" and layout == "soa":
-        key = "prof_step2_soa"
+        key = "prof_step2_pair" if pair else "prof_step2_soa"
     try:
         with open(path) as f:
             rec = json.load(f)[key]

@@ -286,16 +286,29 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
 /* FUSED2 tuning (no reference counterpart; process-wide).  form: how the
- * interior bands of a two-step sweep on the SoA store pull step 1 --
- * 0 (default, measured fastest) per-thread loads, 1 bulk copies staged in
- * shared memory (cp.async.bulk + mbarrier) issued after the moments, 2 the
- * same issued as soon as the stage is in registers; all bit-identical.
+ * interior bands of a two-step sweep on the SoA store are swept -- 0
+ * per-thread loads (one thread per site, 185-column ring), 1 one bulk-copy
+ * stage (cp.async.bulk + mbarrier) issued after the moments, 2 the same
+ * issued as soon as the stage is in registers, 3 two bulk-copy stages beside
+ * a 148-column ring (named-barrier hand-off), 4 (default, measured fastest)
+ * form 3 with two threads per site (512-thread CTAs, the pair's partial
+ * moments swapped through tensor memory; the face bands then run in a
+ * general-form launch beside it); all bit-identical.
  * face_pct: items per face-band CTA relative to an interior CTA, in percent
- * of the interior's cost (0 = the form's default: 115 / 135 for forms 0 / 1-2).
+ * of the interior's cost (0 = the form's default: 115 / 135 for forms 0 / 1-4).
  * A negative argument leaves a setting unchanged; the previous values are
  * returned through prev_form / prev_face_pct when non-null.  Environment:
  * D2Q37_STEP2_FORM, D2Q37_STEP2_FACE_PCT. */
 int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct);
+
+/* FUSED2 interior schedule (no reference counterpart; process-wide; form 0
+ * only): 1 (default) lockstep -- persistent CTA c marches whole bands c,
+ * c + G, ... from column 0, so neighbouring bands sweep the same columns at
+ * the same time (their shared pull rows are L2 hits, each population plane is
+ * streamed as a few column-long runs); 0 band-major item ranges.  Both are
+ * bit-identical.  A negative argument leaves it unchanged; the previous value
+ * is returned through prev_sched when non-null.  Environment: D2Q37_STEP2_SCHED. */
+int d2q37_set_fused2_schedule(int sched, int* prev_sched);
 
 /* Measurement helper (no reference counterpart): the achieved FP64 rate of
  * independent DFMA chains on every SM of `device`, in TFLOP/s (2 FLOP per

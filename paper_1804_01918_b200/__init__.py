@@ -54,7 +54,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "lib", "libd2q37_b200.so")
+    """The in-tree build, or D2Q37_LIBRARY (A/B runs of another build of the same library)."""
+    return os.environ.get("D2Q37_LIBRARY") or os.path.join(_HERE, "lib", "libd2q37_b200.so")
 
 
 class NonPhysicalError(FloatingPointError):
@@ -143,6 +144,7 @@ def _load():
         "d2q37_scalar_steps": (i, [P(_Model), i, i, vp, vp, sz, d, i, i, i]),
         "d2q37_fp64_peak": (i, [i, P(C.c_double)]),
         "d2q37_set_fused2_tuning": (i, [i, i, P(C.c_int), P(C.c_int)]),
+        "d2q37_set_fused2_schedule": (i, [i, P(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -351,13 +353,23 @@ def fp64_peak(device: int = 0) -> float:
 
 
 def set_fused2_tuning(form: int = -1, face_pct: int = -1) -> tuple:
-    """Process-wide FUSED2 tuning (d2q37_set_fused2_tuning): ``form`` 0 = per-thread loads (default),
-    1 / 2 = interior bands staged by bulk copies (bit-identical); ``face_pct`` sizes the face-band CTA
+    """Process-wide FUSED2 tuning (d2q37_set_fused2_tuning): ``form`` 0 = per-thread loads, 1 / 2 =
+    interior bands staged by one bulk-copy stage, 3 = two stages, 4 = two stages and two threads per
+    site (default; all bit-identical); ``face_pct`` sizes the face-band CTA
     groups (0 = the form's default).  -1 leaves a setting unchanged.  Returns the previous
     (form, face_pct)."""
     pf, pp = C.c_int(0), C.c_int(0)
     _check(_load().d2q37_set_fused2_tuning(int(form), int(face_pct), C.byref(pf), C.byref(pp)))
     return pf.value, pp.value
+
+
+def set_fused2_schedule(sched: int = -1) -> int:
+    """Process-wide FUSED2 interior schedule (d2q37_set_fused2_schedule): 1 = lockstep (default; CTAs
+    of neighbouring bands march the same columns together), 0 = band-major item ranges.  Both are
+    bit-identical.  -1 leaves it unchanged.  Returns the previous schedule."""
+    prev = C.c_int(0)
+    _check(_load().d2q37_set_fused2_schedule(int(sched), C.byref(prev)))
+    return prev.value
 
 
 def nccl_unique_id() -> bytes:

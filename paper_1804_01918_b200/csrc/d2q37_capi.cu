@@ -80,6 +80,9 @@ struct d2q37_lattice {
     // NCCL slabs: pack / unpack / boundary sites run on a high-priority stream
     // concurrently with the interior kernel (disjoint sites), joined per step.
     cudaStream_t halo_stream = nullptr;
+    // FUSED2 pair form: the face bands' general-form launch runs beside the interior one
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_start = nullptr, ev_bnd = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
     cudaEvent_t ev_int[kEventRing] = {}, ev_wait[kEventRing] = {};
@@ -340,6 +343,7 @@ void free_lattice(d2q37_lattice* h) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
     if (h->halo_stream) cudaStreamSynchronize(h->halo_stream);
+    if (h->side_stream) cudaStreamSynchronize(h->side_stream);
     if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
     for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->stage2, h->send_lo, h->send_hi, h->recv_lo,
                       h->recv_hi, h->h6[0], h->h6[1], h->h6[2], h->h6[3]})
@@ -367,6 +371,9 @@ void free_lattice(d2q37_lattice* h) {
     if (h->comm) nccl_comm_destroy(h->comm);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->halo_stream) cudaStreamDestroy(h->halo_stream);
+    if (h->side_stream) cudaStreamDestroy(h->side_stream);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ev_start) cudaEventDestroy(h->ev_start);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     h->stream_owner.reset();
@@ -653,6 +660,17 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
         // small lattices (a few persistent-CTA waves of items), or face bands too large a
         // share to split off: every band through the general form
         CK(launch_step2(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, 3, 0));
+    } else if (step2_form() == kStep2Pair) {
+        // two threads per site (512-thread CTAs) on the interior, the face bands' general form
+        // (256-thread CTAs) in a launch beside it on the side stream
+        if (!h->side_stream) {
+            CK(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        }
+        const int ctas[3] = {h->nsm - c_lo - c_hi, c_lo, c_hi};
+        CK(launch_step2_pair_split(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
+                                   h->ev_fork, h->ev_join, ctas));
     } else {
         const int ctas[3] = {h->nsm - c_lo - c_hi, c_lo, c_hi};  // interior >= nsm / 2
         CK(launch_step2_split(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, ctas));
@@ -838,7 +856,7 @@ void drop_step_graph(d2q37_lattice* h) {
 int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     auto& gr = h->graph;
     if (gr.exec && gr.omega == omega && gr.variant == variant && gr.bc == bc && gr.cur == h->cur &&
-        gr.math == h->math && gr.model_gen == h->model_gen && gr.stream == h->stream && gr.form == step2_form())
+        gr.math == h->math && gr.model_gen == h->model_gen && gr.stream == h->stream && gr.form == 2 * step2_form() + step2_sched())
         return D2Q37_OK;
     drop_step_graph(h);
     const int cur0 = h->cur;
@@ -877,7 +895,7 @@ int ensure_step_graph(d2q37_lattice* h, double omega, int variant, int bc) {
     gr.math = h->math;
     gr.model_gen = h->model_gen;
     gr.stream = h->stream;
-    gr.form = step2_form();
+    gr.form = 2 * step2_form() + step2_sched();
     return D2Q37_OK;
 }
 
@@ -1558,7 +1576,8 @@ int d2q37_step(d2q37_lattice* h, double omega, int nsteps, int variant, int bc) 
                     }
                 }
                 for (; s + 2 <= nsteps; s += 2) RET(step2_local(h, omega, fc));
-            } else if (h->transport == kTransportNccl && h->comm_stream && step2_overlap()) {
+            } else if (h->transport == kTransportNccl && h->comm_stream && step2_overlap() && !h->g.band) {
+                // (the overlapped sweep k_step2_slab is the SoA store's; the banded store exchanges first)
                 for (; s + 2 <= nsteps; s += 2) {
                     if (!h->h6_valid) RET(step2_slab_exchange_nccl(h, bc));
                     RET(step2_sweep_overlapped(h, omega, bc, fc));
@@ -2213,9 +2232,16 @@ int d2q37_group_step(d2q37_lattice** slabs_in, int nslabs, double omega, int nst
 int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_face_pct) {
     if (prev_form) *prev_form = step2_form();
     if (prev_face_pct) *prev_face_pct = step2_face_pct();
-    if (form > 2 || face_pct > 1000) return fail(D2Q37_ERR_INVALID_ARGUMENT, "fused2 tuning: form %d, face_pct %d", form, face_pct);
+    if (form > 4 || face_pct > 1000) return fail(D2Q37_ERR_INVALID_ARGUMENT, "fused2 tuning: form %d, face_pct %d", form, face_pct);
     if (form >= 0) set_step2_form(form);
     if (face_pct >= 0) set_step2_face_pct(face_pct);
+    return D2Q37_OK;
+}
+
+int d2q37_set_fused2_schedule(int sched, int* prev_sched) {
+    if (prev_sched) *prev_sched = step2_sched();
+    if (sched > 1) return fail(D2Q37_ERR_INVALID_ARGUMENT, "fused2 schedule %d", sched);
+    if (sched >= 0) set_step2_sched(sched);
     return D2Q37_OK;
 }
 

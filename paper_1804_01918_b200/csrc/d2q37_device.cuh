@@ -264,47 +264,73 @@ struct SymMoments {
     double mom[kNmom];
 };
 
-#ifndef D2Q37_SPLIT_MOMENTS
-#define D2Q37_SPLIT_MOMENTS 0
-#endif
-__device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const ModelParams& mp, SymMoments& m) {
-#if D2Q37_SPLIT_MOMENTS
-    // four interleaved partial sums per moment: 10-deep dependency chains instead of 37
-    double r4[4] = {0.0, 0.0, 0.0, 0.0}, x4[4] = {0.0, 0.0, 0.0, 0.0}, y4[4] = {0.0, 0.0, 0.0, 0.0},
-           e4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i) r4[i & 3] += f[i];
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cx_of(i) != 0) x4[i & 3] = fma((double)cx_of(i), f[i], x4[i & 3]);
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cy_of(i) != 0) y4[i & 3] = fma((double)cy_of(i), f[i], y4[i & 3]);
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cx_of(i) != 0 || cy_of(i) != 0)
-            e4[i & 3] = fma((double)(cx_of(i) * cx_of(i) + cy_of(i) * cy_of(i)), f[i], e4[i & 3]);
-    const double rho = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+// Population halves of the FAST collide.  Half 0 ("A"): the rest velocity and
+// the quadruples (+-1, +-1), (+-2, +-1), (+-1, +-2), (+-2, +-2) (17
+// populations); half 1 ("B"): the three axis shells and the quadruples
+// (+-3, +-1), (+-1, +-3) (20) -- about equal moment and relaxation work
+// (65 / 68 and ~116 / ~129 FP64 operations).  Each half's relaxation is closed
+// (eq_axis / eq_quad groups), so the two-threads-per-site sweep
+// (d2q37_pair.cu) gives each thread of a pair one half; the moments are
+// summed per half (canonical order inside a half) and the halves added A + B,
+// the same order in every FAST kernel, so all of them stay bit-identical.
+D2Q37_HD constexpr int pop_half(int p) {
+    return (cx_of(p) == 0 && cy_of(p) == 0) ||
+                   (cx_of(p) != 0 && cy_of(p) != 0 && cx_of(p) * cx_of(p) <= 4 && cy_of(p) * cy_of(p) <= 4)
+               ? 0
+               : 1;
+}
+
+// Partial moment sums {rho, jx, jy, e2} of half H, group by group: a quadruple
+// (+-a, +-b) adds u1 - u2 (the cx = +a pair minus the cx = -a pair) to jx,
+// v1 - v2 to jy and their total S to rho and (a^2 + b^2) S to e2 -- 11 FP64
+// operations instead of 16 -- and an axis group (+-a, 0), (0, +-a) the same
+// in 9 instead of 12; per site 94 instead of ~145.  Fixed group order per
+// half: A = rest, (1,1), (2,1), (1,2), (2,2); B = axes 1, 2, 3, (3,1), (1,3).
+template <int A, int B>
+__device__ __forceinline__ void part_quad(const double (&f)[kNpop], double (&s)[4]) {
+    constexpr int pp = vel_index(A, B), mp = vel_index(-A, B), pm = vel_index(A, -B), mm = vel_index(-A, -B);
+    const double u1 = f[pp] + f[pm], u2 = f[mp] + f[mm];
+    const double v1 = f[pp] + f[mp], v2 = f[pm] + f[mm];
+    const double t = u1 + u2;
+    s[0] += t;
+    s[1] = fma(double(A), u1 - u2, s[1]);
+    s[2] = fma(double(B), v1 - v2, s[2]);
+    s[3] = fma(double(A * A + B * B), t, s[3]);
+}
+template <int A>
+__device__ __forceinline__ void part_axis(const double (&f)[kNpop], double (&s)[4]) {
+    constexpr int xp = vel_index(A, 0), xm = vel_index(-A, 0), yp = vel_index(0, A), ym = vel_index(0, -A);
+    const double t = (f[xp] + f[xm]) + (f[yp] + f[ym]);
+    s[0] += t;
+    s[1] = fma(double(A), f[xp] - f[xm], s[1]);
+    s[2] = fma(double(A), f[yp] - f[ym], s[2]);
+    s[3] = fma(double(A * A), t, s[3]);
+}
+template <int H>
+__device__ __forceinline__ void sym_partials(const double (&f)[kNpop], double (&s)[4]) {
+    if (H == 0) {
+        s[0] = f[0];
+        s[1] = s[2] = s[3] = 0.0;
+        part_quad<1, 1>(f, s);
+        part_quad<2, 1>(f, s);
+        part_quad<1, 2>(f, s);
+        part_quad<2, 2>(f, s);
+    } else {
+        s[0] = s[1] = s[2] = s[3] = 0.0;
+        part_axis<1>(f, s);
+        part_axis<2>(f, s);
+        part_axis<3>(f, s);
+        part_quad<3, 1>(f, s);
+        part_quad<1, 3>(f, s);
+    }
+}
+
+// the Hermite moment vector from the summed {rho, jx, jy, e2} (half A + half B)
+__device__ __forceinline__ bool sym_macros(const double (&a)[4], const double (&b)[4], const ModelParams& mp,
+                                           SymMoments& m) {
+    const double rho = a[0] + b[0];
     const bool bad = !(rho > 0.0);
-    const double jx = (x4[0] + x4[1]) + (x4[2] + x4[3]), jy = (y4[0] + y4[1]) + (y4[2] + y4[3]);
-    const double e2 = (e4[0] + e4[1]) + (e4[2] + e4[3]);
-#else
-    double rho = 0.0;
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i) rho += f[i];
-    const bool bad = !(rho > 0.0);
-    double jx = 0.0, jy = 0.0, e2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cx_of(i) != 0) jx = fma((double)cx_of(i), f[i], jx);
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cy_of(i) != 0) jy = fma((double)cy_of(i), f[i], jy);
-#pragma unroll
-    for (int i = 0; i < kNpop; ++i)
-        if (cx_of(i) != 0 || cy_of(i) != 0)
-            e2 = fma((double)(cx_of(i) * cx_of(i) + cy_of(i) * cy_of(i)), f[i], e2);
-#endif
+    const double jx = a[1] + b[1], jy = a[2] + b[2], e2 = a[3] + b[3];
     const double inv_rho = 1.0 / rho;
     const double ux = jx * inv_rho;
     const double uy = jy * inv_rho;
@@ -331,28 +357,46 @@ __device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const Mode
     return bad;
 }
 
-__device__ __forceinline__ void sym_relax(double (&f)[kNpop], const SymMoments& m, double omega,
-                                          const ModelParams& mp) {
+__device__ __forceinline__ bool sym_moments(const double (&f)[kNpop], const ModelParams& mp, SymMoments& m) {
+    double a[4], b[4];
+    sym_partials<0>(f, a);
+    sym_partials<1>(f, b);
+    return sym_macros(a, b, mp, m);
+}
+
+// relaxation of the populations of half H (sym_relax = both halves)
+template <int H>
+__device__ __forceinline__ void sym_relax_half(double (&f)[kNpop], const SymMoments& m, double omega,
+                                               const ModelParams& mp) {
     const double* mom = m.mom;
     const double rho = m.rho;
-    {  // rest velocity: even terms only
-        const double* g = mp.eq[0];
-        double ee = fma(g[2], mom[2], 1.0);
-        ee = fma(g[4], mom[4], ee);
-        ee = fma(g[9], mom[9], ee);
-        ee = fma(g[11], mom[11], ee);
-        ee = fma(g[13], mom[13], ee);
-        f[0] = fma(omega, fma(rho * mp.w[0], ee, -f[0]), f[0]);
+    if (H == 0) {
+        {  // rest velocity: even terms only
+            const double* g = mp.eq[0];
+            double ee = fma(g[2], mom[2], 1.0);
+            ee = fma(g[4], mom[4], ee);
+            ee = fma(g[9], mom[9], ee);
+            ee = fma(g[11], mom[11], ee);
+            ee = fma(g[13], mom[13], ee);
+            f[0] = fma(omega, fma(rho * mp.w[0], ee, -f[0]), f[0]);
+        }
+        eq_quad<1, 1>(f, mom, mp, rho, omega);
+        eq_quad<2, 1>(f, mom, mp, rho, omega);
+        eq_quad<1, 2>(f, mom, mp, rho, omega);
+        eq_quad<2, 2>(f, mom, mp, rho, omega);
+    } else {
+        eq_axis<1>(f, mom, mp, rho, omega);
+        eq_axis<2>(f, mom, mp, rho, omega);
+        eq_axis<3>(f, mom, mp, rho, omega);
+        eq_quad<3, 1>(f, mom, mp, rho, omega);
+        eq_quad<1, 3>(f, mom, mp, rho, omega);
     }
-    eq_axis<1>(f, mom, mp, rho, omega);
-    eq_axis<2>(f, mom, mp, rho, omega);
-    eq_axis<3>(f, mom, mp, rho, omega);
-    eq_quad<1, 1>(f, mom, mp, rho, omega);
-    eq_quad<2, 1>(f, mom, mp, rho, omega);
-    eq_quad<1, 2>(f, mom, mp, rho, omega);
-    eq_quad<2, 2>(f, mom, mp, rho, omega);
-    eq_quad<3, 1>(f, mom, mp, rho, omega);
-    eq_quad<1, 3>(f, mom, mp, rho, omega);
+}
+
+__device__ __forceinline__ void sym_relax(double (&f)[kNpop], const SymMoments& m, double omega,
+                                          const ModelParams& mp) {
+    sym_relax_half<0>(f, m, omega, mp);
+    sym_relax_half<1>(f, m, omega, mp);
 }
 
 __device__ __forceinline__ bool collide_site_sym(double (&f)[kNpop], double omega, const ModelParams& mp) {

@@ -125,9 +125,16 @@ long long step2_items(const DevGeo& g, const Faces& fc, int part);
 // default: measured fastest) or bulk copies staged in shared memory (sweep_tma;
 // 1 = issued after the moments, 2 = as soon as the stage is in registers).
 // Environment D2Q37_STEP2_FORM selects one.  set_step2_form returns the previous form.
-enum { kStep2Plain = 0, kStep2Bulk = 1, kStep2BulkEarly = 2 };
+// 3 = two bulk-copy stages beside a 148-column ring (sweep_tma2).
+// 4 = form 3 with two threads per site (k_step2_pair, d2q37_pair.cu).
+enum { kStep2Plain = 0, kStep2Bulk = 1, kStep2BulkEarly = 2, kStep2Bulk2 = 3, kStep2Pair = 4 };
 int step2_form();
 int set_step2_form(int form);
+// Interior schedule of the plain form: 1 = lockstep (CTAs of neighbouring bands
+// march the same columns together; the default), 0 = band-major item ranges.
+// Environment D2Q37_STEP2_SCHED selects one; set_step2_sched returns the previous.
+int step2_sched();
+int set_step2_sched(int sched);
 // percent cost of a face-band (general form) item relative to an interior item,
 // which sizes the face CTA groups of k_step2_split (0 = the form's default)
 int step2_face_pct();
@@ -137,6 +144,15 @@ size_t step2_smem_bytes(int form);
 // with items needs at least one).
 cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
                                const ModelParams& mp, double omega, int* flag, cudaStream_t s, const int ctas[3]);
+// The pair form (kStep2Pair): interior bands [band0, band0 + nb) by k_step2_pair on `ctas` CTAs (lock:
+// the lockstep schedule) ...
+cudaError_t launch_step2_pair(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                              double omega, int* flag, cudaStream_t s, int band0, int nb, int ctas, bool lock);
+// ... and a whole sweep in that form: part 0 by k_step2_pair on s, the face parts 1 and 2 by the
+// general form on `side` in the same interval (ev_fork / ev_join order it with s).
+cudaError_t launch_step2_pair_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                                    const ModelParams& mp, double omega, int* flag, cudaStream_t s, cudaStream_t side,
+                                    cudaEvent_t ev_fork, cudaEvent_t ev_join, const int ctas[3]);
 cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                          double omega, int* flag, cudaStream_t s, int part, int max_ctas);
 // Slab sweeps split in time (the overlapped FUSED2 slab schedule): bands

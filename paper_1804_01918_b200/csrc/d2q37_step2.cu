@@ -56,11 +56,10 @@ namespace d2q37 {
 // WRAPY: y-periodic lattice (rows wrap); otherwise rows are read unwrapped --
 // inside [0, ly) for bands away from the faces, and down to -6 / up to ly+5
 // (the deep ghost rows a slab's halo exchange fills) at ghost faces.
-template <bool WRAPY>
+template <bool WRAPY, class Sched>
 __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
-                                            const ModelParams& mp, double omega, int band0, int nbands,
-                                            long long item_begin, long long item_end_, int* __restrict__ flag,
-                                            double* __restrict__ send_lo = nullptr,
+                                            const ModelParams& mp, double omega, Sched sched,
+                                            int* __restrict__ flag, double* __restrict__ send_lo = nullptr,
                                             double* __restrict__ send_hi = nullptr) {
     extern __shared__ double ring[];
     const bool prod = threadIdx.x < kT2Band;
@@ -69,16 +68,10 @@ __device__ __forceinline__ void sweep_plain(const double* __restrict__ src, doub
     const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
     const long long plane = g.pstride, cs = g.cstride;
-    const long long total = (long long)nbands * lx;
-    long long item = item_begin;
-    const long long item_end = min(total, item_end_);
     auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
     bool bad = false;
-    while (item < item_end) {
-        const int band = band0 + (int)(item / lx);
-        const int xs = (int)(item % lx);
-        const int xe = (int)min((long long)lx, xs + (item_end - item));
-        item += xe - xs;
+    int band, xs, xe;
+    while (sched.next(band, xs, xe)) {
         const int y0 = band * kT2Out;
         const int ny = min(kT2Out, ly - y0);
         const int niter = xe - xs + 7;  // producer rows t = 0 .. niter-2, consumer t = 7 .. niter-1
@@ -268,6 +261,123 @@ __device__ __forceinline__ void sweep_tma(const double* __restrict__ src, double
     if (bad) atomicOr(flag, 1);
 }
 
+// Two-stage bulk-copy sweep (form kStep2Bulk2): the bulk-copy staging of
+// sweep_tma with TWO stages in flight -- column r + 2 is copied while column r
+// is collided and column r + 1 is landing -- which fits beside a 148-column
+// ring (t2n_depth: cx_p + 4) because producers and consumers hand the ring
+// over with named barriers instead of __syncthreads: the consumers read an
+// iteration's slots first (barrier 2 -> the producers may overwrite them),
+// the producers publish a step-1 column with barrier 3.  Stages: 2 x 38.5 KB;
+// ring 148 KB; 228.5 KB of shared memory.  Rows are read unwrapped (as
+// sweep_tma).  Bit-identical to the other forms (same gathered values, same
+// collide_site_sym).
+template <bool GHOST, class Sched>
+__device__ __forceinline__ void sweep_tma2(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
+                                           const ModelParams& mp, double omega, Sched sched,
+                                           int* __restrict__ flag) {
+    extern __shared__ double ring[];
+    double* const stage0 = ring + kT2NRingCols * kT2Band;  // 2 stages [37][130]
+    unsigned long long* const full = reinterpret_cast<unsigned long long*>(stage0 + 2 * kNpop * kStageRows);
+    const bool prod = threadIdx.x < kT2Band;
+    const int tid = threadIdx.x & (kT2Band - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = g.lx, ly = g.ly;
+    const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
+    double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
+    const long long plane = g.pstride, cs = g.cstride;
+    auto wr = [](int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); };
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        mbar_init(full + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    // copy issue: producer warp w, lane l < 10 -> population 10 w + l
+    const int ip = warp * 10 + lane;
+    const bool issuer = prod && lane < 10 && ip < kNpop;
+    const int icx = issuer ? c_cx[ip] : 0, icy = issuer ? c_cy[ip] : 0;
+    unsigned issued = 0, used = 0;  // stage columns issued / consumed (stage = n & 1)
+    bool bad = false;
+    int band, xs, xe;
+    while (sched.next(band, xs, xe)) {
+        const int y0 = band * kT2Out;
+        const int ny = min(kT2Out, ly - y0);
+        const int niter = xe - xs + 7;  // producer columns xs-3 .. xe+2 at t = 0 .. niter-2; outputs at t >= 7
+        if (prod) {
+            const double* const isrc = sb + ip * plane + ((y0 - kHalo - icy) & ~1);
+            auto issue = [&](int r) {
+                const unsigned st = issued & 1u;
+                if (issuer) {
+                    const int col = wr(wr(r, lx) - icx, lx);
+                    bulk_g2s(stage0 + (st * kNpop + ip) * kStageRows, isrc + (long long)col * cs,
+                             kStageRows * sizeof(double), full + st);
+                }
+                if (threadIdx.x == 0) mbar_arrive_expect_tx(full + st, kStageBytes);
+                ++issued;
+            };
+            for (int k = 0; k < 2 && k < niter - 1; ++k) issue(xs - kHalo + k);
+            // stage offset of this thread's step-1 row (y1 - cy_p - row0_p = yo + ((y0-3-cy_p) & 1))
+            const int yo = GHOST ? min(tid, ly + kHalo - 1 - (y0 - kHalo)) : tid;
+            const int par = (y0 - kHalo) & 1;
+#pragma unroll 1
+            for (int t = 0; t < niter - 1; ++t) {
+                const unsigned st = used & 1u;
+                mbar_wait(full + st, (used >> 1) & 1u);
+                ++used;
+                const double* const sg = stage0 + st * kNpop * kStageRows;
+                double f[kNpop];
+                for_pops([&](auto P) {
+                    constexpr int p = decltype(P)::value;
+                    f[p] = sg[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
+                });
+                // the 37 values are in registers (an empty asm consumes them): the stage is free
+#pragma unroll
+                for (int p = 0; p < kNpop; p += 6)
+                    asm volatile("" ::"d"(f[p]), "d"(f[min(p + 1, kNpop - 1)]), "d"(f[min(p + 2, kNpop - 1)]),
+                                 "d"(f[min(p + 3, kNpop - 1)]), "d"(f[min(p + 4, kNpop - 1)]),
+                                 "d"(f[min(p + 5, kNpop - 1)]));
+                bad |= collide_site_sym(f, omega, mp);
+                // the consumers have read this iteration's slots -- and every producer has read the
+                // stage (before its collide): refill it with column t + 2
+                nbar_sync(2);
+                if (t + 2 < niter - 1) issue(xs - kHalo + t + 2);
+                for_pops([&](auto P) {
+                    constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
+                    ring[(rb + t % dp) * kT2Band + tid] = f[p];
+                });
+                nbar_arrive(3);
+            }
+            nbar_sync(2);  // the consumers' last iteration
+        } else {
+#pragma unroll 1
+            for (int t = 0; t < niter; ++t) {
+                if (t > 0) nbar_sync(3);  // step-1 column t - 1 is in the ring
+                const bool work = t >= 7 && tid < ny;
+                double v[kNpop];
+                if (work) {  // column c - cx_p, produced at t - 4 - cx_p: slot t % depth
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
+                        v[p] = ring[(rb + t % dp) * kT2Band + tid + kHalo - cy_of(p)];
+                    });
+#pragma unroll
+                    for (int p = 0; p < kNpop; p += 6)
+                        asm volatile("" ::"d"(v[p]), "d"(v[min(p + 1, kNpop - 1)]), "d"(v[min(p + 2, kNpop - 1)]),
+                                     "d"(v[min(p + 3, kNpop - 1)]), "d"(v[min(p + 4, kNpop - 1)]),
+                                     "d"(v[min(p + 5, kNpop - 1)]));
+                }
+                nbar_arrive(2);
+                if (work) {
+                    bad |= collide_site_sym(v, omega, mp);
+                    const long long e = (long long)(xs - 7 + t) * cs + y0 + tid;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(db + p * plane + e, v[p]);
+                }
+            }
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
 // General sweep: any band, every face kind (periodic wrap, wall image, slab
 // ghost rows) through per-thread row tables.  Launched on the face bands only
 // (k_step2_plain covers the rest).
@@ -419,7 +529,8 @@ template <bool WRAPY>
 __global__ void __launch_bounds__(2 * kT2Band, 1)
     k_step2_plain(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
                   int band0, int nbands, long long per_cta, int* __restrict__ flag) {
-    sweep_plain<WRAPY>(src, dst, g, mp, omega, band0, nbands, blockIdx.x * per_cta, (blockIdx.x + 1) * per_cta, flag);
+    sweep_plain<WRAPY>(src, dst, g, mp, omega, RangeSched(band0, nbands, g.lx, blockIdx.x * per_cta, (blockIdx.x + 1) * per_cta),
+                       flag);
 }
 
 __global__ void __launch_bounds__(2 * kT2Band, 1)
@@ -435,6 +546,8 @@ struct Step2Split {
     int band0[3], nb[3], ctas[3];
     long long per_cta[3];
     int form;  // interior bands: 0 = sweep_plain, 1 = sweep_tma
+    int lock;  // interior bands of the plain form: the lockstep schedule (LockSched)
+    Lockstep ls;
 };
 
 __global__ void __launch_bounds__(2 * kT2Band, 1)
@@ -442,7 +555,15 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                   double omega, Step2Split sp, int* __restrict__ flag) {
     int cta = blockIdx.x;
     if (cta < sp.ctas[0]) {
-        if (sp.form == kStep2Bulk) {
+        if (sp.form == kStep2Bulk2) {
+            const PartSched ps{sp.lock != 0,
+                               RangeSched(sp.band0[0], sp.nb[0], g.lx, cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0]),
+                               LockSched(sp.band0[0], g.lx, sp.ctas[0], cta, sp.ls)};
+            if (fc.hi == kFaceGhost)
+                sweep_tma2<true>(src, dst, g, mp, omega, ps, flag);
+            else
+                sweep_tma2<false>(src, dst, g, mp, omega, ps, flag);
+        } else if (sp.form == kStep2Bulk) {
             if (fc.hi == kFaceGhost)
                 sweep_tma<true, false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
             else
@@ -452,10 +573,14 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
                 sweep_tma<true, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
             else
                 sweep_tma<false, true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
-        } else if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic) {
-            sweep_plain<true>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
         } else {
-            sweep_plain<false>(src, dst, g, mp, omega, sp.band0[0], sp.nb[0], cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0], flag);
+            const PartSched ps{sp.lock != 0,
+                               RangeSched(sp.band0[0], sp.nb[0], g.lx, cta * sp.per_cta[0], (cta + 1) * sp.per_cta[0]),
+                               LockSched(sp.band0[0], g.lx, sp.ctas[0], cta, sp.ls)};
+            if (fc.lo == kFacePeriodic && fc.hi == kFacePeriodic)
+                sweep_plain<true>(src, dst, g, mp, omega, ps, flag);
+            else
+                sweep_plain<false>(src, dst, g, mp, omega, ps, flag);
         }
         return;
     }
@@ -493,7 +618,8 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
         if ((lo ? fc.lo : fc.hi) == kFaceWall)  // a global wall: the general form mirrors
             sweep_general(src, dst, g, fc, mp, omega, b0, nb, c * per, (c + 1) * per, flag, send_lo, send_hi);
         else  // ghost rows: read unwrapped by the plain form
-            sweep_plain<false>(src, dst, g, mp, omega, b0, nb, c * per, (c + 1) * per, flag, send_lo, send_hi);
+            sweep_plain<false>(src, dst, g, mp, omega, RangeSched(b0, nb, g.lx, c * per, (c + 1) * per), flag, send_lo,
+                               send_hi);
         __syncthreads();  // every consumer's face rows (lattice and send buffers) are stored
         if (threadIdx.x == 0) {
             __threadfence_system();
@@ -501,7 +627,8 @@ __global__ void __launch_bounds__(2 * kT2Band, 1)
         }
     }
     if (sp.in_off[cta] < sp.in_off[cta + 1])
-        sweep_plain<false>(src, dst, g, mp, omega, sp.in_band0, sp.in_nb, sp.in_off[cta], sp.in_off[cta + 1], flag);
+        sweep_plain<false>(src, dst, g, mp, omega, RangeSched(sp.in_band0, sp.in_nb, g.lx, sp.in_off[cta], sp.in_off[cta + 1]),
+                           flag);
 }
 
 // 6-row slab halos of FUSED2: rows 0..5 / ly-6..ly-1 of every physical column
@@ -561,6 +688,8 @@ bool step2_supported(const DevGeo& g, const Faces& fc) {
 
 size_t step2_smem_bytes(int form) {
     const size_t ring = (size_t)kT2RingCols * kT2Band * sizeof(double);
+    if (form == kStep2Bulk2)  // 148-column ring + two stages and their mbarriers
+        return (size_t)kT2NRingCols * kT2Band * sizeof(double) + 2 * size_t(kStageBytes) + 16;
     return form != kStep2Plain ? ring + kStageBytes + 16 : ring;  // + the stage and its mbarrier
 }
 
@@ -571,14 +700,32 @@ int g_form = -1;  // interior-band form of every FUSED2 sweep (step2_form)
 int step2_form() {
     if (g_form < 0) {
         const char* v = std::getenv("D2Q37_STEP2_FORM");
-        g_form = v && *v ? std::min(2, std::max(0, std::atoi(v))) : kStep2Plain;  // measured fastest (DESIGN 3.1)
+        g_form = v && *v ? std::min(4, std::max(0, std::atoi(v))) : kStep2Pair;  // measured fastest (DESIGN 3.1)
     }
     return g_form;
 }
 
 int set_step2_form(int form) {
     const int prev = step2_form();
-    g_form = std::min(2, std::max(0, form));
+    g_form = std::min(4, std::max(0, form));
+    return prev;
+}
+
+namespace {
+int g_sched = -1;  // interior schedule of the plain form: 0 = band-major ranges, 1 = lockstep
+}  // namespace
+
+int step2_sched() {
+    if (g_sched < 0) {
+        const char* v = std::getenv("D2Q37_STEP2_SCHED");
+        g_sched = v && *v ? (std::atoi(v) != 0) : 1;
+    }
+    return g_sched;
+}
+
+int set_step2_sched(int sched) {
+    const int prev = step2_sched();
+    g_sched = sched != 0;
     return prev;
 }
 
@@ -609,7 +756,7 @@ void step2_bands(const DevGeo& g, const Faces& fc, int form, int* nbands, int* b
     int lo = 0, hi = *nbands;
     const int inside_hi = g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0;  // bands with rows < ly
     if (per_lo && per_hi) {
-        if (form == kStep2Bulk) lo = 1, hi = inside_hi;
+        if (form != kStep2Plain) lo = 1, hi = inside_hi;  // the bulk-copy forms read rows unwrapped
     } else {
         // ghost faces read the deep ghost rows unwrapped; wall bands need the general form
         lo = fc.lo == kFaceWall ? 1 : 0;
@@ -638,7 +785,8 @@ int device_nsm(cudaError_t* err) {
     int nsm = (e == cudaSuccess && dev < kMaxDev) ? nsm_of[dev] : 0;
     if (e == cudaSuccess && nsm == 0) {
         e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const int ring = (int)step2_smem_bytes(kStep2Plain), bulk = (int)step2_smem_bytes(kStep2Bulk);
+        const int ring = (int)step2_smem_bytes(kStep2Plain),
+                  bulk = (int)std::max(step2_smem_bytes(kStep2Bulk), step2_smem_bytes(kStep2Bulk2));
         if (e == cudaSuccess) e = cudaFuncSetAttribute(k_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_step2_plain<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring);
@@ -779,6 +927,7 @@ cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, 
     if (e != cudaSuccess) return e;
     Step2Split sp{};
     sp.form = step2_form();
+    sp.lock = (sp.form == kStep2Plain || sp.form == kStep2Bulk2) && step2_sched();
     int grid = 0;
     for (int part = 0; part < 3; ++part) {
         part_range(g, fc, sp.form, part, &sp.band0[part], &sp.nb[part]);
@@ -789,8 +938,43 @@ cudaError_t launch_step2_split(const double* src, double* dst, const DevGeo& g, 
         grid += sp.ctas[part];
     }
     if (grid == 0) return cudaSuccess;
+    if (sp.lock && sp.ctas[0] > 0) sp.ls = lockstep_plan(sp.nb[0], sp.ctas[0], g.lx);
     k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(sp.form), s>>>(src, dst, g, fc, mp, omega, sp, flag);
     return cudaGetLastError();
+}
+
+cudaError_t launch_step2_pair_split(const double* src, double* dst, const DevGeo& g, const Faces& fc,
+                                    const ModelParams& mp, double omega, int* flag, cudaStream_t s, cudaStream_t side,
+                                    cudaEvent_t ev_fork, cudaEvent_t ev_join, const int ctas[3]) {
+    cudaError_t e;
+    device_nsm(&e);
+    if (e != cudaSuccess) return e;
+    Step2Split sp{};
+    sp.form = kStep2Plain;  // unused: part 0 has no CTA in the face launch
+    int band0 = 0, nb0 = 0, grid = 0;
+    part_range(g, fc, kStep2Pair, 0, &band0, &nb0);
+    for (int part = 1; part < 3; ++part) {
+        part_range(g, fc, kStep2Pair, part, &sp.band0[part], &sp.nb[part]);
+        const long long total = (long long)std::max(0, sp.nb[part]) * g.lx;
+        sp.ctas[part] = total > 0 ? (int)std::min<long long>(ctas[part], total) : 0;
+        if (total > 0 && sp.ctas[part] < 1) return cudaErrorInvalidValue;
+        sp.per_cta[part] = sp.ctas[part] ? (total + sp.ctas[part] - 1) / sp.ctas[part] : 0;
+        grid += sp.ctas[part];
+    }
+    if (grid > 0) {
+        if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return e;
+        k_step2_split<<<grid, 2 * kT2Band, step2_smem_bytes(kStep2Plain), side>>>(src, dst, g, fc, mp, omega, sp, flag);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (nb0 > 0 && (e = launch_step2_pair(src, dst, g, fc, mp, omega, flag, s, band0, nb0, ctas[0], step2_sched() != 0)) !=
+                       cudaSuccess)
+        return e;
+    if (grid > 0) {
+        if ((e = cudaEventRecord(ev_join, side)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace d2q37

@@ -1066,6 +1066,35 @@ def test_fused2_split_launch_bitwise(gpu, lbm, bc):
     assert np.array_equal(grp.dump(), ref.dump())
 
 
+@pytest.mark.parametrize("lx,ly,bc", [(4096, 2048, "wall"), (4096, 2048, "periodic"), (16384, 400, "wall"),
+                                       (256, 20000, "wall"), (1000, 6000, "periodic")])
+def test_fused2_interior_forms_and_schedules_bitwise(gpu, lbm, lx, ly, bc):
+    """Every interior form of a FUSED2 sweep (0 per-thread loads, 1 / 3 bulk-copy stages, 4 two threads
+    per site with the pair's partial moments swapped through tensor memory) under both schedules
+    (band-major ranges; lockstep -- whole bands per CTA, a tail round, more bands than CTAs at
+    256 x 20000) is bit-identical to fused steps (kernels.cpp:276-283 twice per sweep)."""
+    ref = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused")
+    ref.init_rt_device(7)
+    ref.step(0.8, 4)
+    want = ref.dump()
+    ref.close()
+    prev_form, _ = lbm.set_fused2_tuning(-1, -1)
+    prev_sched = lbm.set_fused2_schedule(-1)
+    try:
+        for form, sched in ((0, 0), (0, 1), (1, 0), (3, 0), (3, 1), (4, 0), (4, 1)):
+            lbm.set_fused2_tuning(form, -1)
+            lbm.set_fused2_schedule(sched)
+            s = sim_of(lbm, "soa", lx, ly, bc=bc, variant="fused2")
+            s.init_rt_device(7)
+            s.step(0.8, 4)
+            got = s.dump()
+            s.close()
+            assert np.array_equal(got, want), (form, sched)
+    finally:
+        lbm.set_fused2_tuning(prev_form, -1)
+        lbm.set_fused2_schedule(prev_sched)
+
+
 @pytest.mark.parametrize("lx,ly", [(2, 5), (3, 6), (6, 130), (4, 250)])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 def test_fused2_degenerate_extents_bitwise(gpu, lbm, lx, ly, bc):

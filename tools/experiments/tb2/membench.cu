@@ -50,7 +50,7 @@ __constant__ int c_gs[8] = {0, 3, 8, 15, 22, 29, 34, 37};
 template <int NST, int MODE, int kOut>
 __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, double* __restrict__ dst, int lx,
                                                 int ly, long long cs, long long plane, int nbands, long long per_cta,
-                                                int delay, unsigned long long* waitcyc) {
+                                                int delay, unsigned long long* waitcyc, int lock) {
     extern __shared__ double sm[];
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + NST * kNpop * kRows);
     const bool prod = threadIdx.x < kBand;
@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
     const long long hsz = (long long)(lx + 8) * nbands * kNpop * 8;  // one halo array (doubles)
     const long long mainsz = (long long)(lx + 8) * nbands * kNpop * 120;
     const int icx = (MODE >= 4) ? ip - 3 : (issuer ? c_cx[ip] : 0), icy = (MODE >= 4) ? 0 : (issuer ? c_cy[ip] : 0);
-    long long item = (long long)blockIdx.x * per_cta;
-    const long long end = min((long long)nbands * lx, item + per_cta);
+    // lock: CTA b marches band b over every column (lockstep: neighbouring bands at the same columns)
+    long long item = lock ? (long long)blockIdx.x * lx : (long long)blockIdx.x * per_cta;
+    const long long end = min((long long)nbands * lx, item + (lock ? lx : per_cta));
     unsigned ph[NST > 0 ? NST : 1] = {};
     unsigned long long waited = 0;
     double acc = 0.0;
@@ -220,7 +221,7 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    auto run = [&](auto kern, int nst, int delay, int kOut, int mode) {
+    auto run = [&](auto kern, int nst, int delay, int kOut, int mode, int lock = 0) {
         const int nbands = ly / kOut - 1;
         const long long items = (long long)nbands * lx, per = (items + nsm - 1) / nsm;
         const int smem = nst * kNpop * kRows * 8 + 64;
@@ -229,7 +230,7 @@ int main(int argc, char** argv) {
         for (int r = 0; r < 4; ++r) {
             CK(cudaMemset(wc, 0, 8));
             CK(cudaEventRecord(e0));
-            kern<<<nsm, 256, smem>>>(a + 8, b + 8, lx, ly, cs, plane, nbands, per, delay, wc);
+            kern<<<lock ? std::min(nbands, nsm) : nsm, 256, smem>>>(a + 8, b + 8, lx, ly, cs, plane, nbands, per, delay, wc, lock);
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms;
@@ -239,17 +240,18 @@ int main(int argc, char** argv) {
         unsigned long long w = 0;
         CK(cudaMemcpy(&w, wc, 8, cudaMemcpyDeviceToHost));
         const double sites = (double)nbands * kOut * lx;
-        printf("mode %d out %d stages %d delay %5d: %7.3f ms  %7.1f GB/s algorithmic (592 B/site)  %6.2f ns/column  producer wait "
+        printf("lock %d mode %d out %d stages %d delay %5d: %7.3f ms  %7.1f GB/s algorithmic (592 B/site)  %6.2f ns/column  producer wait "
                "%.1f%%\n",
-               mode, kOut, nst, delay, best, sites * 592 / (best * 1e6), best * 1e6 / (double)(per + 7),
+               lock, mode, kOut, nst, delay, best, sites * 592 / (best * 1e6), best * 1e6 / (double)(per + 7),
                100.0 * w / (double)nsm / ((double)best * 1e-3 * 1.9e9));
     };
-    for (int delay : {0}) {
-        run(k_mem<2, 1, 120>, 2, delay, 120, 1);
-        run(k_mem<2, 8, 120>, 2, delay, 120, 8);
-        run(k_mem<2, 9, 120>, 2, delay, 120, 9);
-        run(k_mem<1, 9, 120>, 1, delay, 120, 9);
-        run(k_mem<2, 0, 120>, 2, delay, 120, 0);
+    for (int delay : {0, 2000}) {
+        for (int lock : {0, 1}) {
+            run(k_mem<1, 0, 120>, 1, delay, 120, 0, lock);
+            run(k_mem<2, 0, 120>, 2, delay, 120, 0, lock);
+            run(k_mem<3, 0, 120>, 3, delay, 120, 0, lock);
+            run(k_mem<4, 0, 120>, 4, delay, 120, 0, lock);
+        }
     }
     return 0;
 }
