@@ -310,6 +310,17 @@ int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_fa
  * is returned through prev_sched when non-null.  Environment: D2Q37_STEP2_SCHED. */
 int d2q37_set_fused2_schedule(int sched, int* prev_sched);
 
+/* Test hooks (no reference counterpart).  d2q37_debug_step2_slab_sweep: one
+ * overlapped FUSED2 slab sweep of h's current state with faces face_lo /
+ * face_hi (1 = wall, 3 = ghost: the 6 deep ghost rows are read as they stand,
+ * nothing is exchanged) in the pair form (form 4) or the one-thread form
+ * (any other), the new edge rows packed into the halo send buffers;
+ * d2q37_debug_read_halo6 copies send buffer `which` (0 low, 1 high; 37 x lx x 6
+ * doubles, [p][x][row]) to host.  They let one GPU check the two slab sweeps
+ * against each other on the face combinations of a multi-GPU run. */
+int d2q37_debug_step2_slab_sweep(d2q37_lattice* h, double omega, int form, int face_lo, int face_hi);
+int d2q37_debug_read_halo6(d2q37_lattice* h, int which, double* host, size_t n);
+
 /* Measurement helper (no reference counterpart): the achieved FP64 rate of
  * independent DFMA chains on every SM of `device`, in TFLOP/s (2 FLOP per
  * DFMA) -- the FP64 roofline denominator at the clocks the GPU holds under

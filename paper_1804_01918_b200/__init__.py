@@ -145,6 +145,8 @@ def _load():
         "d2q37_fp64_peak": (i, [i, P(C.c_double)]),
         "d2q37_set_fused2_tuning": (i, [i, i, P(C.c_int), P(C.c_int)]),
         "d2q37_set_fused2_schedule": (i, [i, P(C.c_int)]),
+        "d2q37_debug_step2_slab_sweep": (i, [vp, d, i, i, i]),
+        "d2q37_debug_read_halo6": (i, [vp, i, P(d), sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -644,6 +646,19 @@ class Simulation:
 
     def exposed_halo_ms(self) -> float:
         return float(_load().d2q37_exposed_halo_ms(self._h))
+
+    def debug_step2_slab_sweep(self, omega: float, form: int, face_lo: str, face_hi: str):
+        """Test hook (d2q37_debug_step2_slab_sweep): one overlapped FUSED2 slab sweep with the given faces
+        ("wall" / "ghost"; ghost rows read as they stand, nothing exchanged), form 4 = pair form."""
+        f = {"wall": 1, "ghost": 3}
+        _check(_load().d2q37_debug_step2_slab_sweep(self._h, float(omega), int(form), f[face_lo], f[face_hi]))
+
+    def debug_read_halo6(self, which: int) -> np.ndarray:
+        """Test hook: FUSED2 halo send buffer `which` (0 low, 1 high) as [37][lx][6]."""
+        out = np.empty((37, self.lx, 6))
+        _check(_load().d2q37_debug_read_halo6(self._h, int(which), out.ctypes.data_as(C.POINTER(C.c_double)),
+                                              out.size))
+        return out
 
     def moments(self) -> np.ndarray:
         out = np.empty(4)

@@ -626,6 +626,15 @@ int step_local(d2q37_lattice* h, double omega, int variant, int bc) {
     return D2Q37_OK;
 }
 
+// the side stream of the pair form's general-form launches (face / wall bands beside the pair launch)
+int ensure_side_stream(d2q37_lattice* h) {
+    if (h->side_stream) return D2Q37_OK;
+    CK(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    return D2Q37_OK;
+}
+
 // Two time steps in one HBM sweep (D2Q37_FUSED2, d2q37_step2.cu).
 // One sweep.  The interior bands (plain form) and the face bands (general
 // form) write disjoint rows, so on a large lattice one launch runs them side
@@ -663,11 +672,7 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
     } else if (step2_form() == kStep2Pair) {
         // two threads per site (512-thread CTAs) on the interior, the face bands' general form
         // (256-thread CTAs) in a launch beside it on the side stream
-        if (!h->side_stream) {
-            CK(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-        }
+        RET(ensure_side_stream(h));
         const int ctas[3] = {h->nsm - c_lo - c_hi, c_lo, c_hi};
         CK(launch_step2_pair_split(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
                                    h->ev_fork, h->ev_join, ctas));
@@ -785,10 +790,19 @@ int step2_sweep_overlapped(d2q37_lattice* h, double omega, int bc, const Faces& 
     int nsig = 0;
     if (wait) {
         ProfScope ps(h, kProfFused);
-        cudaError_t err;
-        nsig = launch_step2_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid, h->d_sweep_counter,
-                                 h->h6[0], h->h6[1], &err);
-        CK(err);
+        cudaError_t err = cudaSuccess;
+        if (step2_form() == kStep2Pair) {  // the two-threads-per-site form (wall faces beside it)
+            RET(ensure_side_stream(h));
+            nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
+                                          h->ev_fork, h->ev_join, h->nsm - std::min(step2_halo_sms(), h->nsm / 4),
+                                          h->d_sweep_counter, h->h6[0], h->h6[1], &err);
+            CK(err);
+        }
+        if (nsig == 0) {
+            nsig = launch_step2_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid,
+                                     h->d_sweep_counter, h->h6[0], h->h6[1], &err);
+            CK(err);
+        }
     }
     if (nsig == 0) {  // no overlapped form for this slab (small, periodic face): the serial schedule
         RET(step2_local(h, omega, fc));
@@ -2235,6 +2249,55 @@ int d2q37_set_fused2_tuning(int form, int face_pct, int* prev_form, int* prev_fa
     if (form > 4 || face_pct > 1000) return fail(D2Q37_ERR_INVALID_ARGUMENT, "fused2 tuning: form %d, face_pct %d", form, face_pct);
     if (form >= 0) set_step2_form(form);
     if (face_pct >= 0) set_step2_face_pct(face_pct);
+    return D2Q37_OK;
+}
+
+// Test hook: one overlapped FUSED2 slab sweep of this lattice's current state with the given faces
+// (1 wall, 3 ghost: the deep ghost rows are read as they stand; no exchange), interior form `form`
+// (kStep2Pair: k_step2_pair_slab, else k_step2_slab), the new edge rows packed into the halo buffers.
+int d2q37_debug_step2_slab_sweep(d2q37_lattice* h, double omega, int form, int face_lo, int face_hi) {
+    RET(check_handle(h));
+    auto face_ok = [](int f) { return f == kFaceWall || f == kFaceGhost; };
+    if (!face_ok(face_lo) || !face_ok(face_hi) || h->layout != D2Q37_SOA || !h->g.deep)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "debug slab sweep: SoA lattice with deep ghost rows, faces 1 / 3");
+    DeviceGuard dg(h->device);
+    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    RET(ensure_halo6(h));
+    RET(ensure_side_stream(h));
+    if (!h->d_sweep_counter) {
+        CK(cudaMalloc(&h->d_sweep_counter, sizeof(unsigned)));
+        CK(cudaMemset(h->d_sweep_counter, 0, sizeof(unsigned)));
+    }
+    Faces fc = step_faces(h, D2Q37_BC_PERIODIC);
+    fc.lo = face_lo;
+    fc.hi = face_hi;
+    const double* src = h->buf[h->cur];
+    double* dst = h->buf[1 - h->cur];
+    const int grid = h->nsm - std::min(step2_halo_sms(), h->nsm / 4);
+    cudaError_t err = cudaSuccess;
+    int nsig = 0;
+    if (form == kStep2Pair)
+        nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
+                                      h->ev_fork, h->ev_join, grid, h->d_sweep_counter, h->h6[0], h->h6[1], &err);
+    else
+        nsig = launch_step2_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid, h->d_sweep_counter,
+                                 h->h6[0], h->h6[1], &err);
+    CK(err);
+    if (nsig == 0) return fail(D2Q37_ERR_UNSUPPORTED, "debug slab sweep: no overlapped form for this lattice");
+    h->cur = 1 - h->cur;
+    h->time_step += 2;
+    h->h6_valid = false;
+    return d2q37_sync(h);
+}
+
+// Test hook: the FUSED2 halo send buffers ([p][x][6] doubles; which = 0 low face, 1 high face).
+int d2q37_debug_read_halo6(d2q37_lattice* h, int which, double* host, size_t n) {
+    RET(check_handle(h));
+    if (!h->h6[0] || (which != 0 && which != 1) || n != halo6_count(h->g))
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "debug read halo6: no buffers or size mismatch");
+    DeviceGuard dg(h->device);
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(host, h->h6[which], n * sizeof(double), cudaMemcpyDeviceToHost));
     return D2Q37_OK;
 }
 

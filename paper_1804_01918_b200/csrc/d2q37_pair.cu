@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "d2q37_device.cuh"
 #include "d2q37_fused2.cuh"
@@ -42,13 +43,6 @@ namespace d2q37 {
 namespace {
 
 constexpr int kPairThreads = 4 * kT2Band;  // 512
-// Who refills a stage with column t + 2, and when (A/B experiment): 0 the producers after the hand-off
-// barrier (no extra barrier), 1 the producers after a producer-wide barrier right after the stage reads,
-// 3 the consumer warps 8-11 once every producer warp has arrived on the stage's "empty" mbarrier, 4 the
-// consumer warps 8-11 right after the hand-off barrier 3 (the producers have passed barrier 2).
-#ifndef D2Q37_PAIR_REFILL
-#define D2Q37_PAIR_REFILL 0
-#endif
 constexpr int kTmemCols = 64;              // [role][parity][half] x 8 32-bit columns (4 doubles)
 
 __device__ __forceinline__ void tmem_st8(unsigned taddr, const double (&v)[4]) {
@@ -100,6 +94,21 @@ __device__ __forceinline__ bool pair_collide(double (&f)[kNpop], const ModelPara
     return bad;
 }
 
+// t % d for the ring depths d = 1 .. 7 (t2n_depth), advanced once per iteration instead of seven
+// divisions by constants per iteration
+struct SlotClock {
+    int s[7];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) s[i] = 0;
+    }
+    __device__ __forceinline__ void tick() {
+#pragma unroll
+        for (int i = 1; i < 7; ++i) s[i] = s[i] == i ? 0 : s[i] + 1;
+    }
+    __device__ __forceinline__ int operator[](int depth) const { return s[depth - 1]; }
+};
+
 template <typename F>
 __device__ __forceinline__ void consume_regs(const double (&v)[kNpop], F&& in_set) {
     // an empty asm per value of the set: the loads have landed (the stage / ring slots may be reused)
@@ -110,23 +119,22 @@ __device__ __forceinline__ void consume_regs(const double (&v)[kNpop], F&& in_se
 }
 
 // Bulk-copy staging of the producers' pulls: copy n (a whole column, 37 x 1040 B, completion counted on
-// full[n & 1]) fills the stage of producer use n.  With D2Q37_PAIR_REFILL 3 the consumer warps issue the
-// copies, waiting first until use n - 2 of that stage is released on empty[n & 1] (one arrival per producer
-// warp); otherwise producer warps issue them at the point the variant fixes.
+// full[n & 1]) fills the stage of producer use n.  Producer warps 0-3 issue the copies of column t + 2
+// right after the hand-off barrier 2 of iteration t -- every producer has read the stage of iteration t
+// before its collide.  (Measured against earlier refills -- a producer-wide barrier after the stage
+// reads, an "empty" mbarrier with one issuing warp or with the consumers issuing: all slower, DESIGN 3.1.1.)
 struct StageIssuer {
     const double* sb;
     double* stage0;
     unsigned long long* full;
-    unsigned long long* empty;
     long long plane, cs;
     int lx, ip, icx, icy;
     bool issuer, leader;
     unsigned issued;
     const double* isrc;
     __device__ __forceinline__ void set_band(int y0) { isrc = sb + ip * plane + ((y0 - kHalo - icy) & ~1); }
-    __device__ __forceinline__ void issue(int r, bool wait_empty) {
+    __device__ __forceinline__ void issue(int r) {
         const unsigned st = issued & 1u;
-        if (wait_empty && issued >= 2) mbar_wait(empty + st, ((issued >> 1) + 1) & 1u);
         if (issuer) {
             int col = r < 0 ? r + lx : (r >= lx ? r - lx : r);
             col -= icx;
@@ -140,20 +148,19 @@ struct StageIssuer {
 };
 
 __device__ __forceinline__ StageIssuer make_issuer(const double* sb, const DevGeo& g, double* stage0,
-                                                   unsigned long long* full, int first_warp) {
+                                                   unsigned long long* full) {
     StageIssuer is;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     is.sb = sb;
     is.stage0 = stage0;
     is.full = full;
-    is.empty = full + 2;
     is.plane = g.pstride;
     is.cs = g.cstride;
     is.lx = g.lx;
-    // warps first_warp .. +3, lane l < 10 -> population 10 (w - first_warp) + l
-    is.ip = (warp - first_warp) * 10 + lane;
-    is.issuer = warp >= first_warp && warp < first_warp + 4 && lane < 10 && is.ip < kNpop;
-    is.leader = (int)threadIdx.x == first_warp * 32;
+    // warps 0-3, lane l < 10 -> population 10 w + l
+    is.ip = warp * 10 + lane;
+    is.issuer = warp < 4 && lane < 10 && is.ip < kNpop;
+    is.leader = threadIdx.x == 0;
     if (!is.issuer) is.ip = 0;
     is.icx = is.issuer ? c_cx[is.ip] : 0;
     is.icy = is.issuer ? c_cy[is.ip] : 0;
@@ -162,28 +169,52 @@ __device__ __forceinline__ StageIssuer make_issuer(const double* sb, const DevGe
     return is;
 }
 
+// Item schedule of a y-slab face CTA (k_step2_pair_slab): its share of the face band(s) -- whose new
+// edge rows go to the send buffers and, once stored, are announced on the sweep counter -- then its
+// share of the interior bands next to them.
+struct FaceSched {
+    RangeSched face, adj;
+    bool in_face;
+    __device__ __forceinline__ bool next(int& band, int& xs, int& xe) {
+        if (in_face) {
+            if (face.next(band, xs, xe)) return true;
+            in_face = false;
+        }
+        return adj.next(band, xs, xe);
+    }
+};
+
+// Send-buffer packing and the sweep counter of a face CTA (null: none)
+struct SlabPack {
+    double* send_lo;
+    double* send_hi;
+    unsigned* counter;
+};
+
+template <class Sched>
+__device__ __forceinline__ bool sched_in_face(const Sched&) { return false; }
+__device__ __forceinline__ bool sched_in_face(const FaceSched& s) { return s.in_face; }
+
 template <int H, bool GHOST, class Sched>
 __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, const DevGeo& g, const ModelParams& mp,
                                               double omega, Sched sched, double* ring, double* stage0,
                                               unsigned long long* full, unsigned tbase, bool& bad) {
-    unsigned long long* const empty = full + 2;
     const int tid = threadIdx.x & (kT2Band - 1);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int ly = g.ly;
     const int pbar = 4 + (warp & 3);
-    constexpr bool kProdIssue = D2Q37_PAIR_REFILL < 3;
-    StageIssuer is = make_issuer(sb, g, stage0, full, 0);
+    StageIssuer is = make_issuer(sb, g, stage0, full);
     unsigned used = 0;
     int band, xs, xe;
     while (sched.next(band, xs, xe)) {
         const int y0 = band * kT2Out;
         const int niter = xe - xs + 7;
-        if (kProdIssue) {
-            is.set_band(y0);
-            for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k, false);
-        }
+        is.set_band(y0);
+        for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k);
         const int yo = GHOST ? min(tid, ly + kHalo - 1 - (y0 - kHalo)) : tid;
         const int par = (y0 - kHalo) & 1;
+        SlotClock clk;
+        clk.reset();
 #pragma unroll 1
         for (int t = 0; t < niter - 1; ++t) {
             const unsigned st = used & 1u;
@@ -196,25 +227,16 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
                 if (pop_half(p) == H) f[p] = sg[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
             });
             consume_regs(f, [](int p) { return pop_half(p) == H; });
-#if D2Q37_PAIR_REFILL == 1
-            if (t + 2 < niter - 1) {
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // every producer has its values: refill
-                is.issue(xs - kHalo + t + 2, false);
-            }
-#elif D2Q37_PAIR_REFILL == 3
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + st);  // this warp has read the stage
-#endif
             bad |= pair_collide<H>(f, mp, omega, tbase, 0, t & 1, pbar);
-            asm volatile("bar.sync 2, 512;" ::: "memory");  // the consumers have read this iteration's slots
-#if D2Q37_PAIR_REFILL == 0
-            // ... and every producer has read the stage (before its collide): refill it with column t + 2
-            if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2, false);
-#endif
+            // the consumers have read this iteration's slots -- and every producer has read the stage
+            // (before its collide): refill it with column t + 2
+            asm volatile("bar.sync 2, 512;" ::: "memory");
+            if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2);
             for_pops([&](auto P) {
                 constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
-                if (pop_half(p) == H) ring[(rb + t % dp) * kT2Band + tid] = f[p];
+                if (pop_half(p) == H) ring[(rb + clk[dp]) * kT2Band + tid] = f[p];
             });
+            clk.tick();
             asm volatile("bar.arrive 3, 512;" ::: "memory");
         }
         asm volatile("bar.sync 2, 512;" ::: "memory");  // the consumers' last iteration
@@ -222,70 +244,97 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
 }
 
 template <int H, class Sched>
-__device__ __forceinline__ void pair_consumer(const double* __restrict__ sb, double* __restrict__ db, const DevGeo& g,
-                                              const ModelParams& mp, double omega, Sched sched, const double* ring,
-                                              double* stage0, unsigned long long* full, unsigned tbase, bool& bad) {
+__device__ __forceinline__ void pair_consumer(double* __restrict__ db, const DevGeo& g, const ModelParams& mp,
+                                              double omega, Sched sched, const double* ring, unsigned tbase,
+                                              const SlabPack& pk, bool& bad) {
     const int tid = threadIdx.x & (kT2Band - 1);
     const int warp = threadIdx.x >> 5;
-    const int ly = g.ly;
+    const int lx = g.lx, ly = g.ly;
     const long long plane = g.pstride, cs = g.cstride;
     const int cbar = 8 + (warp & 3);
-    constexpr bool kConsIssue = (D2Q37_PAIR_REFILL == 3 || D2Q37_PAIR_REFILL == 4) && H == 0;  // warps 8-11
-    StageIssuer is = make_issuer(sb, g, stage0, full, 8);
     int band, xs, xe;
+    bool was_face = sched_in_face(sched);
     while (sched.next(band, xs, xe)) {
+        const bool face = sched_in_face(sched);
+        if (was_face && !face) {
+            // every consumer's face rows (lattice and send buffers) are stored: announce them
+            asm volatile("bar.sync 12, 256;" ::: "memory");
+            if (threadIdx.x == 2 * kT2Band) {
+                __threadfence_system();
+                atomicAdd(pk.counter, 1u);
+            }
+        }
+        was_face = face;
         const int y0 = band * kT2Out;
         const int ny = min(kT2Out, ly - y0);
         const int niter = xe - xs + 7;
         const bool active = tid < ny;
         const int row = min(tid, kT2Out - 1);  // idle lanes (rows >= 120) collide a copy of row 119
-        if (kConsIssue) {
-            is.set_band(y0);
-            for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k, D2Q37_PAIR_REFILL == 3);
-        }
+        const int y = y0 + tid;
+        // face segments: rows 0..5 / ly-6..ly-1 of the new state also go to the send buffers ([p][x][6])
+        double* __restrict__ sl = face && pk.send_lo && y < 2 * kHalo ? pk.send_lo + y : nullptr;
+        double* __restrict__ sh = face && pk.send_hi && y >= ly - 2 * kHalo && active ? pk.send_hi + (y - (ly - 2 * kHalo))
+                                                                                    : nullptr;
+        SlotClock clk;  // t % depth
+        clk.reset();
 #pragma unroll 1
         for (int t = 0; t < niter; ++t) {
             if (t > 0) asm volatile("bar.sync 3, 512;" ::: "memory");  // step-1 column t - 1 is in the ring
-#if D2Q37_PAIR_REFILL == 4
-            // ... so the producers have read their iteration-(t-1) stage: refill it for iteration t + 1
-            if (kConsIssue && t >= 1 && t + 1 < niter - 1) is.issue(xs - kHalo + t + 1, false);
-#endif
             double v[kNpop];
             if (t >= 7) {  // column c - cx_p, produced at t - 4 - cx_p: slot t % depth
                 for_pops([&](auto P) {
                     constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
-                    if (pop_half(p) == H) v[p] = ring[(rb + t % dp) * kT2Band + row + kHalo - cy_of(p)];
+                    if (pop_half(p) == H) v[p] = ring[(rb + clk[dp]) * kT2Band + row + kHalo - cy_of(p)];
                 });
                 consume_regs(v, [](int p) { return pop_half(p) == H; });
             }
             asm volatile("bar.arrive 2, 512;" ::: "memory");
-#if D2Q37_PAIR_REFILL == 3
-            // the producers' iteration-t stage is released once they have read it: refill it (column t + 2)
-            if (kConsIssue && t + 2 < niter - 1) is.issue(xs - kHalo + t + 2, true);
-#endif
             if (t >= 7) {
                 const bool b = pair_collide<H>(v, mp, omega, tbase, 1, t & 1, cbar);
                 if (active) {
                     bad |= b;
-                    const long long e = (long long)(xs - 7 + t) * cs + y0 + tid;
+                    const int x = xs - 7 + t;
+                    double* __restrict__ o = db + ((long long)x * cs + y);
                     for_pops([&](auto P) {
                         constexpr int p = decltype(P)::value;
-                        if (pop_half(p) == H) __stcs(db + p * plane + e, v[p]);
+                        if (pop_half(p) == H) __stcs(o + p * plane, v[p]);
                     });
+                    if (sl) {
+                        for_pops([&](auto P) {
+                            constexpr int p = decltype(P)::value;
+                            if (pop_half(p) == H) sl[((long long)p * lx + x) * (2 * kHalo)] = v[p];
+                        });
+                    }
+                    if (sh) {
+                        for_pops([&](auto P) {
+                            constexpr int p = decltype(P)::value;
+                            if (pop_half(p) == H) sh[((long long)p * lx + x) * (2 * kHalo)] = v[p];
+                        });
+                    }
                 }
             }
+            clk.tick();
+        }
+    }
+    if (was_face) {  // the schedule ended inside the face bands
+        asm volatile("bar.sync 12, 256;" ::: "memory");
+        if (threadIdx.x == 2 * kT2Band) {
+            __threadfence_system();
+            atomicAdd(pk.counter, 1u);
         }
     }
 }
 
-template <bool GHOST>
-__global__ void __launch_bounds__(kPairThreads, 1)
-    k_step2_pair(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
-                 int band0, int nbands, long long per_cta, int lock, Lockstep ls, int* __restrict__ flag) {
+// Shared-memory layout, TMEM allocation and the role split of every pair kernel; `sched` gives this
+// CTA's segments.
+template <bool GHOST, class Sched>
+__device__ __forceinline__ void pair_sweep(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
+                                           const ModelParams& mp, double omega, const Sched& sched,
+                                           const SlabPack& pk, int* __restrict__ flag) {
     extern __shared__ double ring[];
     double* const stage0 = ring + kT2NRingCols * kT2Band;  // 2 stages [37][130]
     unsigned long long* const full = reinterpret_cast<unsigned long long*>(stage0 + 2 * kNpop * kStageRows);
-    unsigned* const tslot = reinterpret_cast<unsigned*>(full + 4);  // full[2], empty[2], TMEM address
+    unsigned* const tslot = reinterpret_cast<unsigned*>(full + 2);
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tslot)),
@@ -296,8 +345,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     if (threadIdx.x == 0) {
         mbar_init(full, 1);
         mbar_init(full + 1, 1);
-        mbar_init(full + 2, 8);
-        mbar_init(full + 3, 8);
         asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -306,9 +353,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     const unsigned tbase = *tslot;
     const double* __restrict__ sb = src + g.lead + kHalo * g.cstride + kHalo;
     double* __restrict__ db = dst + g.lead + kHalo * g.cstride + kHalo;
-    const int cta = blockIdx.x;
-    const PartSched sched{lock != 0, RangeSched(band0, nbands, g.lx, cta * per_cta, (cta + 1) * per_cta),
-                          LockSched(band0, g.lx, (int)gridDim.x, cta, ls)};
     bool bad = false;
     const bool half = (warp >> 2) & 1;
     if (warp < 8) {
@@ -318,9 +362,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
             pair_producer<1, GHOST>(sb, g, mp, omega, sched, ring, stage0, full, tbase, bad);
     } else {
         if (!half)
-            pair_consumer<0>(sb, db, g, mp, omega, sched, ring, stage0, full, tbase, bad);
+            pair_consumer<0>(db, g, mp, omega, sched, ring, tbase, pk, bad);
         else
-            pair_consumer<1>(sb, db, g, mp, omega, sched, ring, stage0, full, tbase, bad);
+            pair_consumer<1>(db, g, mp, omega, sched, ring, tbase, pk, bad);
     }
     if (bad) atomicOr(flag, 1);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -330,8 +374,54 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
 }
 
+template <bool GHOST>
+__global__ void __launch_bounds__(kPairThreads, 1)
+    k_step2_pair(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
+                 int band0, int nbands, long long per_cta, int lock, Lockstep ls, int* __restrict__ flag) {
+    const int cta = blockIdx.x;
+    const PartSched sched{lock != 0, RangeSched(band0, nbands, g.lx, cta * per_cta, (cta + 1) * per_cta),
+                          LockSched(band0, g.lx, (int)gridDim.x, cta, ls)};
+    pair_sweep<GHOST>(src, dst, g, mp, omega, sched, SlabPack{nullptr, nullptr, nullptr}, flag);
+}
+
+// One overlapped FUSED2 sweep of a y-slab in the pair form.  CTAs [0, nf_lo) / [nf_lo, nf_lo + nf_hi)
+// sweep the ghost-face band(s) of the low / high face first -- packing the new edge rows into the send
+// buffers and announcing them on the sweep counter -- then the interior bands next to them; the other
+// CTAs march the remaining interior bands in lockstep.  Wall faces are swept beside this launch by the
+// general form (launch_step2_pair_slab).
+struct PairSlabPlan {
+    int nf_lo, nf_hi;
+    int lo_face0, lo_face_nb, lo_adj0, lo_adj_nb;  // bands
+    int hi_face0, hi_face_nb, hi_adj0, hi_adj_nb;
+    long long lo_face_per, lo_adj_per, hi_face_per, hi_adj_per;  // items per face CTA
+    int main_band0, main_nb;
+    Lockstep ls;  // main CTAs: grid - nf_lo - nf_hi
+};
+
+__global__ void __launch_bounds__(kPairThreads, 1)
+    k_step2_pair_slab(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp,
+                      double omega, PairSlabPlan sp, int* __restrict__ flag, unsigned* __restrict__ counter,
+                      double* __restrict__ send_lo, double* __restrict__ send_hi) {
+    const int cta = blockIdx.x, lx = g.lx;
+    if (cta < sp.nf_lo + sp.nf_hi) {
+        const bool lo = cta < sp.nf_lo;
+        const long long c = lo ? cta : cta - sp.nf_lo;
+        const FaceSched fs =
+            lo ? FaceSched{RangeSched(sp.lo_face0, sp.lo_face_nb, lx, c * sp.lo_face_per, (c + 1) * sp.lo_face_per),
+                           RangeSched(sp.lo_adj0, sp.lo_adj_nb, lx, c * sp.lo_adj_per, (c + 1) * sp.lo_adj_per), true}
+               : FaceSched{RangeSched(sp.hi_face0, sp.hi_face_nb, lx, c * sp.hi_face_per, (c + 1) * sp.hi_face_per),
+                           RangeSched(sp.hi_adj0, sp.hi_adj_nb, lx, c * sp.hi_adj_per, (c + 1) * sp.hi_adj_per), true};
+        pair_sweep<true>(src, dst, g, mp, omega, fs, SlabPack{lo ? send_lo : nullptr, lo ? nullptr : send_hi, counter},
+                         flag);
+    } else {
+        const int G = (int)gridDim.x - sp.nf_lo - sp.nf_hi;
+        const LockSched ls(sp.main_band0, lx, G, cta - sp.nf_lo - sp.nf_hi, sp.ls);
+        pair_sweep<true>(src, dst, g, mp, omega, ls, SlabPack{nullptr, nullptr, nullptr}, flag);
+    }
+}
+
 size_t pair_smem_bytes() {
-    return (size_t)kT2NRingCols * kT2Band * sizeof(double) + 2 * size_t(kStageBytes) + 32 + 16;  // + mbarriers, TMEM slot
+    return (size_t)kT2NRingCols * kT2Band * sizeof(double) + 2 * size_t(kStageBytes) + 16 + 16;  // + mbarriers, TMEM slot
 }
 
 }  // namespace
@@ -361,6 +451,87 @@ cudaError_t launch_step2_pair(const double* src, double* dst, const DevGeo& g, c
         k_step2_pair<false><<<ctas, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
                                                                         lock, ls, flag);
     return cudaGetLastError();
+}
+
+int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
+                           double omega, int* flag, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
+                           cudaEvent_t ev_join, int grid, unsigned* counter, double* send_lo, double* send_hi,
+                           cudaError_t* err) {
+    *err = cudaSuccess;
+    const int lx = g.lx;
+    int nbands, b_lo, b_hi;
+    step2_interior_bands(g, &nbands, &b_lo, &b_hi);
+    const bool ghost_lo = fc.lo == kFaceGhost, ghost_hi = fc.hi == kFaceGhost;
+    const bool wall_lo = fc.lo == kFaceWall, wall_hi = fc.hi == kFaceWall;
+    // the new edge rows must lie in the face bands: a full first band, >= 6 rows in the last one
+    if (!(ghost_lo || ghost_hi) || !(ghost_lo || wall_lo) || !(ghost_hi || wall_hi) || b_lo != 1 ||
+        b_hi - b_lo < 3 || grid < 16 || g.ly - (nbands - 1) * kT2Out < 2 * kHalo || g.ly < kT2Out)
+        return 0;
+    const double face_cost = step2_face_pct() / 100.0;  // a general-form (wall) item against a pair item
+    const long long lo_items = (long long)b_lo * lx, hi_items = (long long)(nbands - b_hi) * lx;
+    const long long in_items = (long long)(b_hi - b_lo) * lx;
+    const double per = (in_items + (wall_lo ? face_cost : 1.0) * lo_items + (wall_hi ? face_cost : 1.0) * hi_items) / grid;
+    auto wall_ctas = [&](long long items) { return std::max(1, (int)std::ceil(face_cost * items / per)); };
+    const int cw_lo = wall_lo ? wall_ctas(lo_items) : 0, cw_hi = wall_hi ? wall_ctas(hi_items) : 0;
+    const int gp = grid - cw_lo - cw_hi;  // CTAs of the pair launch
+    PairSlabPlan sp{};
+    // ghost faces: enough CTAs that a face share is at most half of a CTA's work (the exchange then hides
+    // under the other half), topped up with whole interior bands next to the face
+    auto face_ctas = [&](long long items) {
+        return std::max(1, std::min(gp / 8, (int)std::ceil(2.0 * items / per)));
+    };
+    int k_lo = 0, k_hi = 0;
+    if (ghost_lo) {
+        sp.nf_lo = face_ctas(lo_items);
+        k_lo = std::max(0, (int)std::floor(sp.nf_lo * per / lx) - b_lo);
+    }
+    if (ghost_hi) {
+        sp.nf_hi = face_ctas(hi_items);
+        k_hi = std::max(0, (int)std::floor(sp.nf_hi * per / lx) - (nbands - b_hi));
+    }
+    while (k_lo + k_hi > b_hi - b_lo - 1) (k_lo >= k_hi ? k_lo : k_hi)--;  // keep >= 1 main band
+    sp.lo_face0 = 0;
+    sp.lo_face_nb = b_lo;
+    sp.lo_adj0 = b_lo;
+    sp.lo_adj_nb = k_lo;
+    sp.hi_face0 = b_hi;
+    sp.hi_face_nb = nbands - b_hi;
+    sp.hi_adj0 = b_hi - k_hi;
+    sp.hi_adj_nb = k_hi;
+    auto share = [](long long items, int n) { return n ? (items + n - 1) / n : 0LL; };
+    sp.lo_face_per = share(lo_items, sp.nf_lo);
+    sp.lo_adj_per = share((long long)k_lo * lx, sp.nf_lo);
+    sp.hi_face_per = share(hi_items, sp.nf_hi);
+    sp.hi_adj_per = share((long long)k_hi * lx, sp.nf_hi);
+    sp.main_band0 = b_lo + k_lo;
+    sp.main_nb = b_hi - k_hi - sp.main_band0;
+    const int gmain = gp - sp.nf_lo - sp.nf_hi;
+    if (gmain < 1 || sp.main_nb < 1) return 0;
+    sp.ls = lockstep_plan(sp.main_nb, gmain, lx);
+    static bool attr = false;
+    if (!attr) {
+        *err = cudaFuncSetAttribute(k_step2_pair_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)pair_smem_bytes());
+        if (*err != cudaSuccess) return 0;
+        attr = true;
+    }
+    const bool walls = cw_lo + cw_hi > 0;
+    if (walls) {  // the wall band(s) in the general form, beside the pair launch
+        if ((*err = cudaEventRecord(ev_fork, s)) != cudaSuccess) return 0;
+        if ((*err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return 0;
+        const int band0[3] = {0, 0, b_hi}, nb[3] = {0, wall_lo ? b_lo : 0, wall_hi ? nbands - b_hi : 0};
+        const int ctas[3] = {0, cw_lo, cw_hi};
+        if ((*err = launch_step2_parts(src, dst, g, fc, mp, omega, flag, side, band0, nb, ctas)) != cudaSuccess)
+            return 0;
+    }
+    k_step2_pair_slab<<<gp, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, sp, flag, counter, send_lo,
+                                                                  send_hi);
+    if ((*err = cudaGetLastError()) != cudaSuccess) return 0;
+    if (walls) {
+        if ((*err = cudaEventRecord(ev_join, side)) != cudaSuccess) return 0;
+        if ((*err = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return 0;
+    }
+    return sp.nf_lo + sp.nf_hi;
 }
 
 }  // namespace d2q37

@@ -1208,6 +1208,28 @@ def test_fused2_nccl_self_ring_overlapped_bitwise(gpu, lbm, lx, ly):
     assert np.array_equal(s.dump(), ref.dump())
 
 
+@pytest.mark.parametrize("lx,ly", [(512, 2048), (4096, 1032), (128, 40000)])
+@pytest.mark.parametrize("faces", [("ghost", "ghost"), ("wall", "ghost"), ("ghost", "wall")])
+def test_fused2_pair_slab_sweep_equals_one_thread_form(gpu, lbm, lx, ly, faces):
+    """The overlapped y-slab sweep in the pair form (k_step2_pair_slab: ghost-face bands first on a few
+    CTAs with the new edge rows packed for the exchange, the interior in lockstep -- more bands than
+    CTAs at 128 x 40000 -- a wall face's band by the general form beside it) equals the one-thread
+    slab sweep (k_step2_slab) bit for bit, lattice and send buffers, on the face combinations of the
+    ranks of a multi-GPU run (interior ranks: ghost / ghost; the first and last: a wall)."""
+    init = lbm.make_lattice("random", lx, ly, seed=83)
+    got = []
+    for form in (4, 0):
+        s = sim_of(lbm, "soa", lx, ly, variant="fused2")
+        s.load(init)
+        s.debug_step2_slab_sweep(0.9, form, *faces)
+        got.append((s.dump(), [s.debug_read_halo6(w) if faces[w] == "ghost" else None for w in (0, 1)]))
+        s.close()
+    assert np.array_equal(got[0][0], got[1][0])
+    for w in (0, 1):
+        if faces[w] == "ghost":
+            assert np.array_equal(got[0][1][w], got[1][1][w]), w
+
+
 @pytest.mark.parametrize("layout,vl", [("aos", 1), ("caosoa", 8), ("caosoa", 32)])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 @pytest.mark.parametrize("nslabs", [2, 3])

@@ -245,13 +245,16 @@ int main(int argc, char** argv) {
                lock, mode, kOut, nst, delay, best, sites * 592 / (best * 1e6), best * 1e6 / (double)(per + 7),
                100.0 * w / (double)nsm / ((double)best * 1e-3 * 1.9e9));
     };
-    for (int delay : {0, 2000}) {
-        for (int lock : {0, 1}) {
-            run(k_mem<1, 0, 120>, 1, delay, 120, 0, lock);
-            run(k_mem<2, 0, 120>, 2, delay, 120, 0, lock);
-            run(k_mem<3, 0, 120>, 3, delay, 120, 0, lock);
-            run(k_mem<4, 0, 120>, 4, delay, 120, 0, lock);
-        }
+    // round 2: which side of the SoA stream costs -- reads (modes 0 / 2) or writes (0 / 3) -- in lockstep
+    for (int lock : {1, 0}) {
+        run(k_mem<2, 0, 120>, 2, 0, 120, 0, lock);
+        run(k_mem<2, 2, 120>, 2, 0, 120, 2, lock);
+        run(k_mem<2, 3, 120>, 2, 0, 120, 3, lock);
+        run(k_mem<2, 1, 120>, 2, 0, 120, 1, lock);
+        run(k_mem<2, 9, 120>, 2, 0, 120, 9, lock);
+        run(k_mem<2, 8, 120>, 2, 0, 120, 8, lock);
+        run(k_mem<2, 4, 120>, 2, 0, 120, 4, lock);
+        run(k_mem<2, 5, 120>, 2, 0, 120, 5, lock);
     }
     return 0;
 }
