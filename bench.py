@@ -732,8 +732,10 @@ def run_b200(args, dist: Dist):
     dom = "fused" if fused_n else "collide"
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
     form = None if STUB else lbm.set_fused2_tuning(-1, -1)[0]
-    pair = args.variant == "fused2" and args.layout == "soa" and form == 4 and transport is None
-    if pair:  # two launches per sweep: k_step2_pair (interior) beside k_step2_split (the two wall bands)
+    pair = args.variant == "fused2" and args.layout == "soa" and form == 4
+    if pair and transport is None:  # two launches per sweep: k_step2_pair beside k_step2_split (wall bands)
+        launches += fused_n
+    elif pair and dist.rank in (0, n - 1) and n > 1:  # a global wall: its band's general launch beside
         launches += fused_n
     # FUSED2: one sweep per timed "fused" interval (k_step2_pair + the face bands' k_step2_split beside it)
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
@@ -742,7 +744,10 @@ def run_b200(args, dist: Dist):
     step_ms = ms_max / args.steps
     two = upd == 2
     roofline = {"bound": "hbm",
-                "kernel": (("k_step2_pair (two fused pull+collide steps per HBM sweep, temporal blocking; two "
+                "kernel": (("k_step2_pair_slab (y-slab sweep in the pair form: ghost-face bands first with the "
+                            "6-row halo pack, interior in lockstep beside the NCCL exchange; two fused steps per "
+                            "HBM sweep, two threads per site)" if pair and transport else
+                            "k_step2_pair (two fused pull+collide steps per HBM sweep, temporal blocking; two "
                             "threads per site, 512-thread CTAs, lockstep band schedule) beside k_step2_split on "
                             "the two wall bands; the sweep interval covers both" if pair else
                             "k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "

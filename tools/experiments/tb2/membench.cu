@@ -34,6 +34,7 @@ __constant__ signed char c_cy[kNpop] = {0, 0, -1, 1, 0, -1, 1, -1, 1, 0, -2, 2, 
 
 __device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __constant__ int c_gs[8] = {0, 3, 8, 15, 22, 29, 34, 37};
+__constant__ int c_slot[kNpop];  // cx-sorted position of population p (MODE 11)
 
 // MODE 0: SoA planes (the library's FUSED2 store): element (p, x, y) at p*plane + x*cs + y.
 // MODE 2: SoA reads, band-blocked writes.  MODE 3: band-blocked reads, SoA writes.
@@ -130,7 +131,9 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
             } else if (issuer) {
                 const int col = wr(wr(xs - 3 + t) - icx);
                 const double* s = (MODE == 0 || MODE == 2) ? src + ip * plane + col * cs + ((y0 + 3 - icy) & ~1)
-                                            : src + (((long long)col * nbands + band) * kNpop + ip) * kOut;
+                                  : (MODE >= 10) ? src + ((long long)col * kNpop + (MODE == 11 ? c_slot[ip] : ip)) * cs +
+                                                       ((y0 + 3 - icy) & ~1)
+                                                 : src + (((long long)col * nbands + band) * kNpop + ip) * kOut;
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         sa(sm + (st * kNpop + ip) * kRows)),
@@ -169,6 +172,10 @@ __global__ void __launch_bounds__(256, 1) k_mem(const double* __restrict__ src, 
                     double* o = dst + (long long)(xs - 7 + t) * cs + y0 + (kOut == 120 ? 4 : 6) + tid;
 #pragma unroll
                     for (int p = 0; p < kNpop; ++p) __stcs(o + p * plane, acc + p);
+                } else if (MODE >= 10) {  // column-major [x][p][y] (11: populations sorted by cx)
+                    double* o = dst + (long long)(xs - 7 + t) * kNpop * cs + y0 + 4 + tid;
+#pragma unroll
+                    for (int p = 0; p < kNpop; ++p) __stcs(o + (long long)(MODE == 11 ? c_slot[p] : p) * cs, acc + p);
                 } else if (MODE == 8) {
                     const long long blk = (long long)(xs - 7 + t) * nbands + band;
                     double* o = dst + blk * kNpop * 120 + tid;
@@ -246,15 +253,23 @@ int main(int argc, char** argv) {
                100.0 * w / (double)nsm / ((double)best * 1e-3 * 1.9e9));
     };
     // round 2: which side of the SoA stream costs -- reads (modes 0 / 2) or writes (0 / 3) -- in lockstep
+    {
+        int slot[kNpop];
+        signed char cx[kNpop];
+        CK(cudaMemcpyFromSymbol(cx, c_cx, sizeof cx));
+        for (int p = 0; p < kNpop; ++p) {
+            int n = 0;
+            for (int q = 0; q < kNpop; ++q) n += (cx[q] < cx[p]) || (cx[q] == cx[p] && q < p);
+            slot[p] = n;
+        }
+        CK(cudaMemcpyToSymbol(c_slot, slot, sizeof slot));
+    }
     for (int lock : {1, 0}) {
+        run(k_mem<2, 10, 120>, 2, 0, 120, 10, lock);
+        run(k_mem<2, 11, 120>, 2, 0, 120, 11, lock);
         run(k_mem<2, 0, 120>, 2, 0, 120, 0, lock);
         run(k_mem<2, 2, 120>, 2, 0, 120, 2, lock);
-        run(k_mem<2, 3, 120>, 2, 0, 120, 3, lock);
         run(k_mem<2, 1, 120>, 2, 0, 120, 1, lock);
-        run(k_mem<2, 9, 120>, 2, 0, 120, 9, lock);
-        run(k_mem<2, 8, 120>, 2, 0, 120, 8, lock);
-        run(k_mem<2, 4, 120>, 2, 0, 120, 4, lock);
-        run(k_mem<2, 5, 120>, 2, 0, 120, 5, lock);
     }
     return 0;
 }
