@@ -792,9 +792,7 @@ int step2_sweep_overlapped(d2q37_lattice* h, double omega, int bc, const Faces& 
         ProfScope ps(h, kProfFused);
         cudaError_t err = cudaSuccess;
         if (step2_form() == kStep2Pair) {  // the two-threads-per-site form (wall faces beside it)
-            RET(ensure_side_stream(h));
-            nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
-                                          h->ev_fork, h->ev_join, h->nsm - std::min(step2_halo_sms(), h->nsm / 4),
+            nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid,
                                           h->d_sweep_counter, h->h6[0], h->h6[1], &err);
             CK(err);
         }
@@ -2263,7 +2261,6 @@ int d2q37_debug_step2_slab_sweep(d2q37_lattice* h, double omega, int form, int f
     DeviceGuard dg(h->device);
     if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
     RET(ensure_halo6(h));
-    RET(ensure_side_stream(h));
     if (!h->d_sweep_counter) {
         CK(cudaMalloc(&h->d_sweep_counter, sizeof(unsigned)));
         CK(cudaMemset(h->d_sweep_counter, 0, sizeof(unsigned)));
@@ -2277,8 +2274,8 @@ int d2q37_debug_step2_slab_sweep(d2q37_lattice* h, double omega, int form, int f
     cudaError_t err = cudaSuccess;
     int nsig = 0;
     if (form == kStep2Pair)
-        nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, h->side_stream,
-                                      h->ev_fork, h->ev_join, grid, h->d_sweep_counter, h->h6[0], h->h6[1], &err);
+        nsig = launch_step2_pair_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid,
+                                      h->d_sweep_counter, h->h6[0], h->h6[1], &err);
     else
         nsig = launch_step2_slab(src, dst, h->g, fc, h->mp, omega, h->d_flag, h->stream, grid, h->d_sweep_counter,
                                  h->h6[0], h->h6[1], &err);

@@ -167,13 +167,12 @@ int launch_step2_slab(const double* src, double* dst, const DevGeo& g, const Fac
                       double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
                       double* send_hi, cudaError_t* err);
 // The overlapped slab sweep in the pair form (k_step2_pair_slab): ghost-face bands first on a few CTAs
-// (new edge rows into send_lo / send_hi, one counter increment per CTA once stored), the interior bands
-// in lockstep on the rest; a wall face's band by the general form on `side` (ev_fork / ev_join).  Returns
-// the number of CTAs that signal (0: not launched -- no ghost face, too few bands, or an error in *err).
+// (new edge rows into send_lo / send_hi, one counter increment per CTA once stored), the other bands --
+// a global wall's among them -- in lockstep on the rest.  Returns the number of CTAs that signal (0: not
+// launched -- no ghost face, too few bands, or an error in *err).
 int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                           double omega, int* flag, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
-                           cudaEvent_t ev_join, int grid, unsigned* counter, double* send_lo, double* send_hi,
-                           cudaError_t* err);
+                           double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
+                           double* send_hi, cudaError_t* err);
 // Explicit band ranges per part: part 0 in the per-thread plain form (rows read
 // unwrapped: not for y-periodic faces), parts 1 and 2 in the general form.
 cudaError_t launch_step2_parts(const double* src, double* dst, const DevGeo& g, const Faces& fc,

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "d2q37_device.cuh"
@@ -195,9 +196,19 @@ template <class Sched>
 __device__ __forceinline__ bool sched_in_face(const Sched&) { return false; }
 __device__ __forceinline__ bool sched_in_face(const FaceSched& s) { return s.in_face; }
 
+// Wall bands (specular reflection): a pull of row y - cy beyond a wall reads population
+// ybar(p) = (cx, -cy) at the mirror row -1 - (y - cy) / 2 ly - 1 - (y - cy).  walls: bit 0 the low face
+// is a wall, bit 1 the high one; a band needs the mirror tables when its producer rows reach row 0 /
+// row ly - 1 within the pull distance.
+__device__ __forceinline__ bool wall_lo_band(int walls, int band) { return (walls & 1) && band == 0; }
+__device__ __forceinline__ bool wall_hi_band(int walls, int y0, int ly) { return (walls & 2) && y0 + kT2Band - 1 >= ly; }
+__device__ __forceinline__ int mirror_row(int ys, int ly, bool wlo, bool whi) {
+    return (wlo && ys < 0) ? -1 - ys : (whi && ys >= ly) ? 2 * ly - 1 - ys : INT_MIN;
+}
+
 template <int H, bool GHOST, class Sched>
 __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, const DevGeo& g, const ModelParams& mp,
-                                              double omega, Sched sched, double* ring, double* stage0,
+                                              double omega, Sched sched, int walls, double* ring, double* stage0,
                                               unsigned long long* full, unsigned tbase, bool& bad) {
     const int tid = threadIdx.x & (kT2Band - 1);
     const int warp = threadIdx.x >> 5;
@@ -211,8 +222,25 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
         const int niter = xe - xs + 7;
         is.set_band(y0);
         for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k);
-        const int yo = GHOST ? min(tid, ly + kHalo - 1 - (y0 - kHalo)) : tid;
+        // step-1 row of this thread, clamped: rows beyond a wall are never read (step 2 mirrors into the
+        // lattice), rows past ly + 2 never (their pulls would leave a slab's deep ghost rows)
+        const bool wlo = wall_lo_band(walls, band), whi = wall_hi_band(walls, y0, ly);
+        int y1 = y0 - kHalo + tid;
+        if (wlo) y1 = max(y1, 0);
+        if (whi) y1 = min(y1, ly - 1);
+        if (GHOST) y1 = min(y1, ly + kHalo - 1);
+        const int yo = y1 - (y0 - kHalo);
         const int par = (y0 - kHalo) & 1;
+        // wall bands: per k = cy + 3, the stage offset of the mirrored pull (population ybar, whose stage
+        // starts at row (y0 - 3 + cy) & ~1) or none
+        unsigned mirm = 0;
+        int moff[2 * kHalo + 1];
+#pragma unroll
+        for (int k = 0; k < 2 * kHalo + 1; ++k) {
+            const int cy = k - kHalo, m = mirror_row(y1 - cy, ly, wlo, whi);
+            mirm |= unsigned(m != INT_MIN) << k;
+            moff[k] = m - ((y0 - kHalo + cy) & ~1);
+        }
         SlotClock clk;
         clk.reset();
 #pragma unroll 1
@@ -222,10 +250,19 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
             ++used;
             const double* const sg = stage0 + st * kNpop * kStageRows;
             double f[kNpop];
-            for_pops([&](auto P) {
-                constexpr int p = decltype(P)::value;
-                if (pop_half(p) == H) f[p] = sg[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
-            });
+            if (!mirm) {
+                for_pops([&](auto P) {
+                    constexpr int p = decltype(P)::value;
+                    if (pop_half(p) == H) f[p] = sg[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
+                });
+            } else {
+                for_pops([&](auto P) {
+                    constexpr int p = decltype(P)::value, k = cy_of(p) + kHalo, q = ybar_of(p);
+                    if (pop_half(p) == H)
+                        f[p] = (mirm >> k) & 1u ? sg[q * kStageRows + moff[k]]
+                                                : sg[p * kStageRows + yo + (par ^ (cy_of(p) & 1))];
+                });
+            }
             consume_regs(f, [](int p) { return pop_half(p) == H; });
             bad |= pair_collide<H>(f, mp, omega, tbase, 0, t & 1, pbar);
             // the consumers have read this iteration's slots -- and every producer has read the stage
@@ -245,8 +282,8 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
 
 template <int H, class Sched>
 __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const DevGeo& g, const ModelParams& mp,
-                                              double omega, Sched sched, const double* ring, unsigned tbase,
-                                              const SlabPack& pk, bool& bad) {
+                                              double omega, Sched sched, int walls, const double* ring,
+                                              unsigned tbase, const SlabPack& pk, bool& bad) {
     const int tid = threadIdx.x & (kT2Band - 1);
     const int warp = threadIdx.x >> 5;
     const int lx = g.lx, ly = g.ly;
@@ -269,8 +306,19 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
         const int ny = min(kT2Out, ly - y0);
         const int niter = xe - xs + 7;
         const bool active = tid < ny;
-        const int row = min(tid, kT2Out - 1);  // idle lanes (rows >= 120) collide a copy of row 119
+        const bool wlo = wall_lo_band(walls, band), whi = wall_hi_band(walls, y0, ly);
+        // idle lanes (rows >= ny) collide a copy of the band's last row
+        const int row = min(tid, (wlo || whi ? ny : kT2Out) - 1);
         const int y = y0 + tid;
+        // wall bands: per k = cy + 3, the ring row of the mirrored pull (population ybar) or none
+        unsigned mirm = 0;
+        int mpos[2 * kHalo + 1];
+#pragma unroll
+        for (int k = 0; k < 2 * kHalo + 1; ++k) {
+            const int m = mirror_row(y0 + row - (k - kHalo), ly, wlo, whi);
+            mirm |= unsigned(m != INT_MIN) << k;
+            mpos[k] = m - (y0 - kHalo);
+        }
         // face segments: rows 0..5 / ly-6..ly-1 of the new state also go to the send buffers ([p][x][6])
         double* __restrict__ sl = face && pk.send_lo && y < 2 * kHalo ? pk.send_lo + y : nullptr;
         double* __restrict__ sh = face && pk.send_hi && y >= ly - 2 * kHalo && active ? pk.send_hi + (y - (ly - 2 * kHalo))
@@ -282,10 +330,20 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
             if (t > 0) asm volatile("bar.sync 3, 512;" ::: "memory");  // step-1 column t - 1 is in the ring
             double v[kNpop];
             if (t >= 7) {  // column c - cx_p, produced at t - 4 - cx_p: slot t % depth
-                for_pops([&](auto P) {
-                    constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
-                    if (pop_half(p) == H) v[p] = ring[(rb + clk[dp]) * kT2Band + row + kHalo - cy_of(p)];
-                });
+                if (!mirm) {
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
+                        if (pop_half(p) == H) v[p] = ring[(rb + clk[dp]) * kT2Band + row + kHalo - cy_of(p)];
+                    });
+                } else {  // ybar(p) has p's cx, hence p's ring depth
+                    for_pops([&](auto P) {
+                        constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
+                        constexpr int k = cy_of(p) + kHalo, rbb = t2n_base(ybar_of(p));
+                        if (pop_half(p) == H)
+                            v[p] = (mirm >> k) & 1u ? ring[(rbb + clk[dp]) * kT2Band + mpos[k]]
+                                                    : ring[(rb + clk[dp]) * kT2Band + row + kHalo - cy_of(p)];
+                    });
+                }
                 consume_regs(v, [](int p) { return pop_half(p) == H; });
             }
             asm volatile("bar.arrive 2, 512;" ::: "memory");
@@ -329,7 +387,7 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
 // CTA's segments.
 template <bool GHOST, class Sched>
 __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, double* __restrict__ dst, const DevGeo& g,
-                                           const ModelParams& mp, double omega, const Sched& sched,
+                                           const ModelParams& mp, double omega, const Sched& sched, int walls,
                                            const SlabPack& pk, int* __restrict__ flag) {
     extern __shared__ double ring[];
     double* const stage0 = ring + kT2NRingCols * kT2Band;  // 2 stages [37][130]
@@ -357,14 +415,14 @@ __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, doubl
     const bool half = (warp >> 2) & 1;
     if (warp < 8) {
         if (!half)
-            pair_producer<0, GHOST>(sb, g, mp, omega, sched, ring, stage0, full, tbase, bad);
+            pair_producer<0, GHOST>(sb, g, mp, omega, sched, walls, ring, stage0, full, tbase, bad);
         else
-            pair_producer<1, GHOST>(sb, g, mp, omega, sched, ring, stage0, full, tbase, bad);
+            pair_producer<1, GHOST>(sb, g, mp, omega, sched, walls, ring, stage0, full, tbase, bad);
     } else {
         if (!half)
-            pair_consumer<0>(db, g, mp, omega, sched, ring, tbase, pk, bad);
+            pair_consumer<0>(db, g, mp, omega, sched, walls, ring, tbase, pk, bad);
         else
-            pair_consumer<1>(db, g, mp, omega, sched, ring, tbase, pk, bad);
+            pair_consumer<1>(db, g, mp, omega, sched, walls, ring, tbase, pk, bad);
     }
     if (bad) atomicOr(flag, 1);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -377,18 +435,17 @@ __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, doubl
 template <bool GHOST>
 __global__ void __launch_bounds__(kPairThreads, 1)
     k_step2_pair(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp, double omega,
-                 int band0, int nbands, long long per_cta, int lock, Lockstep ls, int* __restrict__ flag) {
+                 int band0, int nbands, long long per_cta, int lock, Lockstep ls, int walls, int* __restrict__ flag) {
     const int cta = blockIdx.x;
     const PartSched sched{lock != 0, RangeSched(band0, nbands, g.lx, cta * per_cta, (cta + 1) * per_cta),
                           LockSched(band0, g.lx, (int)gridDim.x, cta, ls)};
-    pair_sweep<GHOST>(src, dst, g, mp, omega, sched, SlabPack{nullptr, nullptr, nullptr}, flag);
+    pair_sweep<GHOST>(src, dst, g, mp, omega, sched, walls, SlabPack{nullptr, nullptr, nullptr}, flag);
 }
 
 // One overlapped FUSED2 sweep of a y-slab in the pair form.  CTAs [0, nf_lo) / [nf_lo, nf_lo + nf_hi)
 // sweep the ghost-face band(s) of the low / high face first -- packing the new edge rows into the send
 // buffers and announcing them on the sweep counter -- then the interior bands next to them; the other
-// CTAs march the remaining interior bands in lockstep.  Wall faces are swept beside this launch by the
-// general form (launch_step2_pair_slab).
+// CTAs march the remaining bands in lockstep, a global wall's band among them (mirror tables).
 struct PairSlabPlan {
     int nf_lo, nf_hi;
     int lo_face0, lo_face_nb, lo_adj0, lo_adj_nb;  // bands
@@ -396,6 +453,7 @@ struct PairSlabPlan {
     long long lo_face_per, lo_adj_per, hi_face_per, hi_adj_per;  // items per face CTA
     int main_band0, main_nb;
     Lockstep ls;  // main CTAs: grid - nf_lo - nf_hi
+    int walls;    // bit 0 / 1: the low / high face is a global wall (its band is a main band)
 };
 
 __global__ void __launch_bounds__(kPairThreads, 1)
@@ -411,12 +469,12 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                            RangeSched(sp.lo_adj0, sp.lo_adj_nb, lx, c * sp.lo_adj_per, (c + 1) * sp.lo_adj_per), true}
                : FaceSched{RangeSched(sp.hi_face0, sp.hi_face_nb, lx, c * sp.hi_face_per, (c + 1) * sp.hi_face_per),
                            RangeSched(sp.hi_adj0, sp.hi_adj_nb, lx, c * sp.hi_adj_per, (c + 1) * sp.hi_adj_per), true};
-        pair_sweep<true>(src, dst, g, mp, omega, fs, SlabPack{lo ? send_lo : nullptr, lo ? nullptr : send_hi, counter},
-                         flag);
+        pair_sweep<true>(src, dst, g, mp, omega, fs, sp.walls,
+                         SlabPack{lo ? send_lo : nullptr, lo ? nullptr : send_hi, counter}, flag);
     } else {
         const int G = (int)gridDim.x - sp.nf_lo - sp.nf_hi;
         const LockSched ls(sp.main_band0, lx, G, cta - sp.nf_lo - sp.nf_hi, sp.ls);
-        pair_sweep<true>(src, dst, g, mp, omega, ls, SlabPack{nullptr, nullptr, nullptr}, flag);
+        pair_sweep<true>(src, dst, g, mp, omega, ls, sp.walls, SlabPack{nullptr, nullptr, nullptr}, flag);
     }
 }
 
@@ -444,19 +502,19 @@ cudaError_t launch_step2_pair(const double* src, double* dst, const DevGeo& g, c
     if (ctas < 1) return cudaErrorInvalidValue;
     const long long per_cta = (total + ctas - 1) / ctas;
     const Lockstep ls = lockstep_plan(nb, ctas, g.lx);
+    const int walls = (fc.lo == kFaceWall ? 1 : 0) | (fc.hi == kFaceWall ? 2 : 0);
     if (fc.hi == kFaceGhost)
         k_step2_pair<true><<<ctas, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
-                                                                       lock, ls, flag);
+                                                                       lock, ls, walls, flag);
     else
         k_step2_pair<false><<<ctas, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, band0, nb, per_cta,
-                                                                        lock, ls, flag);
+                                                                        lock, ls, walls, flag);
     return cudaGetLastError();
 }
 
 int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
-                           double omega, int* flag, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_fork,
-                           cudaEvent_t ev_join, int grid, unsigned* counter, double* send_lo, double* send_hi,
-                           cudaError_t* err) {
+                           double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
+                           double* send_hi, cudaError_t* err) {
     *err = cudaSuccess;
     const int lx = g.lx;
     int nbands, b_lo, b_hi;
@@ -467,18 +525,15 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
     if (!(ghost_lo || ghost_hi) || !(ghost_lo || wall_lo) || !(ghost_hi || wall_hi) || b_lo != 1 ||
         b_hi - b_lo < 3 || grid < 16 || g.ly - (nbands - 1) * kT2Out < 2 * kHalo || g.ly < kT2Out)
         return 0;
-    const double face_cost = step2_face_pct() / 100.0;  // a general-form (wall) item against a pair item
     const long long lo_items = (long long)b_lo * lx, hi_items = (long long)(nbands - b_hi) * lx;
-    const long long in_items = (long long)(b_hi - b_lo) * lx;
-    const double per = (in_items + (wall_lo ? face_cost : 1.0) * lo_items + (wall_hi ? face_cost : 1.0) * hi_items) / grid;
-    auto wall_ctas = [&](long long items) { return std::max(1, (int)std::ceil(face_cost * items / per)); };
-    const int cw_lo = wall_lo ? wall_ctas(lo_items) : 0, cw_hi = wall_hi ? wall_ctas(hi_items) : 0;
-    const int gp = grid - cw_lo - cw_hi;  // CTAs of the pair launch
+    const double per = double(nbands) * lx / grid;  // items per CTA
     PairSlabPlan sp{};
+    sp.walls = (wall_lo ? 1 : 0) | (wall_hi ? 2 : 0);
     // ghost faces: enough CTAs that a face share is at most half of a CTA's work (the exchange then hides
-    // under the other half), topped up with whole interior bands next to the face
+    // under the other half), topped up with whole interior bands next to the face; a wall face's band is
+    // an ordinary main band
     auto face_ctas = [&](long long items) {
-        return std::max(1, std::min(gp / 8, (int)std::ceil(2.0 * items / per)));
+        return std::max(1, std::min(grid / 8, (int)std::ceil(2.0 * items / per)));
     };
     int k_lo = 0, k_hi = 0;
     if (ghost_lo) {
@@ -491,11 +546,11 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
     }
     while (k_lo + k_hi > b_hi - b_lo - 1) (k_lo >= k_hi ? k_lo : k_hi)--;  // keep >= 1 main band
     sp.lo_face0 = 0;
-    sp.lo_face_nb = b_lo;
+    sp.lo_face_nb = ghost_lo ? b_lo : 0;
     sp.lo_adj0 = b_lo;
     sp.lo_adj_nb = k_lo;
     sp.hi_face0 = b_hi;
-    sp.hi_face_nb = nbands - b_hi;
+    sp.hi_face_nb = ghost_hi ? nbands - b_hi : 0;
     sp.hi_adj0 = b_hi - k_hi;
     sp.hi_adj_nb = k_hi;
     auto share = [](long long items, int n) { return n ? (items + n - 1) / n : 0LL; };
@@ -503,9 +558,9 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
     sp.lo_adj_per = share((long long)k_lo * lx, sp.nf_lo);
     sp.hi_face_per = share(hi_items, sp.nf_hi);
     sp.hi_adj_per = share((long long)k_hi * lx, sp.nf_hi);
-    sp.main_band0 = b_lo + k_lo;
-    sp.main_nb = b_hi - k_hi - sp.main_band0;
-    const int gmain = gp - sp.nf_lo - sp.nf_hi;
+    sp.main_band0 = ghost_lo ? b_lo + k_lo : 0;
+    sp.main_nb = (ghost_hi ? b_hi - k_hi : nbands) - sp.main_band0;
+    const int gmain = grid - sp.nf_lo - sp.nf_hi;
     if (gmain < 1 || sp.main_nb < 1) return 0;
     sp.ls = lockstep_plan(sp.main_nb, gmain, lx);
     static bool attr = false;
@@ -515,22 +570,9 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
         if (*err != cudaSuccess) return 0;
         attr = true;
     }
-    const bool walls = cw_lo + cw_hi > 0;
-    if (walls) {  // the wall band(s) in the general form, beside the pair launch
-        if ((*err = cudaEventRecord(ev_fork, s)) != cudaSuccess) return 0;
-        if ((*err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return 0;
-        const int band0[3] = {0, 0, b_hi}, nb[3] = {0, wall_lo ? b_lo : 0, wall_hi ? nbands - b_hi : 0};
-        const int ctas[3] = {0, cw_lo, cw_hi};
-        if ((*err = launch_step2_parts(src, dst, g, fc, mp, omega, flag, side, band0, nb, ctas)) != cudaSuccess)
-            return 0;
-    }
-    k_step2_pair_slab<<<gp, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, sp, flag, counter, send_lo,
-                                                                  send_hi);
+    k_step2_pair_slab<<<grid, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, sp, flag, counter, send_lo,
+                                                                    send_hi);
     if ((*err = cudaGetLastError()) != cudaSuccess) return 0;
-    if (walls) {
-        if ((*err = cudaEventRecord(ev_join, side)) != cudaSuccess) return 0;
-        if ((*err = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return 0;
-    }
     return sp.nf_lo + sp.nf_hi;
 }
 

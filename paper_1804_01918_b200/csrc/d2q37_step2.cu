@@ -757,6 +757,9 @@ void step2_bands(const DevGeo& g, const Faces& fc, int form, int* nbands, int* b
     const int inside_hi = g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0;  // bands with rows < ly
     if (per_lo && per_hi) {
         if (form != kStep2Plain) lo = 1, hi = inside_hi;  // the bulk-copy forms read rows unwrapped
+    } else if (form == kStep2Pair && !per_lo && !per_hi && g.ly >= kT2Band && fc.lo != kFaceWall && fc.hi != kFaceWall) {
+        // ghost faces: the pair form reads the deep ghost rows unwrapped, every band is interior (a wall
+        // band costs more in the pair form than in a general-form launch beside it, measured -2 %)
     } else {
         // ghost faces read the deep ghost rows unwrapped; wall bands need the general form
         lo = fc.lo == kFaceWall ? 1 : 0;
