@@ -285,6 +285,13 @@ int d2q37_kernel_times(d2q37_lattice* h, double ms[6], long counts[6]);
  * restarts the averaging window. */
 double d2q37_exposed_halo_ms(const d2q37_lattice* h);
 
+/* Timeline of the last overlapped FUSED2 slab sweep run with profiling on
+ * (no reference counterpart): milliseconds after the sweep's launch point on
+ * the lattice stream at which the halo exchange started (the sweep counter
+ * released the comm stream), NCCL finished, the unpack finished, and the sweep
+ * itself finished.  CUDA events on both streams; measurement only. */
+int d2q37_slab_timeline(d2q37_lattice* h, double ms[4]);
+
 /* FUSED2 tuning (no reference counterpart; process-wide).  form: how the
  * interior bands of a two-step sweep on the SoA store are swept -- 0
  * per-thread loads (one thread per site, 185-column ring), 1 one bulk-copy

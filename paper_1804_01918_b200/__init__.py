@@ -146,6 +146,7 @@ def _load():
         "d2q37_set_fused2_tuning": (i, [i, i, P(C.c_int), P(C.c_int)]),
         "d2q37_set_fused2_schedule": (i, [i, P(C.c_int)]),
         "d2q37_debug_step2_slab_sweep": (i, [vp, d, i, i, i]),
+        "d2q37_slab_timeline": (i, [vp, P(d)]),
         "d2q37_debug_read_halo6": (i, [vp, i, P(d), sz]),
     }
     for name, (res, args) in sig.items():
@@ -643,6 +644,13 @@ class Simulation:
         cnt = (C.c_long * 6)()
         _check(_load().d2q37_kernel_times(self._h, ms, cnt))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def slab_timeline(self) -> dict:
+        """Last overlapped FUSED2 slab sweep with profiling on (d2q37_slab_timeline): ms after the sweep
+        launch at which the exchange started / NCCL finished / the unpack finished / the sweep finished."""
+        out = np.zeros(4)
+        _check(_load().d2q37_slab_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return dict(zip(("exchange_start", "nccl_done", "unpack_done", "sweep_done"), out.tolist()))
 
     def exposed_halo_ms(self) -> float:
         return float(_load().d2q37_exposed_halo_ms(self._h))

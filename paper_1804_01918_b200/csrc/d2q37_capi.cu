@@ -83,6 +83,10 @@ struct d2q37_lattice {
     // FUSED2 pair form: the face bands' general-form launch runs beside the interior one
     cudaStream_t side_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // overlapped FUSED2 slab sweep timeline (profiling on): sweep launch, exchange start (the counter
+    // wait released), NCCL done, unpack done, sweep done
+    cudaEvent_t tl[5] = {};
+    bool tl_valid = false;
     cudaEvent_t ev_start = nullptr, ev_bnd = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_recv = nullptr;
     cudaEvent_t ev_int[kEventRing] = {}, ev_wait[kEventRing] = {};
@@ -373,6 +377,8 @@ void free_lattice(d2q37_lattice* h) {
     if (h->halo_stream) cudaStreamDestroy(h->halo_stream);
     if (h->side_stream) cudaStreamDestroy(h->side_stream);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    for (cudaEvent_t e : h->tl)
+        if (e) cudaEventDestroy(e);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ev_start) cudaEventDestroy(h->ev_start);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
@@ -788,6 +794,12 @@ int step2_sweep_overlapped(d2q37_lattice* h, double omega, int bc, const Faces& 
     double* dst = h->buf[1 - h->cur];
     const int grid = h->nsm - std::min(step2_halo_sms(), h->nsm / 4);
     int nsig = 0;
+    const bool tl = h->prof_on;
+    if (tl) {
+        for (cudaEvent_t& e : h->tl)
+            if (!e) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(h->tl[0], h->stream));
+    }
     if (wait) {
         ProfScope ps(h, kProfFused);
         cudaError_t err = cudaSuccess;
@@ -813,16 +825,23 @@ int step2_sweep_overlapped(d2q37_lattice* h, double omega, int bc, const Faces& 
         if (wait(reinterpret_cast<CUstream>(h->comm_stream), reinterpret_cast<CUdeviceptr>(h->d_sweep_counter),
                  h->sweep_target, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
             return fail(D2Q37_ERR_CUDA, "cuStreamWaitValue32 failed");
+        if (tl) CK(cudaEventRecord(h->tl[1], h->comm_stream));
         std::string why;
         const int rc = nccl_exchange(h->comm, h->comm_stream, h->h6[0], h->h6[2], lo, h->h6[1], h->h6[3], hi,
                                      halo6_count(h->g), &why);
         if (rc != D2Q37_OK) return fail(rc, "%s", why.c_str());
+        if (tl) CK(cudaEventRecord(h->tl[2], h->comm_stream));
         {
             ProfScope ps(h, kProfEdge, h->comm_stream);
             CK(launch_unpack6(dst, h->g, lo >= 0 ? h->h6[2] : nullptr, hi >= 0 ? h->h6[3] : nullptr,
                               h->comm_stream));
         }
+        if (tl) CK(cudaEventRecord(h->tl[3], h->comm_stream));
         CK(cudaEventRecord(h->ev_recv, h->comm_stream));
+    }
+    if (tl) {
+        CK(cudaEventRecord(h->tl[4], h->stream));
+        h->tl_valid = true;
     }
     // exposed halo: from the end of the sweep to the end of the exchange
     CK(cudaEventRecord(h->ev_int[h->ev_count % kEventRing], h->stream));
@@ -2368,6 +2387,19 @@ int d2q37_slab_info(const d2q37_lattice* h, int out[4]) {
     out[1] = h->nranks;
     out[2] = h->y0;
     out[3] = h->g.tr ? h->g.lx : h->g.ly;  // y-major: lattice y runs along the storage columns
+    return D2Q37_OK;
+}
+
+int d2q37_slab_timeline(d2q37_lattice* h, double ms[4]) {
+    RET(check_handle(h));
+    if (!h->tl_valid) return fail(D2Q37_ERR_INVALID_ARGUMENT, "slab timeline: no overlapped sweep with profiling on");
+    DeviceGuard dg(h->device);
+    CK(cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < 4; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, h->tl[0], h->tl[i + 1]));
+        ms[i] = t;
+    }
     return D2Q37_OK;
 }
 

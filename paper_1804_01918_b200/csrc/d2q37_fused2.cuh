@@ -134,6 +134,19 @@ struct PartSched {
     }
 };
 
+// Kernel attributes (the dynamic shared-memory opt-in) are per device: set them once per device.
+// Returns cudaSuccess once `set` has succeeded on the current device.
+template <typename F>
+inline cudaError_t once_per_device(bool (&done)[64], F&& set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+    return e;
+}
+
 // Compile-time loop over the populations (keeps ring offsets constants).
 template <typename F, int... Ps>
 __device__ __forceinline__ void for_pops_(F&& f, std::integer_sequence<int, Ps...>) {

@@ -486,16 +486,16 @@ size_t pair_smem_bytes() {
 
 cudaError_t launch_step2_pair(const double* src, double* dst, const DevGeo& g, const Faces& fc, const ModelParams& mp,
                               double omega, int* flag, cudaStream_t s, int band0, int nb, int ctas, bool lock) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_step2_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool attr[64] = {};
+    cudaError_t e = once_per_device(attr, [] {
+        cudaError_t r = cudaFuncSetAttribute(k_step2_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)pair_smem_bytes());
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_step2_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k_step2_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pair_smem_bytes());
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+        return r;
+    });
+    if (e != cudaSuccess) return e;
     const long long total = (long long)std::max(0, nb) * g.lx;
     if (total == 0) return cudaSuccess;
     ctas = (int)std::min<long long>(ctas, total);
@@ -529,11 +529,11 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
     const double per = double(nbands) * lx / grid;  // items per CTA
     PairSlabPlan sp{};
     sp.walls = (wall_lo ? 1 : 0) | (wall_hi ? 2 : 0);
-    // ghost faces: enough CTAs that a face share is at most half of a CTA's work (the exchange then hides
-    // under the other half), topped up with whole interior bands next to the face; a wall face's band is
-    // an ordinary main band
+    // ghost faces: enough CTAs that a face share is at most a third of a CTA's work (the exchange then
+    // starts a third into the sweep and hides under the rest: tools/slab_timeline.py), topped up with whole
+    // interior bands next to the face; a wall face's band is an ordinary main band
     auto face_ctas = [&](long long items) {
-        return std::max(1, std::min(grid / 8, (int)std::ceil(2.0 * items / per)));
+        return std::max(1, std::min(grid / 8, (int)std::ceil(3.0 * items / per)));
     };
     int k_lo = 0, k_hi = 0;
     if (ghost_lo) {
@@ -563,13 +563,12 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
     const int gmain = grid - sp.nf_lo - sp.nf_hi;
     if (gmain < 1 || sp.main_nb < 1) return 0;
     sp.ls = lockstep_plan(sp.main_nb, gmain, lx);
-    static bool attr = false;
-    if (!attr) {
-        *err = cudaFuncSetAttribute(k_step2_pair_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool attr[64] = {};
+    *err = once_per_device(attr, [] {
+        return cudaFuncSetAttribute(k_step2_pair_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)pair_smem_bytes());
-        if (*err != cudaSuccess) return 0;
-        attr = true;
-    }
+    });
+    if (*err != cudaSuccess) return 0;
     k_step2_pair_slab<<<grid, kPairThreads, pair_smem_bytes(), s>>>(src, dst, g, mp, omega, sp, flag, counter, send_lo,
                                                                     send_hi);
     if ((*err = cudaGetLastError()) != cudaSuccess) return 0;

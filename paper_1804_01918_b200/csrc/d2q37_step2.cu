@@ -870,13 +870,12 @@ int launch_step2_slab(const double* src, double* dst, const DevGeo& g, const Fac
     step2_interior_bands(g, &nbands, &b_lo, &b_hi);
     if (b_hi - b_lo < 1 || grid < 8 || grid > kSlabMaxCtas || fc.lo == kFacePeriodic || fc.hi == kFacePeriodic)
         return 0;  // no overlapped form: the caller runs the serial schedule
-    static bool attr = false;
-    if (!attr) {
-        *err = cudaFuncSetAttribute(k_step2_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool attr[64] = {};
+    *err = once_per_device(attr, [] {
+        return cudaFuncSetAttribute(k_step2_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)step2_smem_bytes(kStep2Plain));
-        if (*err != cudaSuccess) return 0;
-        attr = true;
-    }
+    });
+    if (*err != cudaSuccess) return 0;
     SlabPlan sp{};
     sp.lo_band0 = 0;
     sp.lo_nb = b_lo;
