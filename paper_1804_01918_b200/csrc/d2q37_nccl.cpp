@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -18,6 +19,7 @@ namespace d2q37 {
 struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*);
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*);  // optional
     ncclResult_t (*CommDestroy)(ncclComm_t);
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
@@ -54,6 +56,7 @@ const NcclApi* nccl_api(std::string* why) {
              bind(lib, "ncclRecv", api.Recv) && bind(lib, "ncclGroupStart", api.GroupStart) &&
              bind(lib, "ncclGroupEnd", api.GroupEnd) && bind(lib, "ncclGetErrorString", api.GetErrorString);
         if (!ok) err = "libnccl.so.2 lacks a required symbol";
+        if (ok && !bind(lib, "ncclCommInitRankConfig", api.CommInitRankConfig)) api.CommInitRankConfig = nullptr;
     });
     if (!ok) {
         if (why) *why = err;
@@ -84,7 +87,21 @@ int nccl_comm_init(void** comm, int nranks, const unsigned char* id, int rank, s
     ncclUniqueId u;
     std::memcpy(u.internal, id, D2Q37_NCCL_ID_BYTES);
     ncclComm_t c = nullptr;
-    const ncclResult_t r = a->CommInitRank(&c, nranks, u, rank);
+    // At most D2Q37_NCCL_MAX_CTAS (default 2) CTAs per NCCL kernel: the halo exchange runs beside a sweep
+    // that holds every other SM, and a send/recv kernel whose blocks cannot all be resident finishes only
+    // when the sweep frees SMs (a 1-rank ring on one B200: 64 channels, the exchange done at the sweep's
+    // end; with 2, 0.35 ms after its start -- tools/slab_timeline.py).  MB-sized halos need no more.
+    const char* env = std::getenv("D2Q37_NCCL_MAX_CTAS");
+    const int max_ctas = env && *env ? std::atoi(env) : 2;
+    ncclResult_t r;
+    if (a->CommInitRankConfig && max_ctas > 0) {
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.maxCTAs = max_ctas;
+        cfg.minCTAs = 1;
+        r = a->CommInitRankConfig(&c, nranks, u, rank, &cfg);
+    } else {
+        r = a->CommInitRank(&c, nranks, u, rank);
+    }
     if (r != ncclSuccess) return fail(why, a, r, "ncclCommInitRank");
     *comm = c;
     return D2Q37_OK;
