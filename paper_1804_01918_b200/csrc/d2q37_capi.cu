@@ -670,6 +670,28 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
         return n == 0 ? 0 : int(std::max<long long>(1, (pct * n * h->nsm + 100 * n_in - 1) / (100 * n_in)));
     };
     const int c_lo = n_in ? share(n_lo) : 0, c_hi = n_in ? share(n_hi) : 0;
+    const bool single = fc.lo != kFaceGhost && fc.hi != kFaceGhost;
+    if (step2_form() == kStep2Pair && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic && h->g.deep &&
+        h->g.ly >= 128 && n_in + n_faces > 256LL * h->nsm) {  // >= one producer band of rows
+        // y-periodic single domain in the pair form: the periodic images live in the deep ghost rows
+        // (k_wrap6; valid across sweeps), so every band is swept in one launch like a 1-rank slab ring's
+        Faces gf = fc;
+        gf.lo = gf.hi = kFaceGhost;
+        int nbands, b_lo, b_hi;
+        step2_interior_bands(h->g, &nbands, &b_lo, &b_hi);
+        if (!h->h6_valid) CK(launch_wrap6(h->buf[h->cur], h->g, h->stream));
+        {
+            ProfScope ps(h, kProfFused);
+            CK(launch_step2_pair(src, dst, h->g, gf, h->mp, omega, h->d_flag, h->stream, 0, nbands, h->nsm,
+                                 step2_sched() != 0));
+            CK(launch_wrap6(dst, h->g, h->stream));
+        }
+        h->cur = 1 - h->cur;
+        h->time_step += 2;
+        h->h6_valid = true;
+        return D2Q37_OK;
+    }
+    if (single) h->h6_valid = false;
     ProfScope ps(h, kProfFused);
     if (n_in == 0 || n_in + n_faces <= 256LL * h->nsm || c_lo + c_hi > h->nsm / 2) {
         // small lattices (a few persistent-CTA waves of items), or face bands too large a

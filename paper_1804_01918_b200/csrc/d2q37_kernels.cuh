@@ -201,6 +201,8 @@ cudaError_t preload_band_kernels();
 // FUSED2 slab halos (deep SoA geometry): 6 rows per face and population,
 // buffers of halo6_count(g) doubles laid out [p][x][6].
 size_t halo6_count(const DevGeo& g);
+// periodic images of rows ly-6..ly-1 / 0..5 into the deep ghost rows -6..-1 / ly..ly+5 (y-periodic single domain)
+cudaError_t launch_wrap6(double* buf, const DevGeo& g, cudaStream_t s);
 cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s);
 cudaError_t launch_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
                            cudaStream_t s);

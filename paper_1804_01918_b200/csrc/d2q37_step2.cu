@@ -660,6 +660,27 @@ __global__ void __launch_bounds__(256) k_unpack6(double* __restrict__ buf, DevGe
     if (recv_hi) buf[base + g.ly + r] = recv_hi[i];       // rows ly .. ly+5
 }
 
+// Periodic images in the deep ghost rows of a y-periodic single domain: rows -6..-1 <- ly-6..ly-1 and
+// ly..ly+5 <- 0..5 of every physical column and population (the pair form then sweeps it like a 1-rank
+// slab ring, every band in one launch).
+__global__ void __launch_bounds__(256) k_wrap6(double* __restrict__ buf, DevGeo g) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = int(i % (2 * kHalo));
+    const long long px = i / (2 * kHalo);
+    const int x = int(px % g.lx), p = int(px / g.lx);
+    double* const col = buf + elem_of(g, p, x + kHalo, kHalo, 0);  // row y = 0
+    col[r - 2 * kHalo] = col[g.ly - 2 * kHalo + r];
+    col[g.ly + r] = col[r];
+}
+
+cudaError_t launch_wrap6(double* buf, const DevGeo& g, cudaStream_t s) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    k_wrap6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g);
+    return cudaGetLastError();
+}
+
 size_t halo6_count(const DevGeo& g) { return size_t(kNpop) * g.lx * 2 * kHalo; }
 
 cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s) {

@@ -1095,6 +1095,26 @@ def test_fused2_interior_forms_and_schedules_bitwise(gpu, lbm, lx, ly, bc):
         lbm.set_fused2_schedule(prev_sched)
 
 
+def test_fused2_periodic_wrap_across_calls_bitwise(gpu, lbm):
+    """A y-periodic single domain in the pair form keeps its periodic images in the deep ghost rows
+    (k_wrap6 after every sweep, refreshed after any other state change): bit-identical to fused steps
+    across calls, a bc change and back, odd step counts, graph replay (n >= 40) and a reload."""
+    lx, ly = 4096, 1440
+    a = sim_of(lbm, "soa", lx, ly, variant="fused2")
+    b = sim_of(lbm, "soa", lx, ly, variant="fused")
+    a.init_rt_device(31)
+    b.init_rt_device(31)
+    for n, bc in ((4, "periodic"), (2, "wall"), (3, "periodic"), (44, "periodic"), (2, "periodic")):
+        a.step(0.9, n, bc=bc)
+        b.step(0.9, n, bc=bc)
+        assert np.array_equal(a.dump(), b.dump()), (n, bc)
+    mid = b.dump()
+    a.load(mid)
+    a.step(0.9, 4)
+    b.step(0.9, 4)
+    assert np.array_equal(a.dump(), b.dump())
+
+
 @pytest.mark.parametrize("lx,ly", [(2, 5), (3, 6), (6, 130), (4, 250)])
 @pytest.mark.parametrize("bc", ["periodic", "wall"])
 def test_fused2_degenerate_extents_bitwise(gpu, lbm, lx, ly, bc):
