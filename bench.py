@@ -733,10 +733,8 @@ def run_b200(args, dist: Dist):
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
     form = None if STUB else lbm.set_fused2_tuning(-1, -1)[0]
     pair = args.variant == "fused2" and args.layout == "soa" and form == 4
-    if pair and transport is None:  # two launches per sweep: k_step2_pair beside k_step2_split (wall bands)
-        launches += fused_n
-    elif pair and dist.rank in (0, n - 1) and n > 1:  # a global wall: its band's general launch beside
-        launches += fused_n
+    # one launch per sweep (k_step2_pair; walls mirrored in the kernel) -- the bench's walls; a
+    # y-periodic domain adds k_wrap6 (periodic images into the deep ghost rows) per sweep
     # FUSED2: one sweep per timed "fused" interval (k_step2_pair + the face bands' k_step2_split beside it)
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
     upd = steps_per_call(args.variant) if dom == "fused" else 1
@@ -748,8 +746,8 @@ def run_b200(args, dist: Dist):
                             "6-row halo pack, interior in lockstep beside the NCCL exchange; two fused steps per "
                             "HBM sweep, two threads per site)" if pair and transport else
                             "k_step2_pair (two fused pull+collide steps per HBM sweep, temporal blocking; two "
-                            "threads per site, 512-thread CTAs, lockstep band schedule) beside k_step2_split on "
-                            "the two wall bands; the sweep interval covers both" if pair else
+                            "threads per site, 512-thread CTAs, lockstep band schedule; wall bands mirrored in "
+                            "the kernel)" if pair else
                             "k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "
                             "interior bands beside the two wall bands in one launch)") if two else
                            "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),

@@ -750,6 +750,18 @@ int set_step2_sched(int sched) {
     return prev;
 }
 
+// Single-domain wall bands in the pair form itself (mirror tables, one launch per sweep) or, with
+// D2Q37_STEP2_PAIR_WALLS=0, in a general-form launch beside it.  Measured with the mirror tables:
+// 4096 x 4096 +8.7 %, 4096 x 8192 +16 %, 4096 x 16384 within run-to-run noise (DESIGN 3.1.1).
+bool step2_pair_walls() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("D2Q37_STEP2_PAIR_WALLS");
+        v = !(e && *e == '0');
+    }
+    return v != 0;
+}
+
 namespace {
 int g_face_pct = -1;  // 0: the form's default
 }  // namespace
@@ -778,9 +790,10 @@ void step2_bands(const DevGeo& g, const Faces& fc, int form, int* nbands, int* b
     const int inside_hi = g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0;  // bands with rows < ly
     if (per_lo && per_hi) {
         if (form != kStep2Plain) lo = 1, hi = inside_hi;  // the bulk-copy forms read rows unwrapped
-    } else if (form == kStep2Pair && !per_lo && !per_hi && g.ly >= kT2Band && fc.lo != kFaceWall && fc.hi != kFaceWall) {
-        // ghost faces: the pair form reads the deep ghost rows unwrapped, every band is interior (a wall
-        // band costs more in the pair form than in a general-form launch beside it, measured -2 %)
+    } else if (form == kStep2Pair && !per_lo && !per_hi && g.ly >= kT2Band &&
+               ((fc.lo != kFaceWall && fc.hi != kFaceWall) || step2_pair_walls())) {
+        // the pair form reads ghost faces' deep ghost rows unwrapped and mirrors at walls: every band is
+        // interior
     } else {
         // ghost faces read the deep ghost rows unwrapped; wall bands need the general form
         lo = fc.lo == kFaceWall ? 1 : 0;
