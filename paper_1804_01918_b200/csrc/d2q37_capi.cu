@@ -112,6 +112,7 @@ struct d2q37_lattice {
     bool p2p_connected = false;
     bool p2p_dirty = true;  // prv changed outside a step: ghost columns must be re-primed
     bool h6_valid = false;  // FUSED2 slab: prv's 6-row ghost rows hold the neighbours' current rows
+    int h6_kind = -1;       // single domain: what they hold -- periodic images (0) or wall images (1)
     int bc_filled = -1;  // y-major slab: boundary mode of the last bc verb while prv is unchanged (else -1)
     unsigned* d_sweep_counter = nullptr;  // overlapped FUSED2 slab sweeps: face CTAs done (k_step2_slab)
     unsigned sweep_target = 0;            // its value once the last queued sweep's face CTAs are done
@@ -671,24 +672,29 @@ int step2_local(d2q37_lattice* h, double omega, const Faces& fc) {
     };
     const int c_lo = n_in ? share(n_lo) : 0, c_hi = n_in ? share(n_hi) : 0;
     const bool single = fc.lo != kFaceGhost && fc.hi != kFaceGhost;
-    if (step2_form() == kStep2Pair && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic && h->g.deep &&
-        h->g.ly >= 128 && n_in + n_faces > 256LL * h->nsm) {  // >= one producer band of rows
-        // y-periodic single domain in the pair form: the periodic images live in the deep ghost rows
-        // (k_wrap6; valid across sweeps), so every band is swept in one launch like a 1-rank slab ring's
+    const bool per = fc.lo == kFacePeriodic && fc.hi == kFacePeriodic, walls = fc.lo == kFaceWall && fc.hi == kFaceWall;
+    if (step2_form() == kStep2Pair && (per || (walls && step2_ghost_walls())) && h->g.deep && h->g.ly >= 128 &&
+        n_in + n_faces > 256LL * h->nsm) {  // >= one producer band of rows
+        // single domain in the pair form: the periodic images (k_wrap6) or the specular-wall images
+        // (k_mirror6) live in the deep ghost rows, valid across sweeps, so every band is swept in one
+        // launch like a 1-rank slab ring's (ghost rows read unwrapped)
         Faces gf = fc;
         gf.lo = gf.hi = kFaceGhost;
+        const int kind = per ? 0 : 1;
+        auto fill = [&](double* buf) { return per ? launch_wrap6(buf, h->g, h->stream) : launch_mirror6(buf, h->g, fc, h->stream); };
         int nbands, b_lo, b_hi;
         step2_interior_bands(h->g, &nbands, &b_lo, &b_hi);
-        if (!h->h6_valid) CK(launch_wrap6(h->buf[h->cur], h->g, h->stream));
+        if (!h->h6_valid || h->h6_kind != kind) CK(fill(h->buf[h->cur]));
         {
             ProfScope ps(h, kProfFused);
             CK(launch_step2_pair(src, dst, h->g, gf, h->mp, omega, h->d_flag, h->stream, 0, nbands, h->nsm,
                                  step2_sched() != 0));
-            CK(launch_wrap6(dst, h->g, h->stream));
+            CK(fill(dst));
         }
         h->cur = 1 - h->cur;
         h->time_step += 2;
         h->h6_valid = true;
+        h->h6_kind = kind;
         return D2Q37_OK;
     }
     if (single) h->h6_valid = false;

@@ -134,6 +134,7 @@ int set_step2_form(int form);
 // march the same columns together; the default), 0 = band-major item ranges.
 // Environment D2Q37_STEP2_SCHED selects one; set_step2_sched returns the previous.
 int step2_sched();
+bool step2_ghost_walls();
 int set_step2_sched(int sched);
 // percent cost of a face-band (general form) item relative to an interior item,
 // which sizes the face CTA groups of k_step2_split (0 = the form's default)
@@ -203,6 +204,8 @@ cudaError_t preload_band_kernels();
 size_t halo6_count(const DevGeo& g);
 // periodic images of rows ly-6..ly-1 / 0..5 into the deep ghost rows -6..-1 / ly..ly+5 (y-periodic single domain)
 cudaError_t launch_wrap6(double* buf, const DevGeo& g, cudaStream_t s);
+// specular-wall images (population ybar at the mirror row) into the deep ghost rows (walls at both faces)
+cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s);
 cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s);
 cudaError_t launch_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
                            cudaStream_t s);

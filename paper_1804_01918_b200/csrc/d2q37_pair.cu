@@ -68,8 +68,9 @@ __device__ __forceinline__ void tmem_ld8(unsigned taddr, double (&v)[4]) {
 
 // The pair's partial sums: this warp's half into its columns, barrier with the
 // partner warp (64 threads), the partner's half back.  Columns alternate with
-// the iteration parity, so a fast thread's next store never overwrites
-// values its partner has not read yet.
+// the swap count's parity (and the role barriers 2 / 3 separate consecutive
+// swaps of a role), so a fast warp's next store never overwrites values its
+// partner has not read yet.
 __device__ __forceinline__ void pair_swap(unsigned tbase, int role, int par, int half, int barid,
                                           const double (&mine)[4], double (&other)[4]) {
     const unsigned lane_base = unsigned((threadIdx.x >> 5) & 3) * 32u << 16;
@@ -264,7 +265,7 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
                 });
             }
             consume_regs(f, [](int p) { return pop_half(p) == H; });
-            bad |= pair_collide<H>(f, mp, omega, tbase, 0, t & 1, pbar);
+            bad |= pair_collide<H>(f, mp, omega, tbase, 0, int(used & 1u), pbar);  // parity: runs across segments
             // the consumers have read this iteration's slots -- and every producer has read the stage
             // (before its collide): refill it with column t + 2
             asm volatile("bar.sync 2, 512;" ::: "memory");
@@ -289,6 +290,7 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
     const int lx = g.lx, ly = g.ly;
     const long long plane = g.pstride, cs = g.cstride;
     const int cbar = 8 + (warp & 3);
+    unsigned swaps = 0;  // TMEM column parity of the pair swaps, running across segments
     int band, xs, xe;
     bool was_face = sched_in_face(sched);
     while (sched.next(band, xs, xe)) {
@@ -348,7 +350,7 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
             }
             asm volatile("bar.arrive 2, 512;" ::: "memory");
             if (t >= 7) {
-                const bool b = pair_collide<H>(v, mp, omega, tbase, 1, t & 1, cbar);
+                const bool b = pair_collide<H>(v, mp, omega, tbase, 1, int(swaps++ & 1u), cbar);
                 if (active) {
                     bad |= b;
                     const int x = xs - 7 + t;

@@ -675,6 +675,31 @@ __global__ void __launch_bounds__(256) k_wrap6(double* __restrict__ buf, DevGeo 
     col[g.ly + r] = col[r];
 }
 
+// Specular-wall images in the deep ghost rows: population p at ghost row -1-r holds ybar(p)
+// = (cx, -cy) at row r, at row ly+r holds ybar(p) at row ly-1-r (r = 0..5).  An unwrapped pull into
+// them is then the wall's mirrored pull, and the sweep's step-1 values on the ghost rows come out as
+// the mirror images of rows 0..2 / ly-3..ly-1 (the FAST collide is exactly reflection-equivariant:
+// the pair-sum moments flip jy by an exact subtraction, the sign-symmetric equilibrium swaps P +- S /
+// Q +- T), so a wall sweep needs no mirror tables.
+__global__ void __launch_bounds__(256) k_mirror6(double* __restrict__ buf, DevGeo g, Faces fc) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = int(i % (2 * kHalo));
+    const long long px = i / (2 * kHalo);
+    const int x = int(px % g.lx), p = int(px / g.lx);
+    double* const col = buf + elem_of(g, p, x + kHalo, kHalo, 0);  // row y = 0 of population p
+    const double* const img = buf + elem_of(g, fc.ybar[p], x + kHalo, kHalo, 0);
+    col[-1 - r] = img[r];
+    col[g.ly + r] = img[g.ly - 1 - r];
+}
+
+cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s) {
+    const long long n = (long long)kNpop * g.lx * 2 * kHalo;
+    k_mirror6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g, fc);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_wrap6(double* buf, const DevGeo& g, cudaStream_t s) {
     const long long n = (long long)kNpop * g.lx * 2 * kHalo;
     k_wrap6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g);
@@ -748,6 +773,17 @@ int set_step2_sched(int sched) {
     const int prev = step2_sched();
     g_sched = sched != 0;
     return prev;
+}
+
+// Single-domain walls through wall images in the deep ghost rows (k_mirror6, the sweep reads them like a
+// ghost face): D2Q37_STEP2_GHOST_WALLS=0 turns it off (then the mirror tables below, or the side launch).
+bool step2_ghost_walls() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("D2Q37_STEP2_GHOST_WALLS");
+        v = !(e && *e == '0');
+    }
+    return v != 0;
 }
 
 // Single-domain wall bands in the pair form itself (mirror tables, one launch per sweep) or, with

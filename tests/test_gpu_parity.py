@@ -1095,16 +1095,19 @@ def test_fused2_interior_forms_and_schedules_bitwise(gpu, lbm, lx, ly, bc):
         lbm.set_fused2_schedule(prev_sched)
 
 
-def test_fused2_periodic_wrap_across_calls_bitwise(gpu, lbm):
-    """A y-periodic single domain in the pair form keeps its periodic images in the deep ghost rows
-    (k_wrap6 after every sweep, refreshed after any other state change): bit-identical to fused steps
-    across calls, a bc change and back, odd step counts, graph replay (n >= 40) and a reload."""
+def test_fused2_ghost_images_across_calls_bitwise(gpu, lbm):
+    """A single domain in the pair form keeps periodic images (k_wrap6) or specular-wall images
+    (k_mirror6: population ybar at the mirror row) in its deep ghost rows, refreshed after every sweep
+    and after any other state change or a bc change: bit-identical to fused steps (whose walls mirror
+    in the pull) across calls, bc changes both ways, odd step counts, graph replay (n >= 40) and a
+    reload."""
     lx, ly = 4096, 1440
     a = sim_of(lbm, "soa", lx, ly, variant="fused2")
     b = sim_of(lbm, "soa", lx, ly, variant="fused")
     a.init_rt_device(31)
     b.init_rt_device(31)
-    for n, bc in ((4, "periodic"), (2, "wall"), (3, "periodic"), (44, "periodic"), (2, "periodic")):
+    for n, bc in ((4, "periodic"), (2, "wall"), (3, "periodic"), (44, "wall"), (2, "periodic"), (44, "periodic"),
+                  (6, "wall")):
         a.step(0.9, n, bc=bc)
         b.step(0.9, n, bc=bc)
         assert np.array_equal(a.dump(), b.dump()), (n, bc)
