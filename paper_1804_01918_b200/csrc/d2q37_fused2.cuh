@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <utility>
 
 #include "d2q37_device.cuh"
@@ -44,13 +45,13 @@ D2Q37_HD constexpr int ybar_of(int p) { return vel_index(cx_of(p), -cy_of(p)); }
 struct RangeSched {
     int band0, lx;
     long long item, end;
-    __device__ RangeSched(int band0_, int nbands, int lx_, long long b, long long e)
-        : band0(band0_), lx(lx_), item(b), end(min((long long)nbands * lx_, e)) {}
-    __device__ __forceinline__ bool next(int& band, int& xs, int& xe) {
+    D2Q37_HD RangeSched(int band0_, int nbands, int lx_, long long b, long long e)
+        : band0(band0_), lx(lx_), item(b), end((long long)nbands * lx_ < e ? (long long)nbands * lx_ : e) {}
+    D2Q37_HD __forceinline__ bool next(int& band, int& xs, int& xe) {
         if (item >= end) return false;
         band = band0 + (int)(item / lx);
         xs = (int)(item % lx);
-        xe = (int)min((long long)lx, xs + (end - item));
+        xe = (int)((long long)lx < xs + (end - item) ? (long long)lx : xs + (end - item));
         item += xe - xs;
         return true;
     }
@@ -74,15 +75,15 @@ struct LockSched {
     int band0, lx, G, c, k;
     Lockstep ls;
     long long j, jend;
-    __device__ LockSched(int band0_, int lx_, int G_, int c_, const Lockstep& l)
+    D2Q37_HD LockSched(int band0_, int lx_, int G_, int c_, const Lockstep& l)
         : band0(band0_), lx(lx_), G(G_), c(c_), k(0), ls(l), j(0), jend(0) {
         if (c >= ls.rem && ls.rem > 0) {
             const long long w = lx - ls.cut;
             j = (long long)(c - ls.rem) * ls.tail_per;
-            jend = min(j + ls.tail_per, (long long)ls.rem * w);
+            jend = j + ls.tail_per < (long long)ls.rem * w ? j + ls.tail_per : (long long)ls.rem * w;
         }
     }
-    __device__ __forceinline__ bool next(int& band, int& xs, int& xe) {
+    D2Q37_HD __forceinline__ bool next(int& band, int& xs, int& xe) {
         if (k < ls.full) {
             band = band0 + c + k * G;
             xs = 0;
@@ -103,7 +104,7 @@ struct LockSched {
         const int w = lx - ls.cut;
         band = base + (int)(j / w);
         xs = ls.cut + (int)(j % w);
-        xe = (int)min((long long)lx, xs + (jend - j));
+        xe = (int)((long long)lx < xs + (jend - j) ? (long long)lx : xs + (jend - j));
         j += xe - xs;
         return true;
     }
@@ -124,6 +125,99 @@ inline Lockstep lockstep_plan(int nb, int G, int lx) {
     }
     return ls;
 }
+// Bands of a sweep: [b_lo, b_hi) pull only rows inside [0, ly) (band 0 pulls rows down to -6, the bands
+// from (ly - 128) / 120 + 1 on reach past ly); degenerate extents: none.
+inline void interior_bands(int lx, int ly, int* nbands, int* b_lo, int* b_hi) {
+    *nbands = (ly + kT2Out - 1) / kT2Out;
+    *b_lo = 1;
+    *b_hi = std::min(*nbands, ly >= kT2Band ? (ly - kT2Band) / kT2Out + 1 : 0);
+    if (lx < kHalo || *b_hi <= *b_lo) *b_lo = *b_hi = 0;
+}
+
+// Item schedule of a y-slab face CTA (k_step2_pair_slab): its share of the face band(s) -- whose new
+// edge rows go to the send buffers and, once stored, are announced on the sweep counter -- then its
+// share of the interior bands next to them.
+struct FaceSched {
+    RangeSched face, adj;
+    bool in_face;
+    D2Q37_HD __forceinline__ bool next(int& band, int& xs, int& xe) {
+        if (in_face) {
+            if (face.next(band, xs, xe)) return true;
+            in_face = false;
+        }
+        return adj.next(band, xs, xe);
+    }
+};
+
+// One overlapped FUSED2 slab sweep in the pair form (k_step2_pair_slab).  CTAs [0, nf_lo) /
+// [nf_lo, nf_lo + nf_hi) sweep the ghost-face band(s) of the low / high face first -- packing the new
+// edge rows into the send buffers and announcing them on the sweep counter -- then the interior bands
+// next to them; the other CTAs march the remaining bands in lockstep, a global wall's band among them
+// (mirror tables).
+struct PairSlabPlan {
+    int nf_lo, nf_hi;
+    int lo_face0, lo_face_nb, lo_adj0, lo_adj_nb;  // bands
+    int hi_face0, hi_face_nb, hi_adj0, hi_adj_nb;
+    long long lo_face_per, lo_adj_per, hi_face_per, hi_adj_per;  // items per face CTA
+    int main_band0, main_nb;
+    Lockstep ls;  // main CTAs: grid - nf_lo - nf_hi
+    int walls;    // bit 0 / 1: the low / high face is a global wall (its band is a main band)
+};
+
+// The plan of one slab sweep on `grid` CTAs (face kinds kFaceGhost = 3 / kFaceWall = 1); false: no
+// overlapped pair form for this slab (no ghost face, too few bands, edge rows outside the face bands).
+inline bool pair_slab_plan(int lx, int ly, int face_lo, int face_hi, int grid, PairSlabPlan* out) {
+    constexpr int kGhost = 3, kWall = 1;
+    int nbands, b_lo, b_hi;
+    interior_bands(lx, ly, &nbands, &b_lo, &b_hi);
+    const bool ghost_lo = face_lo == kGhost, ghost_hi = face_hi == kGhost;
+    const bool wall_lo = face_lo == kWall, wall_hi = face_hi == kWall;
+    // the new edge rows must lie in the face bands: a full first band, >= 6 rows in the last one
+    if (!(ghost_lo || ghost_hi) || !(ghost_lo || wall_lo) || !(ghost_hi || wall_hi) || b_lo != 1 ||
+        b_hi - b_lo < 3 || grid < 16 || ly - (nbands - 1) * kT2Out < 2 * kHalo || ly < kT2Out)
+        return false;
+    const long long lo_items = (long long)b_lo * lx, hi_items = (long long)(nbands - b_hi) * lx;
+    const double per = double(nbands) * lx / grid;  // items per CTA
+    PairSlabPlan sp{};
+    sp.walls = (wall_lo ? 1 : 0) | (wall_hi ? 2 : 0);
+    // ghost faces: enough CTAs that a face share is at most a third of a CTA's work (the exchange then
+    // starts a third into the sweep and hides under the rest: tools/slab_timeline.py), topped up with whole
+    // interior bands next to the face; a wall face's band is an ordinary main band
+    auto face_ctas = [&](long long items) {
+        return std::max(1, std::min(grid / 8, (int)std::ceil(3.0 * items / per)));
+    };
+    int k_lo = 0, k_hi = 0;
+    if (ghost_lo) {
+        sp.nf_lo = face_ctas(lo_items);
+        k_lo = std::max(0, (int)std::floor(sp.nf_lo * per / lx) - b_lo);
+    }
+    if (ghost_hi) {
+        sp.nf_hi = face_ctas(hi_items);
+        k_hi = std::max(0, (int)std::floor(sp.nf_hi * per / lx) - (nbands - b_hi));
+    }
+    while (k_lo + k_hi > b_hi - b_lo - 1) (k_lo >= k_hi ? k_lo : k_hi)--;  // keep >= 1 main band
+    sp.lo_face0 = 0;
+    sp.lo_face_nb = ghost_lo ? b_lo : 0;
+    sp.lo_adj0 = b_lo;
+    sp.lo_adj_nb = k_lo;
+    sp.hi_face0 = b_hi;
+    sp.hi_face_nb = ghost_hi ? nbands - b_hi : 0;
+    sp.hi_adj0 = b_hi - k_hi;
+    sp.hi_adj_nb = k_hi;
+    auto share = [](long long items, int n) { return n ? (items + n - 1) / n : 0LL; };
+    sp.lo_face_per = share(lo_items, sp.nf_lo);
+    sp.lo_adj_per = share((long long)k_lo * lx, sp.nf_lo);
+    sp.hi_face_per = share(hi_items, sp.nf_hi);
+    sp.hi_adj_per = share((long long)k_hi * lx, sp.nf_hi);
+    sp.main_band0 = ghost_lo ? b_lo + k_lo : 0;
+    sp.main_nb = (ghost_hi ? b_hi - k_hi : nbands) - sp.main_band0;
+    const int gmain = grid - sp.nf_lo - sp.nf_hi;
+    if (gmain < 1 || sp.main_nb < 1) return false;
+    sp.ls = lockstep_plan(sp.main_nb, gmain, lx);
+    *out = sp;
+    return true;
+}
+
 // Part 0 of k_step2_split: band-major ranges or the lockstep schedule.
 struct PartSched {
     bool lock;

@@ -44,6 +44,7 @@ namespace d2q37 {
 namespace {
 
 constexpr int kPairThreads = 4 * kT2Band;  // 512
+static_assert(kFaceGhost == 3 && kFaceWall == 1, "pair_slab_plan's face kinds (d2q37_fused2.cuh)");
 constexpr int kTmemCols = 64;              // [role][parity][half] x 8 32-bit columns (4 doubles)
 
 __device__ __forceinline__ void tmem_st8(unsigned taddr, const double (&v)[4]) {
@@ -170,21 +171,6 @@ __device__ __forceinline__ StageIssuer make_issuer(const double* sb, const DevGe
     is.isrc = sb;
     return is;
 }
-
-// Item schedule of a y-slab face CTA (k_step2_pair_slab): its share of the face band(s) -- whose new
-// edge rows go to the send buffers and, once stored, are announced on the sweep counter -- then its
-// share of the interior bands next to them.
-struct FaceSched {
-    RangeSched face, adj;
-    bool in_face;
-    __device__ __forceinline__ bool next(int& band, int& xs, int& xe) {
-        if (in_face) {
-            if (face.next(band, xs, xe)) return true;
-            in_face = false;
-        }
-        return adj.next(band, xs, xe);
-    }
-};
 
 // Send-buffer packing and the sweep counter of a face CTA (null: none)
 struct SlabPack {
@@ -448,15 +434,6 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 // sweep the ghost-face band(s) of the low / high face first -- packing the new edge rows into the send
 // buffers and announcing them on the sweep counter -- then the interior bands next to them; the other
 // CTAs march the remaining bands in lockstep, a global wall's band among them (mirror tables).
-struct PairSlabPlan {
-    int nf_lo, nf_hi;
-    int lo_face0, lo_face_nb, lo_adj0, lo_adj_nb;  // bands
-    int hi_face0, hi_face_nb, hi_adj0, hi_adj_nb;
-    long long lo_face_per, lo_adj_per, hi_face_per, hi_adj_per;  // items per face CTA
-    int main_band0, main_nb;
-    Lockstep ls;  // main CTAs: grid - nf_lo - nf_hi
-    int walls;    // bit 0 / 1: the low / high face is a global wall (its band is a main band)
-};
 
 __global__ void __launch_bounds__(kPairThreads, 1)
     k_step2_pair_slab(const double* __restrict__ src, double* __restrict__ dst, DevGeo g, ModelParams mp,
@@ -518,53 +495,8 @@ int launch_step2_pair_slab(const double* src, double* dst, const DevGeo& g, cons
                            double omega, int* flag, cudaStream_t s, int grid, unsigned* counter, double* send_lo,
                            double* send_hi, cudaError_t* err) {
     *err = cudaSuccess;
-    const int lx = g.lx;
-    int nbands, b_lo, b_hi;
-    step2_interior_bands(g, &nbands, &b_lo, &b_hi);
-    const bool ghost_lo = fc.lo == kFaceGhost, ghost_hi = fc.hi == kFaceGhost;
-    const bool wall_lo = fc.lo == kFaceWall, wall_hi = fc.hi == kFaceWall;
-    // the new edge rows must lie in the face bands: a full first band, >= 6 rows in the last one
-    if (!(ghost_lo || ghost_hi) || !(ghost_lo || wall_lo) || !(ghost_hi || wall_hi) || b_lo != 1 ||
-        b_hi - b_lo < 3 || grid < 16 || g.ly - (nbands - 1) * kT2Out < 2 * kHalo || g.ly < kT2Out)
-        return 0;
-    const long long lo_items = (long long)b_lo * lx, hi_items = (long long)(nbands - b_hi) * lx;
-    const double per = double(nbands) * lx / grid;  // items per CTA
     PairSlabPlan sp{};
-    sp.walls = (wall_lo ? 1 : 0) | (wall_hi ? 2 : 0);
-    // ghost faces: enough CTAs that a face share is at most a third of a CTA's work (the exchange then
-    // starts a third into the sweep and hides under the rest: tools/slab_timeline.py), topped up with whole
-    // interior bands next to the face; a wall face's band is an ordinary main band
-    auto face_ctas = [&](long long items) {
-        return std::max(1, std::min(grid / 8, (int)std::ceil(3.0 * items / per)));
-    };
-    int k_lo = 0, k_hi = 0;
-    if (ghost_lo) {
-        sp.nf_lo = face_ctas(lo_items);
-        k_lo = std::max(0, (int)std::floor(sp.nf_lo * per / lx) - b_lo);
-    }
-    if (ghost_hi) {
-        sp.nf_hi = face_ctas(hi_items);
-        k_hi = std::max(0, (int)std::floor(sp.nf_hi * per / lx) - (nbands - b_hi));
-    }
-    while (k_lo + k_hi > b_hi - b_lo - 1) (k_lo >= k_hi ? k_lo : k_hi)--;  // keep >= 1 main band
-    sp.lo_face0 = 0;
-    sp.lo_face_nb = ghost_lo ? b_lo : 0;
-    sp.lo_adj0 = b_lo;
-    sp.lo_adj_nb = k_lo;
-    sp.hi_face0 = b_hi;
-    sp.hi_face_nb = ghost_hi ? nbands - b_hi : 0;
-    sp.hi_adj0 = b_hi - k_hi;
-    sp.hi_adj_nb = k_hi;
-    auto share = [](long long items, int n) { return n ? (items + n - 1) / n : 0LL; };
-    sp.lo_face_per = share(lo_items, sp.nf_lo);
-    sp.lo_adj_per = share((long long)k_lo * lx, sp.nf_lo);
-    sp.hi_face_per = share(hi_items, sp.nf_hi);
-    sp.hi_adj_per = share((long long)k_hi * lx, sp.nf_hi);
-    sp.main_band0 = ghost_lo ? b_lo + k_lo : 0;
-    sp.main_nb = (ghost_hi ? b_hi - k_hi : nbands) - sp.main_band0;
-    const int gmain = grid - sp.nf_lo - sp.nf_hi;
-    if (gmain < 1 || sp.main_nb < 1) return 0;
-    sp.ls = lockstep_plan(sp.main_nb, gmain, lx);
+    if (!pair_slab_plan(g.lx, g.ly, fc.lo, fc.hi, grid, &sp)) return 0;
     static bool attr[64] = {};
     *err = once_per_device(attr, [] {
         return cudaFuncSetAttribute(k_step2_pair_slab, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -902,10 +902,7 @@ cudaError_t launch_step2(const double* src, double* dst, const DevGeo& g, const 
 }
 
 void step2_interior_bands(const DevGeo& g, int* nbands, int* b_lo, int* b_hi) {
-    *nbands = (g.ly + kT2Out - 1) / kT2Out;
-    *b_lo = 1;  // band 0 pulls rows down to -6
-    *b_hi = std::min(*nbands, g.ly >= kT2Band ? (g.ly - kT2Band) / kT2Out + 1 : 0);  // pulls stay below ly
-    if (g.lx < kHalo || *b_hi <= *b_lo) *b_lo = *b_hi = 0;
+    interior_bands(g.lx, g.ly, nbands, b_lo, b_hi);
 }
 
 cudaError_t launch_step2_parts(const double* src, double* dst, const DevGeo& g, const Faces& fc,
