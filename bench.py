@@ -896,10 +896,14 @@ def run_b200(args, dist: Dist):
 
 
 def run_e2e(lbm, sim, args, dist: Dist):
-    """load(host) -> step x n -> dump(host) through the public API, one pinned host canonical per rank.
+    """Host canonical in -> n steps -> host canonical out through the public API, one pinned host
+    canonical per rank.
 
-    The rank's current state is dumped into the host buffer first; every call
-    then loads it, advances n steps and dumps the result back into it.
+    The rank's current state is dumped into the host buffer first.  The headline call is the streamed
+    run, Simulation.run(host, omega, n, out=host) (d2q37_run_canonical): on a single wall domain the
+    upload, the sweeps and the download are pipelined in y-chunks, bit-identical to the three verbs.
+    The three verbs one after another (load + step + dump: nothing overlaps) are timed beside it.
+    Slab ranks have no streamed path and time the three verbs only.
     """
     nsteps = args.e2e_steps
     need = 37 * sim.lx * sim.ly * 8
@@ -912,23 +916,42 @@ def run_e2e(lbm, sim, args, dist: Dist):
     canon = np.empty((37, sim.lx, sim.ly), dtype=np.float64)
     pinned = pin(canon)
     sim.dump(out=canon)
-    times = []
-    for _ in range(1 + args.e2e_iters):  # first call warms the pinned path
-        dist.barrier()
-        t0 = time.perf_counter()
+    sites = LX * sim.ly * dist.world
+
+    def three_verbs():
         sim.load(canon)
         sim.step(OMEGA, nsteps)
         sim.dump(out=canon)
-        times.append(time.perf_counter() - t0)
+
+    def streamed():
+        sim.run(canon, OMEGA, nsteps, out=canon)
+
+    def timed(call):
+        times = []
+        for _ in range(1 + args.e2e_iters):  # first call warms the pinned path
+            dist.barrier()
+            t0 = time.perf_counter()
+            call()
+            times.append(time.perf_counter() - t0)
+        return dist.max(min(times[1:]))
+
+    t3 = timed(three_verbs)
+    rec = {"unit": "MLUPS", "h2d_bytes_per_step": need / nsteps, "d2h_bytes_per_step": need / nsteps,
+           "steps_per_call": nsteps, "h2d_bytes_per_call": need, "d2h_bytes_per_call": need, "pinned": pinned,
+           "three_verbs": {"value": sites * nsteps / t3 / 1e6, "seconds_per_call": t3,
+                           "call": f"Simulation.load(host canonical) + step(0.8, n, {sim.variant}, wall) + "
+                                   "dump(host canonical)"}}
+    if dist.world == 1 and sim.variant == "fused2":
+        t = timed(streamed)
+        rec.update({"value": sites * nsteps / t / 1e6, "seconds_per_call": t,
+                    "call": f"Simulation.run(host canonical, 0.8, n, out=host canonical) [{sim.variant}, wall]: "
+                            "upload, sweeps and download pipelined in y-chunks (d2q37_run_canonical)"})
+    else:
+        rec.update({"value": rec["three_verbs"]["value"], "seconds_per_call": t3,
+                    "call": rec["three_verbs"]["call"]})
     if pinned:
         unpin(canon)
-    t = dist.max(min(times[1:]))
-    sites = LX * sim.ly * dist.world
-    return {"value": sites * nsteps / t / 1e6, "unit": "MLUPS", "h2d_bytes_per_step": need / nsteps,
-            "d2h_bytes_per_step": need / nsteps, "steps_per_call": nsteps,
-            "h2d_bytes_per_call": need, "d2h_bytes_per_call": need, "pinned": pinned,
-            "seconds_per_call": t,
-            "call": f"Simulation.load(host canonical) + step(0.8, n, {sim.variant}, wall) + dump(host canonical)"}
+    return rec
 
 
 def load_ncu_traffic(layout: str, ly: int, variant: str = "fused", pair: bool = False):

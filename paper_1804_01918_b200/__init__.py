@@ -106,6 +106,7 @@ def _load():
         "d2q37_time_step": (C.c_long, [vp]),
         "d2q37_load_canonical": (i, [vp, vp, sz]),
         "d2q37_dump_canonical": (i, [vp, vp, sz]),
+        "d2q37_run_canonical": (i, [vp, vp, vp, sz, d, i, i, i]),
         "d2q37_load_buffer": (i, [vp, i, vp, sz]),
         "d2q37_dump_buffer": (i, [vp, i, vp, sz]),
         "d2q37_load_buffer_device": (i, [vp, i, vp, sz]),
@@ -550,6 +551,22 @@ class Simulation:
         if out.shape != self.shape or not out.flags.c_contiguous or out.dtype != np.float64:
             raise ValueError("out must be a C-contiguous float64 (37, lx, ly) array")
         _check(_load().d2q37_dump_buffer(self._h, which, _ptr(out), out.size))
+        return out
+
+    def run(self, arr, omega: float = 1.0, n: int = 1, *, out: np.ndarray | None = None, bc: str | None = None,
+            variant: str | None = None) -> np.ndarray:
+        """load(arr) + step(omega, n) + dump(out) in one call (d2q37_run_canonical), bit-identical to the
+        three verbs; on a single SoA wall domain with FUSED2 and an even n the copies are pipelined in
+        y-chunks under the sweeps.  ``out`` may be ``arr`` itself (pinned host memory overlaps best)."""
+        a = self._canon_in(arr)
+        if a.shape != self.shape:
+            raise ValueError("expected an array of shape (37, lx, ly)")
+        if out is None:
+            out = np.empty(self.shape, dtype=np.float64)
+        if out.shape != self.shape or not out.flags.c_contiguous or out.dtype != np.float64:
+            raise ValueError("out must be a C-contiguous float64 (37, lx, ly) array")
+        _check(_load().d2q37_run_canonical(self._h, _ptr(a), _ptr(out), a.size, float(omega), int(n),
+                                           VARIANTS[variant or self.variant], BCS[bc or self.bc_mode]))
         return out
 
     def load_device(self, ptr: int, n: int, which: int = 0):

@@ -61,6 +61,7 @@ struct d2q37_lattice {
     // scatter / gather kernel
     double* stage2 = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t copy_stream2 = nullptr;  // streamed run (d2q37_run_canonical): downloads beside the uploads
     cudaEvent_t ev_io[4] = {};
     long time_step = 0;
 
@@ -350,10 +351,12 @@ void free_lattice(d2q37_lattice* h) {
     if (h->halo_stream) cudaStreamSynchronize(h->halo_stream);
     if (h->side_stream) cudaStreamSynchronize(h->side_stream);
     if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    if (h->copy_stream2) cudaStreamSynchronize(h->copy_stream2);
     for (double* p : {h->buf[0], h->buf[1], h->d_part, h->stage, h->stage2, h->send_lo, h->send_hi, h->recv_lo,
                       h->recv_hi, h->h6[0], h->h6[1], h->h6[2], h->h6[3]})
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->copy_stream2) cudaStreamDestroy(h->copy_stream2);
     for (cudaEvent_t e : h->ev_io)
         if (e) cudaEventDestroy(e);
     if (h->d_flag) cudaFree(h->d_flag);
@@ -1348,6 +1351,127 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
     return D2Q37_OK;
 }
 
+// ---- streamed run: load -> nsteps FUSED2 steps -> dump, pipelined in y-chunks -------------------
+//
+// d2q37_run_canonical on a single SoA wall domain.  The canonical host array is [p][x][y]
+// (dump.hpp:19-21), so rows [r0, r1) of every population are one pitched copy each; chunk k of the
+// input is uploaded on the copy stream while the compute stream sweeps the chunks before it, and
+// finished rows are downloaded on a second copy stream (the other DMA direction) while later chunks
+// are still being swept.  A FUSED2 sweep s (two steps) of rows [a, b) needs sweep s - 1 on rows
+// [a - 6, b + 6), so chunk k is swept as a parallelogram: sweep s covers rows
+//     [edge[k] - 6 s, edge[k+1] - 6 s)           (clipped at row 0; the last chunk ends at ly)
+// and every sweep's input rows are then final when it is launched (all in stream order on the compute
+// stream).  The two state buffers still alternate (X_s = sweep s's output; X_s and X_{s-2} share a
+// buffer): sweep s on chunk k overwrites X_{s-2} rows below edge[k+1] - 6 s, and the only reader of
+// X_{s-2} still to come -- sweep s - 1 on chunk k + 1 -- reads rows from edge[k+1] - 6 s on.  The sweep
+// of a row range is the pair form on a pointer-shifted geometry with ghost faces (k_step2_pair<true>,
+// rows beyond the range read as they stand, like a slab's deep ghost rows); the walls stay the wall
+// images of step2_local (k_mirror6 after every sweep that wrote rows 0..5 / ly-6..ly-1).  Results are
+// bit-identical to load + step + dump (same kernel, same values).
+bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, const Faces& fc) {
+    return h->layout == D2Q37_SOA && !h->g.band && h->g.deep && !h->g.tr && h->g.vl == 1 && local_only(h) &&
+           h->math == D2Q37_MATH_FAST && variant == D2Q37_FUSED2 && bc == D2Q37_BC_WALL && fc.lo == kFaceWall &&
+           fc.hi == kFaceWall && step2_form() == kStep2Pair && step2_ghost_walls() && step2_supported(h->g, fc) &&
+           nsteps >= 2 && nsteps % 2 == 0 && h->g.ly >= 4 * step2_band_rows() && !h->prof_on;
+}
+
+// chunk edges (even rows): D2Q37_STREAM_ROWS rows per chunk (default 17 bands), a smaller first chunk
+// (D2Q37_STREAM_FIRST) so the first sweep starts early
+std::vector<int> stream_edges(int ly) {
+    auto env_rows = [](const char* name, int dflt) {
+        const char* e = std::getenv(name);
+        int v = e ? std::atoi(e) : dflt;
+        v = std::max(2 * kHalo, v) & ~1;
+        return v;
+    };
+    const int rows = env_rows("D2Q37_STREAM_ROWS", 17 * step2_band_rows());
+    const int first = std::min(rows, env_rows("D2Q37_STREAM_FIRST", 4 * step2_band_rows()));
+    std::vector<int> edge{0};
+    for (int y = first; y < ly; y += rows) edge.push_back(y);
+    if (ly - edge.back() < 2 * kHalo && edge.size() > 1) edge.pop_back();  // no sliver at the top wall
+    edge.push_back(ly);
+    return edge;
+}
+
+int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, int nsteps, const Faces& fc) {
+    DeviceGuard dg(h->device);
+    const DevGeo& g = h->g;
+    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    if (!h->copy_stream2) CK(cudaStreamCreateWithFlags(&h->copy_stream2, cudaStreamNonBlocking));
+    const std::vector<int> edge = stream_edges(g.ly);
+    const int K = int(edge.size()) - 1, S = nsteps / 2;
+    std::vector<cudaEvent_t> ev(2 * size_t(K) + 1, nullptr);
+    struct EventsGuard {
+        std::vector<cudaEvent_t>& e;
+        ~EventsGuard() {
+            for (cudaEvent_t x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } guard{ev};
+    for (cudaEvent_t& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* const uploaded = ev.data();
+    cudaEvent_t* const swept = ev.data() + K;
+    cudaEvent_t& start = ev[2 * size_t(K)];
+    double* const X[2] = {h->buf[h->cur], h->buf[1 - h->cur]};  // X[s & 1]: the state after sweep s
+    const size_t plane_vals = size_t(g.lx) * g.ly;
+    const long long row0 = site_of(g, kHalo, 0);
+    auto copy_rows = [&](bool up, double* dev, int r0, int r1, cudaStream_t st) -> int {
+        for (int p = 0; p < kNpop; ++p) {
+            double* const d = dev + row0 + p * g.pstride + r0;
+            if (up)
+                CK(cudaMemcpy2DAsync(d, size_t(g.cstride) * sizeof(double), in + p * plane_vals + r0,
+                                     size_t(g.ly) * sizeof(double), size_t(r1 - r0) * sizeof(double), size_t(g.lx),
+                                     cudaMemcpyHostToDevice, st));
+            else
+                CK(cudaMemcpy2DAsync(out + p * plane_vals + r0, size_t(g.ly) * sizeof(double), d,
+                                     size_t(g.cstride) * sizeof(double), size_t(r1 - r0) * sizeof(double),
+                                     size_t(g.lx), cudaMemcpyDeviceToHost, st));
+        }
+        return D2Q37_OK;
+    };
+    Faces gf = fc;
+    gf.lo = gf.hi = kFaceGhost;
+    const bool lock = step2_sched() != 0;
+    // the copies start after whatever the lattice's stream still has queued
+    CK(cudaEventRecord(start, h->stream));
+    CK(cudaStreamWaitEvent(h->copy_stream, start, 0));
+    CK(cudaStreamWaitEvent(h->copy_stream2, start, 0));
+    for (int k = 0; k < K; ++k) {
+        RET(copy_rows(true, X[0], edge[k], edge[k + 1], h->copy_stream));
+        CK(cudaEventRecord(uploaded[k], h->copy_stream));
+    }
+    for (int k = 0; k < K; ++k) {
+        const bool last = k == K - 1;
+        CK(cudaStreamWaitEvent(h->stream, uploaded[k], 0));
+        if (k == 0) CK(launch_mirror6(X[0], g, fc, h->stream, 1));
+        if (last) CK(launch_mirror6(X[0], g, fc, h->stream, 2));
+        int lo = 0, hi = 0;
+        for (int s = 1; s <= S; ++s) {
+            lo = k == 0 ? 0 : std::max(0, edge[k] - 2 * kHalo * s);
+            hi = last ? g.ly : std::max(0, edge[k + 1] - 2 * kHalo * s);
+            if (hi <= lo) continue;
+            DevGeo gs = g;
+            gs.ly = hi - lo;
+            const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
+            CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, h->stream, 0, nb,
+                                 h->nsm, lock));
+            const int mask = (lo == 0 ? 1 : 0) | (hi == g.ly ? 2 : 0);
+            if (mask) CK(launch_mirror6(X[s & 1], g, fc, h->stream, mask));
+        }
+        CK(cudaEventRecord(swept[k], h->stream));
+        CK(cudaStreamWaitEvent(h->copy_stream2, swept[k], 0));
+        if (hi > lo) RET(copy_rows(false, X[S & 1], lo, hi, h->copy_stream2));
+    }
+    h->cur = S & 1 ? 1 - h->cur : h->cur;
+    h->time_step += nsteps;
+    h->h6_valid = true;
+    h->h6_kind = 1;
+    CK(cudaStreamSynchronize(h->copy_stream2));
+    CK(cudaStreamSynchronize(h->copy_stream));
+    return D2Q37_OK;
+}
+
 // ymajor: store the lattice transposed (storage columns along y, rows along x)
 // -- the y-slab layout of the site-major layouts, whose slab faces are then
 // whole contiguous storage columns.
@@ -1463,6 +1587,28 @@ int d2q37_load_canonical(d2q37_lattice* h, const double* host, size_t n) {
     return load_canonical_impl(h, 0, host, n, false);
 }
 int d2q37_dump_canonical(d2q37_lattice* h, double* host, size_t n) { return dump_canonical_impl(h, 0, host, n, false); }
+
+int d2q37_run_canonical(d2q37_lattice* h, const double* host_in, double* host_out, size_t n, double omega, int nsteps,
+                        int variant, int bc) {
+    RET(check_handle(h));
+    if (n != canon_count(h)) return fail(D2Q37_ERR_INVALID_ARGUMENT, "run_canonical: dimension mismatch");
+    if (!host_in || !host_out) return fail(D2Q37_ERR_INVALID_ARGUMENT, "null canonical array");
+    if (nsteps < 0) return fail(D2Q37_ERR_INVALID_ARGUMENT, "nsteps must be >= 0");
+    if (variant != D2Q37_FUSED && variant != D2Q37_UNFUSED && variant != D2Q37_FUSED2)
+        return fail(D2Q37_ERR_INVALID_ARGUMENT, "unknown variant");
+    RET(validate_bc(h, bc));
+    const Faces fc = step_faces(h, bc);
+    const char* off = std::getenv("D2Q37_STREAM_RUN");
+    if (!(off && std::atoi(off) == 0) && can_stream_run(h, nsteps, variant, bc, fc)) {
+        h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
+        RET(run_streamed(h, host_in, host_out, omega, nsteps, fc));
+        return d2q37_sync(h);
+    }
+    RET(load_canonical_impl(h, 0, host_in, n, false));
+    RET(d2q37_step(h, omega, nsteps, variant, bc));
+    RET(d2q37_sync(h));
+    return dump_canonical_impl(h, 0, host_out, n, false);
+}
 int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n) {
     return load_canonical_impl(h, which, host, n, false);
 }

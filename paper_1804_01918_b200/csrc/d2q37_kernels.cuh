@@ -128,6 +128,7 @@ long long step2_items(const DevGeo& g, const Faces& fc, int part);
 // 3 = two bulk-copy stages beside a 148-column ring (sweep_tma2).
 // 4 = form 3 with two threads per site (k_step2_pair, d2q37_pair.cu).
 enum { kStep2Plain = 0, kStep2Bulk = 1, kStep2BulkEarly = 2, kStep2Bulk2 = 3, kStep2Pair = 4 };
+int step2_band_rows();  // output rows per band (kT2Out)
 int step2_form();
 int set_step2_form(int form);
 // Interior schedule of the plain form: 1 = lockstep (CTAs of neighbouring bands
@@ -204,8 +205,9 @@ cudaError_t preload_band_kernels();
 size_t halo6_count(const DevGeo& g);
 // periodic images of rows ly-6..ly-1 / 0..5 into the deep ghost rows -6..-1 / ly..ly+5 (y-periodic single domain)
 cudaError_t launch_wrap6(double* buf, const DevGeo& g, cudaStream_t s);
-// specular-wall images (population ybar at the mirror row) into the deep ghost rows (walls at both faces)
-cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s);
+// specular-wall images (population ybar at the mirror row) into the deep ghost rows (walls at both faces);
+// mask: bit 0 the low face's rows -6..-1, bit 1 the high face's rows ly..ly+5
+cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s, int mask = 3);
 cudaError_t launch_pack6(const double* buf, const DevGeo& g, double* send_lo, double* send_hi, cudaStream_t s);
 cudaError_t launch_unpack6(double* buf, const DevGeo& g, const double* recv_lo, const double* recv_hi,
                            cudaStream_t s);

@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(256) k_wrap6(double* __restrict__ buf, DevGeo 
 // the mirror images of rows 0..2 / ly-3..ly-1 (the FAST collide is exactly reflection-equivariant:
 // the pair-sum moments flip jy by an exact subtraction, the sign-symmetric equilibrium swaps P +- S /
 // Q +- T), so a wall sweep needs no mirror tables.
-__global__ void __launch_bounds__(256) k_mirror6(double* __restrict__ buf, DevGeo g, Faces fc) {
+__global__ void __launch_bounds__(256) k_mirror6(double* __restrict__ buf, DevGeo g, Faces fc, int mask) {
     const long long n = (long long)kNpop * g.lx * 2 * kHalo;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -690,13 +690,13 @@ __global__ void __launch_bounds__(256) k_mirror6(double* __restrict__ buf, DevGe
     const int x = int(px % g.lx), p = int(px / g.lx);
     double* const col = buf + elem_of(g, p, x + kHalo, kHalo, 0);  // row y = 0 of population p
     const double* const img = buf + elem_of(g, fc.ybar[p], x + kHalo, kHalo, 0);
-    col[-1 - r] = img[r];
-    col[g.ly + r] = img[g.ly - 1 - r];
+    if (mask & 1) col[-1 - r] = img[r];
+    if (mask & 2) col[g.ly + r] = img[g.ly - 1 - r];
 }
 
-cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s) {
+cudaError_t launch_mirror6(double* buf, const DevGeo& g, const Faces& fc, cudaStream_t s, int mask) {
     const long long n = (long long)kNpop * g.lx * 2 * kHalo;
-    k_mirror6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g, fc);
+    k_mirror6<<<unsigned((n + 255) / 256), 256, 0, s>>>(buf, g, fc, mask);
     return cudaGetLastError();
 }
 
@@ -742,6 +742,8 @@ size_t step2_smem_bytes(int form) {
 namespace {
 int g_form = -1;  // interior-band form of every FUSED2 sweep (step2_form)
 }  // namespace
+
+int step2_band_rows() { return kT2Out; }
 
 int step2_form() {
     if (g_form < 0) {

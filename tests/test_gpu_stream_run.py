@@ -1,0 +1,126 @@
+"""The streamed run (d2q37_run_canonical / Simulation.run): load + step + dump as one call.
+
+The reference's host-side sequence is LatticeState::load, n x lbm::step, LatticeState::dump
+(lattice.hpp:18-19, kernels.cpp:276-283; module.cpp:44-99 for the Python Simulation).  The streamed
+run must return exactly what those three verbs return, bit for bit, whether it pipelines the copies
+under the sweeps (single SoA wall domain, FUSED2, even n: y-chunks swept as parallelograms of
+sweeps) or falls back to the three verbs one after another (every other case).
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+OMEGA = 0.8
+
+
+class _Env:
+    def __init__(self, **kv):
+        self.kv = {k: str(v) for k, v in kv.items()}
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _three_verbs(lbm, init, n, bc="wall", variant="fused2"):
+    lx, ly = init.shape[1:]
+    s = lbm.Simulation("soa", lx, ly, device=0, bc=bc, variant=variant)
+    s.load(init)
+    s.step(OMEGA, n)
+    out = s.dump()
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("rows,first,n", [(480, 240, 20), (240, 120, 100), (600, 600, 2), (2040, 480, 40)])
+def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, n):
+    """Several chunk heights, including chunks shorter than the 6-rows-per-sweep skew accumulates to
+    (240 rows against 50 sweeps x 6 rows) and a single sweep."""
+    lx, ly = 1024, 2400
+    init = lbm.make_lattice("rt", lx, ly, seed=777)
+    want = _three_verbs(lbm, init, n)
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    with _Env(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=first):
+        got = s.run(init, OMEGA, n)
+    assert np.array_equal(got, want)
+    assert s.time_step == n
+    # the lattice is left in the state the three verbs leave it in: stepping on agrees too
+    s.step(OMEGA, 3)
+    assert np.array_equal(s.dump(), _three_verbs(lbm, init, n + 3))
+    s.close()
+
+
+def test_streamed_run_in_place_and_repeated(gpu, lbm):
+    """out may be the input array; a second run on the same handle starts from the new input."""
+    lx, ly = 512, 1920
+    init = lbm.make_lattice("rt", lx, ly, seed=5)
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    buf = init.copy()
+    with _Env(D2Q37_STREAM_ROWS=360, D2Q37_STREAM_FIRST=120):
+        s.run(buf, OMEGA, 10, out=buf)
+        assert np.array_equal(buf, _three_verbs(lbm, init, 10))
+        s.run(buf, OMEGA, 6, out=buf)  # an odd sweep count: the state ends in the other buffer
+    assert np.array_equal(buf, _three_verbs(lbm, init, 16))
+    assert np.array_equal(s.dump(), buf)
+    s.close()
+
+
+def test_streamed_run_default_chunks_larger_lattice(gpu, lbm):
+    """Default chunk heights (17 bands, first chunk 4 bands) on a lattice wide enough for the lockstep
+    schedule's full rounds."""
+    lx, ly = 4096, 4800
+    a = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    a.init_rt_device(2018)
+    init = a.dump()
+    a.step(OMEGA, 8)
+    want = a.dump()
+    got = a.run(init, OMEGA, 8)
+    assert np.array_equal(got, want)
+    a.close()
+
+
+@pytest.mark.parametrize("bc,variant,n", [("periodic", "fused2", 6), ("wall", "fused2", 5), ("wall", "fused", 4),
+                                          ("wall", "unfused", 2)])
+def test_run_falls_back_to_three_verbs(gpu, lbm, bc, variant, n):
+    lx, ly = 256, 600
+    init = lbm.make_lattice("rt", lx, ly, seed=11)
+    s = lbm.Simulation("soa", lx, ly, device=0, bc=bc, variant=variant)
+    got = s.run(init, OMEGA, n)
+    assert np.array_equal(got, _three_verbs(lbm, init, n, bc, variant))
+    s.close()
+
+
+def test_run_other_layouts_and_switch(gpu, lbm):
+    """Layouts without the streamed path, and D2Q37_STREAM_RUN=0 on one that has it."""
+    lx, ly = 256, 640
+    init = lbm.make_lattice("rt", lx, ly, seed=3)
+    want = _three_verbs(lbm, init, 4)
+    for layout, vl in (("caosoa", 32), ("csoa", 8), ("aos", 1)):
+        s = lbm.Simulation(layout, lx, ly, vl, device=0, bc="wall", variant="fused2")
+        assert np.array_equal(s.run(init, OMEGA, 4), want)
+        s.close()
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    with _Env(D2Q37_STREAM_RUN=0):
+        assert np.array_equal(s.run(init, OMEGA, 4), want)
+    s.close()
+
+
+def test_streamed_run_reports_nonphysical(gpu, lbm):
+    """A non-positive density inside a streamed sweep surfaces as NonPhysicalError from run()."""
+    lx, ly = 512, 1200
+    init = lbm.make_lattice("rt", lx, ly, seed=9)
+    init[:, 100, 700] = -1.0
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    with pytest.raises(lbm.NonPhysicalError):
+        s.run(init, OMEGA, 4)
+    s.close()
