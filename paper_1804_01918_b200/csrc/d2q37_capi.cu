@@ -1359,11 +1359,11 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
 // finished rows are downloaded on a second copy stream (the other DMA direction) while later chunks
 // are still being swept.  A FUSED2 sweep s (two steps) of rows [a, b) needs sweep s - 1 on rows
 // [a - 6, b + 6), so chunk k is swept as a parallelogram: sweep s covers rows
-//     [edge[k] - 6 s, edge[k+1] - 6 s)           (clipped at row 0; the last chunk ends at ly)
+//     [edge[k] - d s, edge[k+1] - d s),  d >= 6   (clipped at row 0; the last chunk ends at ly)
 // and every sweep's input rows are then final when it is launched (all in stream order on the compute
 // stream).  The two state buffers still alternate (X_s = sweep s's output; X_s and X_{s-2} share a
-// buffer): sweep s on chunk k overwrites X_{s-2} rows below edge[k+1] - 6 s, and the only reader of
-// X_{s-2} still to come -- sweep s - 1 on chunk k + 1 -- reads rows from edge[k+1] - 6 s on.  The sweep
+// buffer): sweep s on chunk k overwrites X_{s-2} rows below edge[k+1] - d s, and the only reader of
+// X_{s-2} still to come -- sweep s - 1 on chunk k + 1 -- reads rows from edge[k+1] - d s + d - 6 on.  The sweep
 // of a row range is the pair form on a pointer-shifted geometry with ghost faces (k_step2_pair<true>,
 // rows beyond the range read as they stand, like a slab's deep ghost rows); the walls stay the wall
 // images of step2_local (k_mirror6 after every sweep that wrote rows 0..5 / ly-6..ly-1).  Results are
@@ -1375,22 +1375,51 @@ bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, con
            nsteps >= 2 && nsteps % 2 == 0 && h->g.ly >= 4 * step2_band_rows() && !h->prof_on;
 }
 
-// chunk edges (even rows): D2Q37_STREAM_ROWS rows per chunk (default 17 bands), a smaller first chunk
-// (D2Q37_STREAM_FIRST) so the first sweep starts early
+// Chunk edges (multiples of 4 rows).  The sweeps take longer than the copies, so only the first upload
+// and the last download are exposed: the chunk heights double from D2Q37_STREAM_FIRST (2 bands) while
+// they stay within half of D2Q37_STREAM_ROWS (37 bands: 4 CTAs per band on 148 SMs, the lockstep
+// plan's even split) -- the upload stays ahead of the sweeps as long as a chunk is little more than
+// twice the rows before it -- and halve again down to D2Q37_STREAM_LAST (1 band) at the top wall, whose
+// last chunk (plus the d rows per sweep the parallelograms lean back) is downloaded after the last
+// sweep.  Band counts of 2^n and 37 divide the 148 CTAs (almost) evenly.
 std::vector<int> stream_edges(int ly) {
+    const int band = step2_band_rows();
     auto env_rows = [](const char* name, int dflt) {
         const char* e = std::getenv(name);
-        int v = e ? std::atoi(e) : dflt;
-        v = std::max(2 * kHalo, v) & ~1;
-        return v;
+        const int v = e ? std::atoi(e) : dflt;
+        return std::max(2 * kHalo, v) & ~1;
     };
-    const int rows = env_rows("D2Q37_STREAM_ROWS", 17 * step2_band_rows());
-    const int first = std::min(rows, env_rows("D2Q37_STREAM_FIRST", 4 * step2_band_rows()));
+    const int rows = env_rows("D2Q37_STREAM_ROWS", 37 * band);
+    const int first = std::min(rows, env_rows("D2Q37_STREAM_FIRST", 2 * band));
+    const int last = std::min(rows, env_rows("D2Q37_STREAM_LAST", band));
+    std::vector<int> head, tail;
+    long long used = 0;
+    for (int h = first, t = last; used + h + t <= ly && (2 * h <= rows || 2 * t <= rows);) {
+        if (2 * h <= rows) head.push_back(h), used += h, h *= 2;
+        if (used + t <= ly && 2 * t <= rows) tail.push_back(t), used += t, t *= 2;
+        if (head.size() + tail.size() > 64) break;
+    }
     std::vector<int> edge{0};
-    for (int y = first; y < ly; y += rows) edge.push_back(y);
-    if (ly - edge.back() < 2 * kHalo && edge.size() > 1) edge.pop_back();  // no sliver at the top wall
-    edge.push_back(ly);
-    return edge;
+    for (int h : head) edge.push_back(edge.back() + h);
+    const int mid_end = ly - int(std::accumulate(tail.begin(), tail.end(), 0LL));
+    // the middle: whole `rows` chunks, the remainder spread as one shorter chunk in front of them
+    const int mid = mid_end - edge.back();
+    if (mid > 0) {
+        const int rem = mid % rows;
+        if (rem >= 2 * kHalo) edge.push_back(edge.back() + (rem & ~1));
+        while (mid_end - edge.back() > rows) edge.push_back(edge.back() + rows);
+        if (edge.back() < mid_end) edge.push_back(mid_end);
+    }
+    for (auto t = tail.rbegin(); t != tail.rend(); ++t) edge.push_back(edge.back() + *t);
+    edge.back() = ly;
+    // no sliver (< 6 rows) and no empty chunk anywhere
+    std::vector<int> out{0};
+    for (size_t i = 1; i < edge.size(); ++i) {
+        const int e = edge[i] == ly ? ly : edge[i] & ~3;  // inner edges on 32-byte sectors (even: 16-byte bulk copies)
+        if (e - out.back() >= 2 * kHalo && (ly - e >= 2 * kHalo || e == ly)) out.push_back(e);
+    }
+    if (out.back() != ly) out.back() == 0 ? out.push_back(ly) : void(out.back() = ly);
+    return out;
 }
 
 int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, int nsteps, const Faces& fc) {
@@ -1401,7 +1430,16 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     if (!h->copy_stream2) CK(cudaStreamCreateWithFlags(&h->copy_stream2, cudaStreamNonBlocking));
     const std::vector<int> edge = stream_edges(g.ly);
     const int K = int(edge.size()) - 1, S = nsteps / 2;
-    std::vector<cudaEvent_t> ev(2 * size_t(K) + 1, nullptr);
+    // optional second compute stream (D2Q37_STREAM_STREAMS=2): chunk k is swept on stream k & 1, so the
+    // ramp-up and tail of a sweep launch overlap a launch of the neighbouring chunk -- sweep s of chunk k
+    // needs only sweep s - 1 of chunks k and k - 1 (`done` events), which also orders every reuse of the
+    // two state buffers.  Measured: the sweeps gain 0.5 %, but each chunk's upload is needed a chunk
+    // earlier and the whole run loses 1 - 4 % (4096 x 16384), so one stream is the default.
+    const char* ns_env = std::getenv("D2Q37_STREAM_STREAMS");
+    const int nstreams = ns_env && std::atoi(ns_env) == 2 ? 2 : 1;
+    if (nstreams == 2) RET(ensure_side_stream(h));
+    cudaStream_t cs[2] = {h->stream, nstreams == 2 ? h->side_stream : h->stream};
+    std::vector<cudaEvent_t> ev(2 * size_t(K) + 1 + 2 * (size_t(S) + 1) + 1, nullptr);
     struct EventsGuard {
         std::vector<cudaEvent_t>& e;
         ~EventsGuard() {
@@ -1410,14 +1448,19 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
         }
     } guard{ev};
     for (cudaEvent_t& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* const done[2] = {ev.data() + 2 * size_t(K) + 1, ev.data() + 2 * size_t(K) + 1 + (S + 1)};
+    cudaEvent_t& joined = ev.back();
     cudaEvent_t* const uploaded = ev.data();
     cudaEvent_t* const swept = ev.data() + K;
     cudaEvent_t& start = ev[2 * size_t(K)];
     double* const X[2] = {h->buf[h->cur], h->buf[1 - h->cur]};  // X[s & 1]: the state after sweep s
     const size_t plane_vals = size_t(g.lx) * g.ly;
     const long long row0 = site_of(g, kHalo, 0);
+    // timing probes (results are then meaningless): 1 = no copies, 2 = no sweeps, 3 = no downloads, 4 = no uploads
+    const char* probe_env = std::getenv("D2Q37_STREAM_PROBE");
+    const int probe = probe_env ? std::atoi(probe_env) : 0;
     auto copy_rows = [&](bool up, double* dev, int r0, int r1, cudaStream_t st) -> int {
-        for (int p = 0; p < kNpop; ++p) {
+        for (int p = 0; p < kNpop && probe != 1 && probe != (up ? 4 : 3); ++p) {
             double* const d = dev + row0 + p * g.pstride + r0;
             if (up)
                 CK(cudaMemcpy2DAsync(d, size_t(g.cstride) * sizeof(double), in + p * plane_vals + r0,
@@ -1433,35 +1476,51 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     Faces gf = fc;
     gf.lo = gf.hi = kFaceGhost;
     const bool lock = step2_sched() != 0;
+    // rows a chunk's range moves down per sweep: at least the 6 a sweep reaches; 8 keeps the bands'
+    // 960-byte column stores on 32-byte sectors (D2Q37_STREAM_SKEW)
+    const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
+    const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
     // the copies start after whatever the lattice's stream still has queued
     CK(cudaEventRecord(start, h->stream));
     CK(cudaStreamWaitEvent(h->copy_stream, start, 0));
     CK(cudaStreamWaitEvent(h->copy_stream2, start, 0));
+    if (nstreams == 2) CK(cudaStreamWaitEvent(cs[1], start, 0));
     for (int k = 0; k < K; ++k) {
         RET(copy_rows(true, X[0], edge[k], edge[k + 1], h->copy_stream));
         CK(cudaEventRecord(uploaded[k], h->copy_stream));
     }
     for (int k = 0; k < K; ++k) {
         const bool last = k == K - 1;
-        CK(cudaStreamWaitEvent(h->stream, uploaded[k], 0));
-        if (k == 0) CK(launch_mirror6(X[0], g, fc, h->stream, 1));
-        if (last) CK(launch_mirror6(X[0], g, fc, h->stream, 2));
+        cudaStream_t st = cs[k & 1];
+        cudaEvent_t* const mine = done[k & 1];
+        cudaEvent_t* const below = done[(k - 1) & 1];
+        CK(cudaStreamWaitEvent(st, uploaded[k], 0));
+        if (k == 0) CK(launch_mirror6(X[0], g, fc, st, 1));
+        if (last) CK(launch_mirror6(X[0], g, fc, st, 2));
+        if (nstreams == 2) CK(cudaEventRecord(mine[0], st));
         int lo = 0, hi = 0;
         for (int s = 1; s <= S; ++s) {
-            lo = k == 0 ? 0 : std::max(0, edge[k] - 2 * kHalo * s);
-            hi = last ? g.ly : std::max(0, edge[k + 1] - 2 * kHalo * s);
-            if (hi <= lo) continue;
-            DevGeo gs = g;
-            gs.ly = hi - lo;
-            const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
-            CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, h->stream, 0, nb,
-                                 h->nsm, lock));
-            const int mask = (lo == 0 ? 1 : 0) | (hi == g.ly ? 2 : 0);
-            if (mask) CK(launch_mirror6(X[s & 1], g, fc, h->stream, mask));
+            lo = k == 0 ? 0 : std::max(0, edge[k] - skew * s);
+            hi = last ? g.ly : std::max(0, edge[k + 1] - skew * s);
+            if (nstreams == 2 && k > 0) CK(cudaStreamWaitEvent(st, below[s - 1], 0));
+            if (hi > lo && probe != 2) {
+                DevGeo gs = g;
+                gs.ly = hi - lo;
+                const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
+                CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, st, 0, nb,
+                                     h->nsm, lock));
+                const int mask = (lo == 0 ? 1 : 0) | (hi == g.ly ? 2 : 0);
+                if (mask) CK(launch_mirror6(X[s & 1], g, fc, st, mask));
+            }
+            if (nstreams == 2) CK(cudaEventRecord(mine[s], st));
         }
-        CK(cudaEventRecord(swept[k], h->stream));
+        CK(cudaEventRecord(swept[k], st));
         CK(cudaStreamWaitEvent(h->copy_stream2, swept[k], 0));
         if (hi > lo) RET(copy_rows(false, X[S & 1], lo, hi, h->copy_stream2));
+    }
+    if (nstreams == 2) {  // later work on the lattice's stream follows both
+        CK(cudaEventRecord(joined, cs[1]));
+        CK(cudaStreamWaitEvent(cs[0], joined, 0));
     }
     h->cur = S & 1 ? 1 - h->cur : h->cur;
     h->time_step += nsteps;

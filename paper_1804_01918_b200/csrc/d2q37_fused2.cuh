@@ -70,6 +70,10 @@ struct Lockstep {
     int rem;   // bands of the last round
     int cut;   // columns [0, cut) of a last-round band on its own CTA
     long long tail_per;  // items of [cut, lx) x rem bands per tail CTA
+    // even split (q > 0, only without whole rounds): each band on q CTAs, CTA i of a band marching
+    // columns [i w, (i + 1) w) -- every band's CTAs start on the same columns, so neighbouring bands
+    // stay in lockstep over the whole sweep (few bands on many CTAs: the streamed run's chunks)
+    int q, w;
 };
 struct LockSched {
     int band0, lx, G, c, k;
@@ -92,6 +96,14 @@ struct LockSched {
             return true;
         }
         const int base = band0 + ls.full * G;
+        if (ls.q > 0) {
+            if (k > ls.full || c >= ls.q * ls.rem) return false;
+            ++k;
+            band = base + c / ls.q;
+            xs = (c % ls.q) * ls.w;
+            xe = lx < xs + ls.w ? lx : xs + ls.w;
+            return xs < xe;
+        }
         if (c < ls.rem) {  // own last-round band, columns [0, cut)
             if (k > ls.full || ls.cut <= 0) return false;
             ++k;
@@ -115,6 +127,12 @@ inline Lockstep lockstep_plan(int nb, int G, int lx) {
     Lockstep ls{};
     ls.full = nb / G;
     ls.rem = nb % G;
+    // few bands on many CTAs: the even split when it idles at most 1 CTA in 32
+    if (ls.full == 0 && ls.rem > 0 && G >= 2 * ls.rem && (G % ls.rem) * 32 <= G && lx >= 8 * (G / ls.rem)) {
+        ls.q = G / ls.rem;
+        ls.w = (lx + ls.q - 1) / ls.q;
+        return ls;
+    }
     if (ls.rem > 0) {
         const long long T = G - ls.rem;  // tail CTAs
         // cut + 7 = rem (lx - cut) / T + 7 rem / T: a tail CTA's columns and segment starts

@@ -2,7 +2,7 @@
 //
 // Every (band, column) item of a sweep must be swept by exactly one persistent CTA, whatever the extents
 // and CTA counts: the lockstep schedule (LockSched over lockstep_plan: whole rounds, the last round's
-// own-band prefixes and the band-major tail), the band-major ranges (RangeSched), and the overlapped slab
+// own-band prefixes and the band-major tail, or the even split of few bands over many CTAs), the band-major ranges (RangeSched), and the overlapped slab
 // plan of the pair form (pair_slab_plan: ghost-face CTAs' face + adjacent bands, main CTAs in lockstep).
 // Also checks the balance the plans promise (no CTA more than one band-width plus the segment starts
 // above the mean) and that a face CTA's schedule starts with its face items.
@@ -100,7 +100,7 @@ static void check_slab(int lx, int ly, int flo, int fhi, int grid) {
 
 int main() {
     const int lxs[] = {3, 7, 64, 256, 1000, 4096};
-    const int nbs[] = {1, 2, 9, 35, 69, 135, 137, 147, 148, 149, 274, 300};
+    const int nbs[] = {1, 2, 4, 5, 8, 9, 16, 35, 37, 69, 74, 135, 137, 147, 148, 149, 274, 300};
     const int Gs[] = {1, 4, 100, 135, 144, 147, 148};
     int n = 0;
     for (int lx : lxs)

@@ -42,15 +42,19 @@ def _three_verbs(lbm, init, n, bc="wall", variant="fused2"):
     return out
 
 
-@pytest.mark.parametrize("rows,first,n", [(480, 240, 20), (240, 120, 100), (600, 600, 2), (2040, 480, 40)])
-def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, n):
-    """Several chunk heights, including chunks shorter than the 6-rows-per-sweep skew accumulates to
-    (240 rows against 50 sweeps x 6 rows) and a single sweep."""
-    lx, ly = 1024, 2400
+@pytest.mark.parametrize("streams", [2, 1])
+@pytest.mark.parametrize("rows,first,last,n", [(480, 240, 120, 20), (240, 120, 240, 100), (600, 600, 600, 2),
+                                               (2040, 480, 240, 40), (720, 120, 6, 12), (24, 8, 8, 8)])
+def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, last, n, streams):
+    """Several chunk heights, including chunks shorter than the rows-per-sweep skew accumulates to
+    (240 rows against 50 sweeps x 8 rows), chunks of a few rows and a single sweep; on one compute
+    stream and on two (neighbouring chunks' sweeps overlap)."""
+    lx, ly = (1024, 2400) if rows > 24 else (256, 600)
     init = lbm.make_lattice("rt", lx, ly, seed=777)
     want = _three_verbs(lbm, init, n)
     s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
-    with _Env(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=first):
+    with _Env(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=first, D2Q37_STREAM_LAST=last,
+              D2Q37_STREAM_STREAMS=streams):
         got = s.run(init, OMEGA, n)
     assert np.array_equal(got, want)
     assert s.time_step == n
@@ -60,13 +64,15 @@ def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, n):
     s.close()
 
 
-def test_streamed_run_in_place_and_repeated(gpu, lbm):
-    """out may be the input array; a second run on the same handle starts from the new input."""
+@pytest.mark.parametrize("skew", [6, 8, 14])
+def test_streamed_run_in_place_and_repeated(gpu, lbm, skew):
+    """out may be the input array; a second run on the same handle starts from the new input.  Any
+    rows-per-sweep skew >= 6 gives the same result."""
     lx, ly = 512, 1920
     init = lbm.make_lattice("rt", lx, ly, seed=5)
     s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
     buf = init.copy()
-    with _Env(D2Q37_STREAM_ROWS=360, D2Q37_STREAM_FIRST=120):
+    with _Env(D2Q37_STREAM_ROWS=360, D2Q37_STREAM_FIRST=120, D2Q37_STREAM_SKEW=skew):
         s.run(buf, OMEGA, 10, out=buf)
         assert np.array_equal(buf, _three_verbs(lbm, init, 10))
         s.run(buf, OMEGA, 6, out=buf)  # an odd sweep count: the state ends in the other buffer
@@ -76,8 +82,8 @@ def test_streamed_run_in_place_and_repeated(gpu, lbm):
 
 
 def test_streamed_run_default_chunks_larger_lattice(gpu, lbm):
-    """Default chunk heights (17 bands, first chunk 4 bands) on a lattice wide enough for the lockstep
-    schedule's full rounds."""
+    """Default chunk heights (2 bands doubling up to 37-band chunks, halving to 1 band at the top wall) on
+    a lattice wide enough for the lockstep plan's even split (4096 columns on 148 CTAs)."""
     lx, ly = 4096, 4800
     a = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
     a.init_rt_device(2018)
