@@ -9,6 +9,7 @@
 //   propagate(state)                        kernels.hpp:33   (prv -> nxt)
 //   collide(state, model, omega)            kernels.hpp:40   (nxt -> prv)
 //   step(state, model, omega)               kernels.hpp:45
+//   run(state, model, in, out, omega, n)    load + n x step + dump in one (streamed) call
 //   mlups / propagate_gbps / collide_gflops metrics.hpp:27-33
 // Every verb blocks until the device work is done (the reference is
 // synchronous); std::invalid_argument and NonPhysicalError are thrown where
@@ -316,6 +317,25 @@ inline void step(LatticeState& s, const VelocityModel& m, double omega, int nste
     s.set_model(m);
     check(d2q37_step(s.handle(), omega, nsteps, int(variant), int(bc)));
     s.sync();
+}
+
+/// load(in) + step x nsteps + dump as one call (d2q37_run_canonical): the result of LatticeState::load,
+/// nsteps x step (kernels.hpp:45) and LatticeState::dump (lattice.hpp:18-19), bit for bit.  On a single
+/// SoA wall domain with StepVariant::Fused2 and an even nsteps the upload, the sweeps and the download
+/// are pipelined in y-chunks, so the host copies hide under the sweeps.  `out` may be `in` itself.
+inline void run(LatticeState& s, const VelocityModel& m, const CanonicalLattice& in, CanonicalLattice& out,
+                double omega, int nsteps, StepVariant variant = StepVariant::Fused, Boundary bc = Boundary::Periodic) {
+    if (in.lx != s.geom().lx || in.ly != s.geom().ly || in.npop != kNpop)
+        throw std::invalid_argument("from_canonical: dimension mismatch");
+    if (&out != &in) {
+        out.lx = in.lx;
+        out.ly = in.ly;
+        out.npop = in.npop;
+        out.values.resize(in.values.size());
+    }
+    s.set_model(m);
+    check(d2q37_run_canonical(s.handle(), in.values.data(), out.values.data(), in.values.size(), omega, nsteps,
+                              int(variant), int(bc)));
 }
 
 // metrics.cpp:50-63

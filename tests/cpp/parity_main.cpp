@@ -27,6 +27,9 @@
 //   G11 VelocityModel per-site verbs (model.hpp:60-72): macros_of,
 //       equilibrium and collide_site <= 1e-14 vs the reference's on random
 //       sites; macros_of of a non-positive density throws NonPhysicalError
+//   G12 run(state, model, in, out, omega, n): the streamed load + step + dump
+//       (walls, Fused2, y-chunks) bit for bit == load, step, dump; the periodic
+//       call (three verbs inside) <= 1e-12 vs the reference load / lbm::step / dump
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -309,10 +312,38 @@ bool g11() {
     return true;
 }
 
+bool g12() {
+    const lbm::VelocityModel& m = lbm::VelocityModel::d2q37();
+    const lbm::CanonicalLattice init = lbm::make_random_lattice(64, 960, 1212);
+    const lbm_b200::CanonicalLattice in = to_gpu(init);
+    // walls (no reference counterpart: SURVEY A8): streamed in 120/240-row chunks vs the three verbs
+    setenv("D2Q37_STREAM_ROWS", "240", 1);
+    setenv("D2Q37_STREAM_FIRST", "120", 1);
+    lbm_b200::LatticeState a(B::SoA, lbm_b200::Geometry{64, 960}), b(B::SoA, lbm_b200::Geometry{64, 960});
+    lbm_b200::CanonicalLattice out;
+    lbm_b200::run(a, reference_model(), in, out, 0.9, 6, lbm_b200::StepVariant::Fused2, lbm_b200::Boundary::Wall);
+    unsetenv("D2Q37_STREAM_ROWS");
+    unsetenv("D2Q37_STREAM_FIRST");
+    b.load(in);
+    lbm_b200::step(b, reference_model(), 0.9, 6, lbm_b200::StepVariant::Fused2, lbm_b200::Boundary::Wall);
+    const auto want = b.dump().values;
+    if (out.values.size() != want.size() || std::memcmp(out.values.data(), want.data(), want.size() * sizeof(double)) != 0)
+        return false;
+    if (a.time_step() != 6 || a.dump().values != want) return false;
+    // periodic: against the reference's own load / step / dump
+    lbm::LatticeState ref{lbm::Descriptor(lbm::LayoutKind::SoA, lbm::Geometry{64, 960})};
+    ref.load(init);
+    lbm::ThreadPool pool(4);
+    for (int n = 0; n < 4; ++n) lbm::step(ref, m, 0.9, pool);
+    lbm_b200::CanonicalLattice io = in;
+    lbm_b200::run(a, reference_model(), io, io, 0.9, 4, lbm_b200::StepVariant::Fused2);  // in place
+    return max_rel(io.values, ref.dump().values) <= 1e-12;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    const std::array<std::pair<const char*, bool (*)()>, 11> all = {{{"G1", g1},
+    const std::array<std::pair<const char*, bool (*)()>, 12> all = {{{"G1", g1},
                                                                      {"G2", g2},
                                                                      {"G3", g3},
                                                                      {"G4", g4},
@@ -322,7 +353,8 @@ int main(int argc, char** argv) {
                                                                      {"G8", g8},
                                                                      {"G9", g9},
                                                                      {"G10", g10},
-                                                                     {"G11", g11}}};
+                                                                     {"G11", g11},
+                                                                     {"G12", g12}}};
     int failures = 0;
     for (const auto& [name, fn] : all) {
         if (argc > 1 && std::strcmp(argv[1], name) != 0) continue;

@@ -42,4 +42,4 @@ def test_cpp_parity_all_criteria(gpu):
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 11
+    assert r.stdout.count("PASS") == 12
