@@ -44,6 +44,11 @@ namespace d2q37 {
 namespace {
 
 constexpr int kPairThreads = 4 * kT2Band;  // 512
+// who refills a stage with column t + 2, and when: 0 the producers right after barrier 2 of iteration t,
+// 1 the producers after publishing column t (barrier 3), 2 the consumers once they hold column t
+#ifndef D2Q37_PAIR_ISSUE_MODE
+#define D2Q37_PAIR_ISSUE_MODE 1
+#endif
 static_assert(kFaceGhost == 3 && kFaceWall == 1, "pair_slab_plan's face kinds (d2q37_fused2.cuh)");
 constexpr int kTmemCols = 64;              // [role][parity][half] x 8 32-bit columns (4 doubles)
 
@@ -136,34 +141,38 @@ struct StageIssuer {
     unsigned issued;
     const double* isrc;
     __device__ __forceinline__ void set_band(int y0) { isrc = sb + ip * plane + ((y0 - kHalo - icy) & ~1); }
-    __device__ __forceinline__ void issue(int r) {
+    __device__ __forceinline__ void issue(int r, bool active = true) {
         const unsigned st = issued & 1u;
-        if (issuer) {
+        if (issuer && active) {
             int col = r < 0 ? r + lx : (r >= lx ? r - lx : r);
             col -= icx;
             col = col < 0 ? col + lx : (col >= lx ? col - lx : col);
             bulk_g2s(stage0 + (st * kNpop + ip) * kStageRows, isrc + (long long)col * cs, kStageRows * sizeof(double),
                      full + st);
         }
-        if (leader) mbar_arrive_expect_tx(full + st, kStageBytes);
+        if (leader && active) mbar_arrive_expect_tx(full + st, kStageBytes);
         ++issued;
     }
 };
 
 __device__ __forceinline__ StageIssuer make_issuer(const double* sb, const DevGeo& g, double* stage0,
-                                                   unsigned long long* full) {
+                                                   unsigned long long* full, int warp0 = 0) {
     StageIssuer is;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = (threadIdx.x >> 5) - warp0, lane = threadIdx.x & 31;
     is.sb = sb;
     is.stage0 = stage0;
     is.full = full;
     is.plane = g.pstride;
     is.cs = g.cstride;
     is.lx = g.lx;
-    // warps 0-3, lane l < 10 -> population 10 w + l
-    is.ip = warp * 10 + lane;
-    is.issuer = warp < 4 && lane < 10 && is.ip < kNpop;
-    is.leader = threadIdx.x == 0;
+#ifndef D2Q37_PAIR_ISSUE_WARPS
+#define D2Q37_PAIR_ISSUE_WARPS 4
+#endif
+    // warps 0 .. W-1, lane l < 40 / W -> population (40 / W) w + l
+    constexpr int kPer = 40 / D2Q37_PAIR_ISSUE_WARPS;
+    is.ip = warp * kPer + lane;
+    is.issuer = warp >= 0 && warp < D2Q37_PAIR_ISSUE_WARPS && lane < kPer && is.ip < kNpop;
+    is.leader = warp == 0 && lane == 0;
     if (!is.issuer) is.ip = 0;
     is.icx = is.issuer ? c_cx[is.ip] : 0;
     is.icy = is.issuer ? c_cy[is.ip] : 0;
@@ -208,7 +217,7 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
         const int y0 = band * kT2Out;
         const int niter = xe - xs + 7;
         is.set_band(y0);
-        for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k);
+        for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k);  // (every mode: by the producers)
         // step-1 row of this thread, clamped: rows beyond a wall are never read (step 2 mirrors into the
         // lattice), rows past ly + 2 never (their pulls would leave a slab's deep ghost rows)
         const bool wlo = wall_lo_band(walls, band), whi = wall_hi_band(walls, y0, ly);
@@ -255,21 +264,29 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
             // the consumers have read this iteration's slots -- and every producer has read the stage
             // (before its collide): refill it with column t + 2
             asm volatile("bar.sync 2, 512;" ::: "memory");
+#if D2Q37_PAIR_ISSUE_MODE == 0
             if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2);
+#endif
             for_pops([&](auto P) {
                 constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
                 if (pop_half(p) == H) ring[(rb + clk[dp]) * kT2Band + tid] = f[p];
             });
             clk.tick();
             asm volatile("bar.arrive 3, 512;" ::: "memory");
+#if D2Q37_PAIR_ISSUE_MODE == 1
+            if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2);
+#elif D2Q37_PAIR_ISSUE_MODE == 2
+            if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2, false);  // the consumers issue it; count it
+#endif
         }
         asm volatile("bar.sync 2, 512;" ::: "memory");  // the consumers' last iteration
     }
 }
 
 template <int H, class Sched>
-__device__ __forceinline__ void pair_consumer(double* __restrict__ db, const DevGeo& g, const ModelParams& mp,
-                                              double omega, Sched sched, int walls, const double* ring,
+__device__ __forceinline__ void pair_consumer(const double* __restrict__ sb, double* __restrict__ db, const DevGeo& g,
+                                              const ModelParams& mp, double omega, Sched sched, int walls,
+                                              const double* ring, double* stage0, unsigned long long* full,
                                               unsigned tbase, const SlabPack& pk, bool& bad) {
     const int tid = threadIdx.x & (kT2Band - 1);
     const int warp = threadIdx.x >> 5;
@@ -277,6 +294,11 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
     const long long plane = g.pstride, cs = g.cstride;
     const int cbar = 8 + (warp & 3);
     unsigned swaps = 0;  // TMEM column parity of the pair swaps, running across segments
+#if D2Q37_PAIR_ISSUE_MODE == 2
+    StageIssuer is = make_issuer(sb, g, stage0, full, 8);
+#else
+    (void)sb, (void)stage0, (void)full;
+#endif
     int band, xs, xe;
     bool was_face = sched_in_face(sched);
     while (sched.next(band, xs, xe)) {
@@ -313,6 +335,10 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
                                                                                     : nullptr;
         SlotClock clk;  // t % depth
         clk.reset();
+#if D2Q37_PAIR_ISSUE_MODE == 2
+        is.set_band(y0);
+        for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k, false);  // (the producers' prologue)
+#endif
 #pragma unroll 1
         for (int t = 0; t < niter; ++t) {
             if (t > 0) asm volatile("bar.sync 3, 512;" ::: "memory");  // step-1 column t - 1 is in the ring
@@ -335,6 +361,10 @@ __device__ __forceinline__ void pair_consumer(double* __restrict__ db, const Dev
                 consume_regs(v, [](int p) { return pop_half(p) == H; });
             }
             asm volatile("bar.arrive 2, 512;" ::: "memory");
+#if D2Q37_PAIR_ISSUE_MODE == 2
+            // every producer has passed barrier 2 of iteration t - 1, hence read its stage: refill it
+            if (t >= 1 && t + 1 < niter - 1) is.issue(xs - kHalo + t + 1);
+#endif
             if (t >= 7) {
                 const bool b = pair_collide<H>(v, mp, omega, tbase, 1, int(swaps++ & 1u), cbar);
                 if (active) {
@@ -408,9 +438,9 @@ __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, doubl
             pair_producer<1, GHOST>(sb, g, mp, omega, sched, walls, ring, stage0, full, tbase, bad);
     } else {
         if (!half)
-            pair_consumer<0>(db, g, mp, omega, sched, walls, ring, tbase, pk, bad);
+            pair_consumer<0>(sb, db, g, mp, omega, sched, walls, ring, stage0, full, tbase, pk, bad);
         else
-            pair_consumer<1>(db, g, mp, omega, sched, walls, ring, tbase, pk, bad);
+            pair_consumer<1>(sb, db, g, mp, omega, sched, walls, ring, stage0, full, tbase, pk, bad);
     }
     if (bad) atomicOr(flag, 1);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
