@@ -45,7 +45,9 @@ namespace {
 
 constexpr int kPairThreads = 4 * kT2Band;  // 512
 // who refills a stage with column t + 2, and when: 0 the producers right after barrier 2 of iteration t,
-// 1 the producers after publishing column t (barrier 3), 2 the consumers once they hold column t
+// 1 the producers after publishing column t (barrier 3), 2 the consumers once they hold column t,
+// 3 the half-0 consumers at the end of their iteration t, behind an "empty" mbarrier the producer warps
+// arrive on when their stage reads of iteration t have landed
 #ifndef D2Q37_PAIR_ISSUE_MODE
 #define D2Q37_PAIR_ISSUE_MODE 1
 #endif
@@ -141,14 +143,23 @@ struct StageIssuer {
     unsigned issued;
     const double* isrc;
     __device__ __forceinline__ void set_band(int y0) { isrc = sb + ip * plane + ((y0 - kHalo - icy) & ~1); }
-    __device__ __forceinline__ void issue(int r, bool active = true) {
+    __device__ __forceinline__ void issue(int r, bool active = true, unsigned long long* empty = nullptr) {
         const unsigned st = issued & 1u;
+        // mode 3: the use this copy overwrites (two copies back) has been read by every producer warp
+        if (empty && active && (issuer || leader)) mbar_wait(empty + st, ((issued - 2u) >> 1) & 1u);
         if (issuer && active) {
             int col = r < 0 ? r + lx : (r >= lx ? r - lx : r);
             col -= icx;
             col = col < 0 ? col + lx : (col >= lx ? col - lx : col);
             bulk_g2s(stage0 + (st * kNpop + ip) * kStageRows, isrc + (long long)col * cs, kStageRows * sizeof(double),
                      full + st);
+#ifdef D2Q37_PAIR_PREFETCH  // L2 prefetch of the column D2Q37_PAIR_PREFETCH further on
+            int pc = col + D2Q37_PAIR_PREFETCH;
+            pc = pc >= lx ? pc - lx : pc;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(isrc + (long long)pc * cs),
+                         "r"(unsigned(kStageRows * sizeof(double)))
+                         : "memory");
+#endif
         }
         if (leader && active) mbar_arrive_expect_tx(full + st, kStageBytes);
         ++issued;
@@ -260,10 +271,26 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
                 });
             }
             consume_regs(f, [](int p) { return pop_half(p) == H; });
+#if D2Q37_PAIR_ISSUE_MODE == 3
+            if ((threadIdx.x & 31) == 0) mbar_arrive(full + 2 + st);  // empty[st]: this warp's stage reads landed
+#endif
             bad |= pair_collide<H>(f, mp, omega, tbase, 0, int(used & 1u), pbar);  // parity: runs across segments
             // the consumers have read this iteration's slots -- and every producer has read the stage
             // (before its collide): refill it with column t + 2
+#ifdef D2Q37_PAIR_PRESYNC  // measured -2 %: the producers do not wait at this barrier
+            // The barrier number depends on every relaxed value (or'ed high words, masked by a run-time
+            // zero), so the relaxation is complete before the hand-off barrier: ptxas otherwise sinks its
+            // tail (~25 FP64 operations, a 10-deep dependent chain) below the barrier, between it and the
+            // ring stores the consumers wait for.
+            unsigned dep = 0;
+            for_pops([&](auto P) {
+                constexpr int p = decltype(P)::value;
+                if (pop_half(p) == H) dep |= unsigned(__double2hiint(f[p]));
+            });
+            asm volatile("bar.sync %0, 512;" ::"r"(2u + (dep & unsigned(g.band))) : "memory");  // g.band == 0 here
+#else
             asm volatile("bar.sync 2, 512;" ::: "memory");
+#endif
 #if D2Q37_PAIR_ISSUE_MODE == 0
             if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2);
 #endif
@@ -271,13 +298,13 @@ __device__ __forceinline__ void pair_producer(const double* __restrict__ sb, con
                 constexpr int p = decltype(P)::value, rb = t2n_base(p), dp = t2n_depth(p);
                 if (pop_half(p) == H) ring[(rb + clk[dp]) * kT2Band + tid] = f[p];
             });
-            clk.tick();
             asm volatile("bar.arrive 3, 512;" ::: "memory");
 #if D2Q37_PAIR_ISSUE_MODE == 1
             if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2);
-#elif D2Q37_PAIR_ISSUE_MODE == 2
+#elif D2Q37_PAIR_ISSUE_MODE >= 2
             if (t + 2 < niter - 1) is.issue(xs - kHalo + t + 2, false);  // the consumers issue it; count it
 #endif
+            clk.tick();
         }
         asm volatile("bar.sync 2, 512;" ::: "memory");  // the consumers' last iteration
     }
@@ -296,6 +323,8 @@ __device__ __forceinline__ void pair_consumer(const double* __restrict__ sb, dou
     unsigned swaps = 0;  // TMEM column parity of the pair swaps, running across segments
 #if D2Q37_PAIR_ISSUE_MODE == 2
     StageIssuer is = make_issuer(sb, g, stage0, full, 8);
+#elif D2Q37_PAIR_ISSUE_MODE == 3
+    StageIssuer is = make_issuer(sb, g, stage0, full, H == 0 ? 8 : 64);  // half 1: no issuing lane
 #else
     (void)sb, (void)stage0, (void)full;
 #endif
@@ -338,6 +367,11 @@ __device__ __forceinline__ void pair_consumer(const double* __restrict__ sb, dou
 #if D2Q37_PAIR_ISSUE_MODE == 2
         is.set_band(y0);
         for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k, false);  // (the producers' prologue)
+#elif D2Q37_PAIR_ISSUE_MODE == 3
+        if (H == 0) {
+            is.set_band(y0);
+            for (int k = 0; k < 2 && k < niter - 1; ++k) is.issue(xs - kHalo + k, false);
+        }
 #endif
 #pragma unroll 1
         for (int t = 0; t < niter; ++t) {
@@ -390,6 +424,10 @@ __device__ __forceinline__ void pair_consumer(const double* __restrict__ sb, dou
                 }
             }
             clk.tick();
+#if D2Q37_PAIR_ISSUE_MODE == 3
+            // the producers' iteration t runs beside this one and read its stage at its start: refill it
+            if (H == 0 && t + 2 < niter - 1) is.issue(xs - kHalo + t + 2, true, full + 2);
+#endif
         }
     }
     if (was_face) {  // the schedule ended inside the face bands
@@ -410,7 +448,7 @@ __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, doubl
     extern __shared__ double ring[];
     double* const stage0 = ring + kT2NRingCols * kT2Band;  // 2 stages [37][130]
     unsigned long long* const full = reinterpret_cast<unsigned long long*>(stage0 + 2 * kNpop * kStageRows);
-    unsigned* const tslot = reinterpret_cast<unsigned*>(full + 2);
+    unsigned* const tslot = reinterpret_cast<unsigned*>(full + 4);  // full[2], empty[2] (issue mode 3)
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tslot)),
@@ -421,6 +459,8 @@ __device__ __forceinline__ void pair_sweep(const double* __restrict__ src, doubl
     if (threadIdx.x == 0) {
         mbar_init(full, 1);
         mbar_init(full + 1, 1);
+        mbar_init(full + 2, 8);  // one arrival per producer warp
+        mbar_init(full + 3, 8);
         asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -488,7 +528,7 @@ __global__ void __launch_bounds__(kPairThreads, 1)
 }
 
 size_t pair_smem_bytes() {
-    return (size_t)kT2NRingCols * kT2Band * sizeof(double) + 2 * size_t(kStageBytes) + 16 + 16;  // + mbarriers, TMEM slot
+    return (size_t)kT2NRingCols * kT2Band * sizeof(double) + 2 * size_t(kStageBytes) + 32 + 16;  // + mbarriers, TMEM slot
 }
 
 }  // namespace
