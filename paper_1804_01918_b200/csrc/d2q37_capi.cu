@@ -1509,7 +1509,10 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
                 const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
                 CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, st, 0, nb,
                                      h->nsm, lock));
-                const int mask = (lo == 0 ? 1 : 0) | (hi == g.ly ? 2 : 0);
+                // wall images once the six rows they mirror are complete: the launch that wrote row 5 (a
+                // range clipped at row 0 may end below it; the chunk above then finishes the rows) / the
+                // last chunk's (it always reaches from below ly - 6 to ly)
+                const int mask = (lo < 2 * kHalo && hi >= 2 * kHalo ? 1 : 0) | (hi == g.ly ? 2 : 0);
                 if (mask) CK(launch_mirror6(X[s & 1], g, fc, st, mask));
             }
             if (nstreams == 2) CK(cudaEventRecord(mine[s], st));

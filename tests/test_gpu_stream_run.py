@@ -81,6 +81,20 @@ def test_streamed_run_in_place_and_repeated(gpu, lbm, skew):
     s.close()
 
 
+@pytest.mark.parametrize("lx,ly,n", [(64, 1201, 10), (8, 700, 6), (3, 486, 4), (1000, 481, 2), (200, 1000, 30)])
+def test_streamed_run_odd_extents(gpu, lbm, lx, ly, n):
+    """Odd and non-band-multiple heights (the last chunk ends at ly whatever its parity), very narrow
+    lattices, default chunk heights."""
+    init = lbm.make_lattice("rt", lx, ly, seed=lx + ly)
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+    got = s.run(init, OMEGA, n)
+    assert np.array_equal(got, _three_verbs(lbm, init, n))
+    with _Env(D2Q37_STREAM_ROWS=124, D2Q37_STREAM_FIRST=36, D2Q37_STREAM_LAST=12):
+        got = s.run(init, OMEGA, n)
+    assert np.array_equal(got, _three_verbs(lbm, init, n))
+    s.close()
+
+
 def test_streamed_run_default_chunks_larger_lattice(gpu, lbm):
     """Default chunk heights (2 bands doubling up to 37-band chunks, halving to 1 band at the top wall) on
     a lattice wide enough for the lockstep plan's even split (4096 columns on 148 CTAs)."""
