@@ -136,14 +136,17 @@ int d2q37_load_canonical(d2q37_lattice* h, const double* host, size_t n);
 int d2q37_dump_canonical(d2q37_lattice* h, double* host, size_t n);
 /* load(host_in) -> step x nsteps -> dump(host_out) as one call (lattice.hpp:18-19 + kernels.hpp:45): the
  * same result as d2q37_load_canonical + d2q37_step + d2q37_sync + d2q37_dump_canonical, bit for bit.
- * On a single-GPU SoA domain with wall bc, FUSED2, FAST math and an even nsteps the three phases are
- * pipelined in y-chunks: rows are uploaded, swept (each chunk as a parallelogram of sweeps, 6 rows
+ * On a single-GPU SoA domain (wall or periodic bc), FUSED2, FAST math and an even nsteps the three phases
+ * are pipelined in y-chunks: rows are uploaded, swept (each chunk as a parallelogram of sweeps, 8 rows
  * lower per sweep) and downloaded concurrently, so the PCIe copies hide under the sweeps (pinned
  * host arrays; pageable ones work but serialise).  host_out may be host_in.  Every other case runs
  * the three verbs one after another.  D2Q37_STREAM_RUN=0 forces that, D2Q37_STREAM_ROWS /
- * D2Q37_STREAM_FIRST set the chunk heights. */
+ * D2Q37_STREAM_FIRST / D2Q37_STREAM_LAST set the chunk heights, D2Q37_STREAM_SKEW the rows per sweep. */
 int d2q37_run_canonical(d2q37_lattice* h, const double* host_in, double* host_out, size_t n, double omega,
                         int nsteps, int variant, int bc);
+/* How the last d2q37_run_canonical on h ran: 0 the three verbs one after another, 1 pipelined between
+ * walls, 2 pipelined on a y-periodic domain (-1: null handle). */
+int d2q37_last_run_mode(const d2q37_lattice* h);
 /* from_canonical / to_canonical on one buffer: which = 0 prv, 1 nxt (dump.hpp:28-29). */
 int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n);
 int d2q37_dump_buffer(d2q37_lattice* h, int which, double* host, size_t n);

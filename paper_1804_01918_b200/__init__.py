@@ -107,6 +107,7 @@ def _load():
         "d2q37_load_canonical": (i, [vp, vp, sz]),
         "d2q37_dump_canonical": (i, [vp, vp, sz]),
         "d2q37_run_canonical": (i, [vp, vp, vp, sz, d, i, i, i]),
+        "d2q37_last_run_mode": (i, [vp]),
         "d2q37_load_buffer": (i, [vp, i, vp, sz]),
         "d2q37_dump_buffer": (i, [vp, i, vp, sz]),
         "d2q37_load_buffer_device": (i, [vp, i, vp, sz]),
@@ -568,6 +569,11 @@ class Simulation:
         _check(_load().d2q37_run_canonical(self._h, _ptr(a), _ptr(out), a.size, float(omega), int(n),
                                            VARIANTS[variant or self.variant], BCS[bc or self.bc_mode]))
         return out
+
+    @property
+    def last_run_mode(self) -> str:
+        """How the last run() ran: "three_verbs", "pipelined_walls" or "pipelined_periodic"."""
+        return ("three_verbs", "pipelined_walls", "pipelined_periodic")[_load().d2q37_last_run_mode(self._h)]
 
     def load_device(self, ptr: int, n: int, which: int = 0):
         _check(_load().d2q37_load_buffer_device(self._h, which, C.c_void_p(ptr), n))

@@ -62,6 +62,7 @@ struct d2q37_lattice {
     double* stage2 = nullptr;
     cudaStream_t copy_stream = nullptr;
     cudaStream_t copy_stream2 = nullptr;  // streamed run (d2q37_run_canonical): downloads beside the uploads
+    int last_run_mode = 0;  // last d2q37_run_canonical: 0 three verbs, 1 pipelined (walls), 2 pipelined (y-periodic)
     cudaEvent_t ev_io[4] = {};
     long time_step = 0;
 
@@ -1368,11 +1369,22 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
 // rows beyond the range read as they stand, like a slab's deep ghost rows); the walls stay the wall
 // images of step2_local (k_mirror6 after every sweep that wrote rows 0..5 / ly-6..ly-1).  Results are
 // bit-identical to load + step + dump (same kernel, same values).
+int seam_rows(int S, int skew);
+
 bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, const Faces& fc) {
-    return h->layout == D2Q37_SOA && !h->g.band && h->g.deep && !h->g.tr && h->g.vl == 1 && local_only(h) &&
-           h->math == D2Q37_MATH_FAST && variant == D2Q37_FUSED2 && bc == D2Q37_BC_WALL && fc.lo == kFaceWall &&
-           fc.hi == kFaceWall && step2_form() == kStep2Pair && step2_ghost_walls() && step2_supported(h->g, fc) &&
-           nsteps >= 2 && nsteps % 2 == 0 && h->g.ly >= 4 * step2_band_rows() && !h->prof_on;
+    const bool walls = bc == D2Q37_BC_WALL && fc.lo == kFaceWall && fc.hi == kFaceWall && step2_ghost_walls();
+    const bool per = bc == D2Q37_BC_PERIODIC && fc.lo == kFacePeriodic && fc.hi == kFacePeriodic;
+    if (!(h->layout == D2Q37_SOA && !h->g.band && h->g.deep && !h->g.tr && h->g.vl == 1 && local_only(h) &&
+          h->math == D2Q37_MATH_FAST && variant == D2Q37_FUSED2 && (walls || per) && step2_form() == kStep2Pair &&
+          step2_supported(h->g, fc) && nsteps >= 2 && nsteps % 2 == 0 && h->g.ly >= 4 * step2_band_rows() &&
+          !h->prof_on))
+        return false;
+    if (per) {  // the two seam pieces (8 rows per sweep each, whatever D2Q37_STREAM_SKEW says below 8) and a wave
+        const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
+        const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
+        return h->g.ly >= 2 * seam_rows(nsteps / 2, skew) + 4 * step2_band_rows();
+    }
+    return true;
 }
 
 // Chunk edges (multiples of 4 rows).  The sweeps take longer than the copies, so only the first upload
@@ -1422,24 +1434,32 @@ std::vector<int> stream_edges(int ly) {
     return out;
 }
 
+// Rows the seam pieces of a y-periodic streamed run need beyond the d rows per sweep they lose
+// (the seam's wrap images mirror 6 rows on each side; two bands of margin keep the launches useful)
+int seam_rows(int S, int skew) { return skew * S + 2 * step2_band_rows(); }
+
 int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, int nsteps, const Faces& fc) {
     DeviceGuard dg(h->device);
     const DevGeo& g = h->g;
     if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
     if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
     if (!h->copy_stream2) CK(cudaStreamCreateWithFlags(&h->copy_stream2, cudaStreamNonBlocking));
-    const std::vector<int> edge = stream_edges(g.ly);
-    const int K = int(edge.size()) - 1, S = nsteps / 2;
-    // optional second compute stream (D2Q37_STREAM_STREAMS=2): chunk k is swept on stream k & 1, so the
-    // ramp-up and tail of a sweep launch overlap a launch of the neighbouring chunk -- sweep s of chunk k
-    // needs only sweep s - 1 of chunks k and k - 1 (`done` events), which also orders every reuse of the
-    // two state buffers.  Measured: the sweeps gain 0.5 %, but each chunk's upload is needed a chunk
-    // earlier and the whole run loses 1 - 4 % (4096 x 16384), so one stream is the default.
-    const char* ns_env = std::getenv("D2Q37_STREAM_STREAMS");
-    const int nstreams = ns_env && std::atoi(ns_env) == 2 ? 2 : 1;
-    if (nstreams == 2) RET(ensure_side_stream(h));
-    cudaStream_t cs[2] = {h->stream, nstreams == 2 ? h->side_stream : h->stream};
-    std::vector<cudaEvent_t> ev(2 * size_t(K) + 1 + 2 * (size_t(S) + 1) + 1, nullptr);
+    const int S = nsteps / 2, ly = g.ly;
+    const bool per = fc.lo == kFacePeriodic;
+    // rows a chunk's range moves down per sweep: at least the 6 a sweep reaches; 8 keeps the bands'
+    // 960-byte column stores on 32-byte sectors (D2Q37_STREAM_SKEW)
+    const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
+    const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
+    // y-periodic: the two pieces at the seam, BOT = [0, base) and TOP = [top0, ly), are uploaded first and
+    // swept together -- sweep s on [0, base - d s) and [top0 + d s, ly), then the periodic images of the
+    // new state's rows 0..5 / ly-6..ly-1 (k_wrap6) -- losing d rows per sweep on their far sides; the wave
+    // of chunks then runs over [base, top0) as between walls, its last chunk growing into the rows TOP
+    // lost: sweep s up to top0 + d s.  Walls: base = 0, top0 = ly, no seam pieces.
+    const int base = per ? seam_rows(S, skew) & ~3 : 0, top0 = per ? (ly - seam_rows(S, skew)) & ~3 : ly;
+    std::vector<int> edge = stream_edges(top0 - base);
+    for (int& e : edge) e += base;
+    const int K = int(edge.size()) - 1;
+    std::vector<cudaEvent_t> ev(2 * size_t(K) + 3, nullptr);
     struct EventsGuard {
         std::vector<cudaEvent_t>& e;
         ~EventsGuard() {
@@ -1448,11 +1468,11 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
         }
     } guard{ev};
     for (cudaEvent_t& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cudaEvent_t* const done[2] = {ev.data() + 2 * size_t(K) + 1, ev.data() + 2 * size_t(K) + 1 + (S + 1)};
-    cudaEvent_t& joined = ev.back();
     cudaEvent_t* const uploaded = ev.data();
     cudaEvent_t* const swept = ev.data() + K;
     cudaEvent_t& start = ev[2 * size_t(K)];
+    cudaEvent_t& seam_up = ev[2 * size_t(K) + 1];
+    cudaEvent_t& seam_swept = ev[2 * size_t(K) + 2];
     double* const X[2] = {h->buf[h->cur], h->buf[1 - h->cur]};  // X[s & 1]: the state after sweep s
     const size_t plane_vals = size_t(g.lx) * g.ly;
     const long long row0 = site_of(g, kHalo, 0);
@@ -1460,7 +1480,7 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     const char* probe_env = std::getenv("D2Q37_STREAM_PROBE");
     const int probe = probe_env ? std::atoi(probe_env) : 0;
     auto copy_rows = [&](bool up, double* dev, int r0, int r1, cudaStream_t st) -> int {
-        for (int p = 0; p < kNpop && probe != 1 && probe != (up ? 4 : 3); ++p) {
+        for (int p = 0; p < kNpop && r1 > r0 && probe != 1 && probe != (up ? 4 : 3); ++p) {
             double* const d = dev + row0 + p * g.pstride + r0;
             if (up)
                 CK(cudaMemcpy2DAsync(d, size_t(g.cstride) * sizeof(double), in + p * plane_vals + r0,
@@ -1476,59 +1496,68 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     Faces gf = fc;
     gf.lo = gf.hi = kFaceGhost;
     const bool lock = step2_sched() != 0;
-    // rows a chunk's range moves down per sweep: at least the 6 a sweep reaches; 8 keeps the bands'
-    // 960-byte column stores on 32-byte sectors (D2Q37_STREAM_SKEW)
-    const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
-    const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
+    cudaStream_t st = h->stream;
+    // rows [lo, hi) of sweep s: the pair form on the pointer-shifted range, ghost faces
+    auto sweep = [&](int s, int lo, int hi) -> int {
+        if (hi <= lo || probe == 2) return D2Q37_OK;
+        DevGeo gs = g;
+        gs.ly = hi - lo;
+        const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
+        CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, st, 0, nb, h->nsm, lock));
+        return D2Q37_OK;
+    };
     // the copies start after whatever the lattice's stream still has queued
-    CK(cudaEventRecord(start, h->stream));
+    CK(cudaEventRecord(start, st));
     CK(cudaStreamWaitEvent(h->copy_stream, start, 0));
     CK(cudaStreamWaitEvent(h->copy_stream2, start, 0));
-    if (nstreams == 2) CK(cudaStreamWaitEvent(cs[1], start, 0));
+    if (per) {
+        RET(copy_rows(true, X[0], top0, ly, h->copy_stream));
+        RET(copy_rows(true, X[0], 0, base, h->copy_stream));
+        CK(cudaEventRecord(seam_up, h->copy_stream));
+    }
     for (int k = 0; k < K; ++k) {
         RET(copy_rows(true, X[0], edge[k], edge[k + 1], h->copy_stream));
         CK(cudaEventRecord(uploaded[k], h->copy_stream));
     }
+    if (per) {
+        CK(cudaStreamWaitEvent(st, seam_up, 0));
+        CK(launch_wrap6(X[0], g, st));
+        for (int s = 1; s <= S; ++s) {
+            RET(sweep(s, top0 + skew * s, ly));
+            RET(sweep(s, 0, base - skew * s));
+            CK(launch_wrap6(X[s & 1], g, st));
+        }
+        CK(cudaEventRecord(seam_swept, st));
+        CK(cudaStreamWaitEvent(h->copy_stream2, seam_swept, 0));
+        RET(copy_rows(false, X[S & 1], top0 + skew * S, ly, h->copy_stream2));
+        RET(copy_rows(false, X[S & 1], 0, base - skew * S, h->copy_stream2));
+    }
     for (int k = 0; k < K; ++k) {
         const bool last = k == K - 1;
-        cudaStream_t st = cs[k & 1];
-        cudaEvent_t* const mine = done[k & 1];
-        cudaEvent_t* const below = done[(k - 1) & 1];
         CK(cudaStreamWaitEvent(st, uploaded[k], 0));
-        if (k == 0) CK(launch_mirror6(X[0], g, fc, st, 1));
-        if (last) CK(launch_mirror6(X[0], g, fc, st, 2));
-        if (nstreams == 2) CK(cudaEventRecord(mine[0], st));
+        if (!per && k == 0) CK(launch_mirror6(X[0], g, fc, st, 1));
+        if (!per && last) CK(launch_mirror6(X[0], g, fc, st, 2));
         int lo = 0, hi = 0;
         for (int s = 1; s <= S; ++s) {
-            lo = k == 0 ? 0 : std::max(0, edge[k] - skew * s);
-            hi = last ? g.ly : std::max(0, edge[k + 1] - skew * s);
-            if (nstreams == 2 && k > 0) CK(cudaStreamWaitEvent(st, below[s - 1], 0));
-            if (hi > lo && probe != 2) {
-                DevGeo gs = g;
-                gs.ly = hi - lo;
-                const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
-                CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, st, 0, nb,
-                                     h->nsm, lock));
+            lo = !per && k == 0 ? 0 : std::max(0, edge[k] - skew * s);
+            hi = last ? (per ? top0 + skew * s : ly) : std::max(0, edge[k + 1] - skew * s);
+            RET(sweep(s, lo, hi));
+            if (!per && hi > lo && probe != 2) {
                 // wall images once the six rows they mirror are complete: the launch that wrote row 5 (a
                 // range clipped at row 0 may end below it; the chunk above then finishes the rows) / the
                 // last chunk's (it always reaches from below ly - 6 to ly)
-                const int mask = (lo < 2 * kHalo && hi >= 2 * kHalo ? 1 : 0) | (hi == g.ly ? 2 : 0);
+                const int mask = (lo < 2 * kHalo && hi >= 2 * kHalo ? 1 : 0) | (hi == ly ? 2 : 0);
                 if (mask) CK(launch_mirror6(X[s & 1], g, fc, st, mask));
             }
-            if (nstreams == 2) CK(cudaEventRecord(mine[s], st));
         }
         CK(cudaEventRecord(swept[k], st));
         CK(cudaStreamWaitEvent(h->copy_stream2, swept[k], 0));
-        if (hi > lo) RET(copy_rows(false, X[S & 1], lo, hi, h->copy_stream2));
-    }
-    if (nstreams == 2) {  // later work on the lattice's stream follows both
-        CK(cudaEventRecord(joined, cs[1]));
-        CK(cudaStreamWaitEvent(cs[0], joined, 0));
+        RET(copy_rows(false, X[S & 1], lo, hi, h->copy_stream2));
     }
     h->cur = S & 1 ? 1 - h->cur : h->cur;
     h->time_step += nsteps;
     h->h6_valid = true;
-    h->h6_kind = 1;
+    h->h6_kind = per ? 0 : 1;
     CK(cudaStreamSynchronize(h->copy_stream2));
     CK(cudaStreamSynchronize(h->copy_stream));
     return D2Q37_OK;
@@ -1663,14 +1692,18 @@ int d2q37_run_canonical(d2q37_lattice* h, const double* host_in, double* host_ou
     const char* off = std::getenv("D2Q37_STREAM_RUN");
     if (!(off && std::atoi(off) == 0) && can_stream_run(h, nsteps, variant, bc, fc)) {
         h->p2p_dirty = true, h->h6_valid = false, h->bc_filled = -1;
+        h->last_run_mode = fc.lo == kFacePeriodic ? 2 : 1;
         RET(run_streamed(h, host_in, host_out, omega, nsteps, fc));
         return d2q37_sync(h);
     }
+    h->last_run_mode = 0;
     RET(load_canonical_impl(h, 0, host_in, n, false));
     RET(d2q37_step(h, omega, nsteps, variant, bc));
     RET(d2q37_sync(h));
     return dump_canonical_impl(h, 0, host_out, n, false);
 }
+int d2q37_last_run_mode(const d2q37_lattice* h) { return h ? h->last_run_mode : -1; }
+
 int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n) {
     return load_canonical_impl(h, which, host, n, false);
 }

@@ -42,22 +42,19 @@ def _three_verbs(lbm, init, n, bc="wall", variant="fused2"):
     return out
 
 
-@pytest.mark.parametrize("streams", [2, 1])
 @pytest.mark.parametrize("rows,first,last,n", [(480, 240, 120, 20), (240, 120, 240, 100), (600, 600, 600, 2),
                                                (2040, 480, 240, 40), (720, 120, 6, 12), (24, 8, 8, 8)])
-def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, last, n, streams):
+def test_streamed_run_bitwise_equals_load_step_dump(gpu, lbm, rows, first, last, n):
     """Several chunk heights, including chunks shorter than the rows-per-sweep skew accumulates to
-    (240 rows against 50 sweeps x 8 rows), chunks of a few rows and a single sweep; on one compute
-    stream and on two (neighbouring chunks' sweeps overlap)."""
+    (240 rows against 50 sweeps x 8 rows), chunks of a few rows and a single sweep."""
     lx, ly = (1024, 2400) if rows > 24 else (256, 600)
     init = lbm.make_lattice("rt", lx, ly, seed=777)
     want = _three_verbs(lbm, init, n)
     s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
-    with _Env(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=first, D2Q37_STREAM_LAST=last,
-              D2Q37_STREAM_STREAMS=streams):
+    with _Env(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=first, D2Q37_STREAM_LAST=last):
         got = s.run(init, OMEGA, n)
     assert np.array_equal(got, want)
-    assert s.time_step == n
+    assert s.time_step == n and s.last_run_mode == "pipelined_walls"
     # the lattice is left in the state the three verbs leave it in: stepping on agrees too
     s.step(OMEGA, 3)
     assert np.array_equal(s.dump(), _three_verbs(lbm, init, n + 3))
@@ -109,6 +106,40 @@ def test_streamed_run_default_chunks_larger_lattice(gpu, lbm):
     a.close()
 
 
+@pytest.mark.parametrize("lx,ly,n,rows", [(512, 2400, 20, 0), (512, 2400, 100, 240), (64, 1203, 6, 36),
+                                          (4096, 2560, 8, 0), (256, 1124, 2, 0)])
+def test_streamed_run_periodic_bitwise(gpu, lbm, lx, ly, n, rows):
+    """y-periodic domains (the reference's own boundary mode, kernels.cpp:197-234): the two pieces at the
+    seam are swept first, with the periodic images between their sweeps, then the wave of chunks."""
+    init = lbm.make_lattice("rt", lx, ly, seed=ly)
+    want = _three_verbs(lbm, init, n, bc="periodic")
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="periodic", variant="fused2")
+    env = dict(D2Q37_STREAM_ROWS=rows, D2Q37_STREAM_FIRST=max(12, rows // 4), D2Q37_STREAM_LAST=12) if rows else {}
+    buf = init.copy()
+    with _Env(**env):
+        s.run(buf, OMEGA, n, out=buf)
+    assert np.array_equal(buf, want) and s.last_run_mode == "pipelined_periodic"
+    s.step(OMEGA, 2)  # the periodic images left in the ghost rows are the final state's
+    assert np.array_equal(s.dump(), _three_verbs(lbm, init, n + 2, bc="periodic"))
+    s.close()
+
+
+def test_streamed_run_periodic_vs_unmodified_reference(gpu, lbm, po):
+    """load -> 4 x lbm::step -> dump of the unmodified reference (lattice.hpp:18-19, kernels.cpp:276-283)
+    against one streamed run: populations within 1e-12."""
+    lx, ly, n = 96, 1200, 4
+    init = lbm.make_lattice("random", lx, ly, seed=31)
+    ref = po.RefSim(po.AOS, lx, ly, 1, workers=os.cpu_count() or 1)
+    ref.load(init)
+    ref.step(OMEGA, n)
+    s = lbm.Simulation("soa", lx, ly, device=0, bc="periodic", variant="fused2")
+    got = s.run(init, OMEGA, n)
+    want = ref.dump()
+    assert s.last_run_mode == "pipelined_periodic"
+    assert float(np.max(np.abs(got - want) / np.abs(want))) <= 1e-12
+    s.close()
+
+
 @pytest.mark.parametrize("bc,variant,n", [("periodic", "fused2", 6), ("wall", "fused2", 5), ("wall", "fused", 4),
                                           ("wall", "unfused", 2)])
 def test_run_falls_back_to_three_verbs(gpu, lbm, bc, variant, n):
@@ -116,7 +147,7 @@ def test_run_falls_back_to_three_verbs(gpu, lbm, bc, variant, n):
     init = lbm.make_lattice("rt", lx, ly, seed=11)
     s = lbm.Simulation("soa", lx, ly, device=0, bc=bc, variant=variant)
     got = s.run(init, OMEGA, n)
-    assert np.array_equal(got, _three_verbs(lbm, init, n, bc, variant))
+    assert np.array_equal(got, _three_verbs(lbm, init, n, bc, variant)) and s.last_run_mode == "three_verbs"
     s.close()
 
 

@@ -15,7 +15,8 @@ ly = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 combos = [tuple(int(v) for v in a.split(":")) for a in sys.argv[3:]] or [(4080, 480, 240)]
 lx = 4096
-s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
+bc = os.environ.get("BC", "wall")  # wall | periodic
+s = lbm.Simulation("soa", lx, ly, device=0, bc=bc, variant="fused2")
 s.init_rt_device(2018)
 canon = np.empty((37, lx, ly))
 assert int(torch.cuda.cudart().cudaHostRegister(canon.ctypes.data, canon.nbytes, 0)) == 0
@@ -46,13 +47,8 @@ for rows, first, last in combos:
     os.environ["D2Q37_STREAM_FIRST"] = str(first)
     os.environ["D2Q37_STREAM_LAST"] = str(last)
     t = timed(lambda: s.run(canon, 0.8, n, out=canon))
-    print(f"streamed rows {rows} first {first} last {last}: {t:.4f} s  {lx * ly * n / t / 1e6:.0f} MLUPS", flush=True)
-os.environ["D2Q37_STREAM_PROBE"] = "1"
-for skew in (6, 8, 12, 16):
-    os.environ["D2Q37_STREAM_SKEW"] = str(skew)
-    t = timed(lambda: s.run(canon, 0.8, n, out=canon))
-    print(f"sweeps only, skew {skew}: {t:.4f} s", flush=True)
-os.environ.pop("D2Q37_STREAM_SKEW")
+    print(f"streamed ({s.last_run_mode}) rows {rows} first {first} last {last}: {t:.4f} s  "
+          f"{lx * ly * n / t / 1e6:.0f} MLUPS", flush=True)
 for probe, what in ((1, "sweeps only (no copies)"), (2, "copies only (no sweeps)")):
     os.environ["D2Q37_STREAM_PROBE"] = str(probe)
     t = timed(lambda: s.run(canon, 0.8, n, out=canon))
