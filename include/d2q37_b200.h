@@ -147,6 +147,14 @@ int d2q37_run_canonical(d2q37_lattice* h, const double* host_in, double* host_ou
 /* How the last d2q37_run_canonical on h ran: 0 the three verbs one after another, 1 pipelined between
  * walls, 2 pipelined on a y-periodic domain (-1: null handle). */
 int d2q37_last_run_mode(const d2q37_lattice* h);
+/* Test hook (no GPU needed): the operations a pipelined d2q37_run_canonical of an ly-row domain would
+ * queue, 4 ints each {kind, a, b, c}: kind 0 upload rows [a, b) (upload index c), 1 the compute stream
+ * waits for upload c, 2 sweep c (two steps) of rows [a, b), 3 wall images of the state after sweep c
+ * (a: bit 0 low face, bit 1 high face), 4 periodic images of the state after sweep c, 5 download rows
+ * [a, b) of the final state once everything before it has run.  Uploads come first (their own stream, in
+ * order).  Returns the number of operations (0: the call would run the three verbs; < 0: minus an error
+ * code), fills up to cap. */
+int d2q37_debug_stream_plan(int ly, int nsteps, int bc, int* ops, int cap);
 /* from_canonical / to_canonical on one buffer: which = 0 prv, 1 nxt (dump.hpp:28-29). */
 int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n);
 int d2q37_dump_buffer(d2q37_lattice* h, int which, double* host, size_t n);

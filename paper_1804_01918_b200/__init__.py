@@ -108,6 +108,7 @@ def _load():
         "d2q37_dump_canonical": (i, [vp, vp, sz]),
         "d2q37_run_canonical": (i, [vp, vp, vp, sz, d, i, i, i]),
         "d2q37_last_run_mode": (i, [vp]),
+        "d2q37_debug_stream_plan": (i, [i, i, i, P(C.c_int), i]),
         "d2q37_load_buffer": (i, [vp, i, vp, sz]),
         "d2q37_dump_buffer": (i, [vp, i, vp, sz]),
         "d2q37_load_buffer_device": (i, [vp, i, vp, sz]),
@@ -157,6 +158,19 @@ def _load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def stream_plan(ly: int, nsteps: int, bc: str = "wall") -> np.ndarray:
+    """Test hook (d2q37_debug_stream_plan, no GPU needed): the operations of a pipelined run() as an
+    (n, 4) int array of {kind, a, b, c}; empty when the call would run the three verbs."""
+    lib = _load()
+    n = lib.d2q37_debug_stream_plan(int(ly), int(nsteps), BCS[bc], None, 0)
+    if n < 0:
+        _check(-n)
+    out = np.zeros((max(n, 0), 4), dtype=np.int32)
+    if n > 0:
+        lib.d2q37_debug_stream_plan(int(ly), int(nsteps), BCS[bc], out.ctypes.data_as(C.POINTER(C.c_int)), n)
+    return out
 
 
 def _check(rc: int) -> None:

@@ -1370,6 +1370,7 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
 // images of step2_local (k_mirror6 after every sweep that wrote rows 0..5 / ly-6..ly-1).  Results are
 // bit-identical to load + step + dump (same kernel, same values).
 int seam_rows(int S, int skew);
+int stream_skew();
 
 bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, const Faces& fc) {
     const bool walls = bc == D2Q37_BC_WALL && fc.lo == kFaceWall && fc.hi == kFaceWall && step2_ghost_walls();
@@ -1380,9 +1381,7 @@ bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, con
           !h->prof_on))
         return false;
     if (per) {  // the two seam pieces (8 rows per sweep each, whatever D2Q37_STREAM_SKEW says below 8) and a wave
-        const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
-        const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
-        return h->g.ly >= 2 * seam_rows(nsteps / 2, skew) + 4 * step2_band_rows();
+        return h->g.ly >= 2 * seam_rows(nsteps / 2, stream_skew()) + 4 * step2_band_rows();
     }
     return true;
 }
@@ -1438,18 +1437,26 @@ std::vector<int> stream_edges(int ly) {
 // (the seam's wrap images mirror 6 rows on each side; two bands of margin keep the launches useful)
 int seam_rows(int S, int skew) { return skew * S + 2 * step2_band_rows(); }
 
-int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, int nsteps, const Faces& fc) {
-    DeviceGuard dg(h->device);
-    const DevGeo& g = h->g;
-    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
-    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-    if (!h->copy_stream2) CK(cudaStreamCreateWithFlags(&h->copy_stream2, cudaStreamNonBlocking));
-    const int S = nsteps / 2, ly = g.ly;
-    const bool per = fc.lo == kFacePeriodic;
+// The streamed run as a list of operations (also exported to the host-side schedule test,
+// d2q37_debug_stream_plan): uploads first (copy stream, in order), then the compute stream's operations in
+// order; a download follows everything before it on the compute stream (second copy stream).
+enum { kOpUpload = 0, kOpWaitUpload = 1, kOpSweep = 2, kOpMirror = 3, kOpWrap = 4, kOpDownload = 5 };
+struct StreamOp {
+    int kind;
+    int a, b;  // rows [a, b) (upload, sweep, download); mirror: a = face mask
+    int c;     // upload / wait: upload index; sweep / mirror / wrap: the sweep s whose output (or, s = 0,
+               // the uploaded state) it writes / completes
+};
+
+int stream_skew() {
     // rows a chunk's range moves down per sweep: at least the 6 a sweep reaches; 8 keeps the bands'
     // 960-byte column stores on 32-byte sectors (D2Q37_STREAM_SKEW)
     const char* skew_env = std::getenv("D2Q37_STREAM_SKEW");
-    const int skew = std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
+    return std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
+}
+
+std::vector<StreamOp> stream_plan(int ly, int S, bool per) {
+    const int skew = stream_skew();
     // y-periodic: the two pieces at the seam, BOT = [0, base) and TOP = [top0, ly), are uploaded first and
     // swept together -- sweep s on [0, base - d s) and [top0 + d s, ly), then the periodic images of the
     // new state's rows 0..5 / ly-6..ly-1 (k_wrap6) -- losing d rows per sweep on their far sides; the wave
@@ -1459,7 +1466,63 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     std::vector<int> edge = stream_edges(top0 - base);
     for (int& e : edge) e += base;
     const int K = int(edge.size()) - 1;
-    std::vector<cudaEvent_t> ev(2 * size_t(K) + 3, nullptr);
+    std::vector<StreamOp> ops;
+    int nup = 0;
+    if (per) {
+        ops.push_back({kOpUpload, top0, ly, nup});
+        ops.push_back({kOpUpload, 0, base, nup++});  // (one event after both)
+    }
+    const int up0 = nup;
+    for (int k = 0; k < K; ++k) ops.push_back({kOpUpload, edge[k], edge[k + 1], nup++});
+    auto sweep = [&](int s, int lo, int hi) {
+        if (hi > lo) ops.push_back({kOpSweep, lo, hi, s});
+    };
+    if (per) {
+        ops.push_back({kOpWaitUpload, 0, 0, 0});
+        ops.push_back({kOpWrap, 0, 0, 0});
+        for (int s = 1; s <= S; ++s) {
+            sweep(s, top0 + skew * s, ly);
+            sweep(s, 0, base - skew * s);
+            ops.push_back({kOpWrap, 0, 0, s});
+        }
+        ops.push_back({kOpDownload, top0 + skew * S, ly, 0});
+        ops.push_back({kOpDownload, 0, base - skew * S, 0});
+    }
+    for (int k = 0; k < K; ++k) {
+        const bool last = k == K - 1;
+        ops.push_back({kOpWaitUpload, 0, 0, up0 + k});
+        if (!per && k == 0) ops.push_back({kOpMirror, 1, 0, 0});
+        if (!per && last) ops.push_back({kOpMirror, 2, 0, 0});
+        int lo = 0, hi = 0;
+        for (int s = 1; s <= S; ++s) {
+            lo = !per && k == 0 ? 0 : std::max(0, edge[k] - skew * s);
+            hi = last ? (per ? top0 + skew * s : ly) : std::max(0, edge[k + 1] - skew * s);
+            sweep(s, lo, hi);
+            if (!per && hi > lo) {
+                // wall images once the six rows they mirror are complete: the launch that wrote row 5 (a
+                // range clipped at row 0 may end below it; the chunk above then finishes the rows) / the
+                // last chunk's (it always reaches from below ly - 6 to ly)
+                const int mask = (lo < 2 * kHalo && hi >= 2 * kHalo ? 1 : 0) | (hi == ly ? 2 : 0);
+                if (mask) ops.push_back({kOpMirror, mask, 0, s});
+            }
+        }
+        if (hi > lo) ops.push_back({kOpDownload, lo, hi, 0});
+    }
+    return ops;
+}
+
+int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, int nsteps, const Faces& fc) {
+    DeviceGuard dg(h->device);
+    const DevGeo& g = h->g;
+    if (!h->nsm) CK(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->device));
+    if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    if (!h->copy_stream2) CK(cudaStreamCreateWithFlags(&h->copy_stream2, cudaStreamNonBlocking));
+    const int S = nsteps / 2;
+    const bool per = fc.lo == kFacePeriodic;
+    const std::vector<StreamOp> ops = stream_plan(g.ly, S, per);
+    size_t nev = 1;
+    for (const StreamOp& op : ops) nev += op.kind == kOpUpload || op.kind == kOpDownload;
+    std::vector<cudaEvent_t> ev(nev, nullptr);
     struct EventsGuard {
         std::vector<cudaEvent_t>& e;
         ~EventsGuard() {
@@ -1468,11 +1531,11 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
         }
     } guard{ev};
     for (cudaEvent_t& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    cudaEvent_t* const uploaded = ev.data();
-    cudaEvent_t* const swept = ev.data() + K;
-    cudaEvent_t& start = ev[2 * size_t(K)];
-    cudaEvent_t& seam_up = ev[2 * size_t(K) + 1];
-    cudaEvent_t& seam_swept = ev[2 * size_t(K) + 2];
+    cudaEvent_t& start = ev[0];
+    cudaEvent_t* const uploaded = ev.data() + 1;  // by upload index (two seam uploads share one)
+    size_t next_ev = 1;
+    for (const StreamOp& op : ops)
+        if (op.kind == kOpUpload) next_ev = std::max(next_ev, size_t(op.c) + 2);
     double* const X[2] = {h->buf[h->cur], h->buf[1 - h->cur]};  // X[s & 1]: the state after sweep s
     const size_t plane_vals = size_t(g.lx) * g.ly;
     const long long row0 = site_of(g, kHalo, 0);
@@ -1497,62 +1560,38 @@ int run_streamed(d2q37_lattice* h, const double* in, double* out, double omega, 
     gf.lo = gf.hi = kFaceGhost;
     const bool lock = step2_sched() != 0;
     cudaStream_t st = h->stream;
-    // rows [lo, hi) of sweep s: the pair form on the pointer-shifted range, ghost faces
-    auto sweep = [&](int s, int lo, int hi) -> int {
-        if (hi <= lo || probe == 2) return D2Q37_OK;
-        DevGeo gs = g;
-        gs.ly = hi - lo;
-        const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
-        CK(launch_step2_pair(X[(s - 1) & 1] + lo, X[s & 1] + lo, gs, gf, h->mp, omega, h->d_flag, st, 0, nb, h->nsm, lock));
-        return D2Q37_OK;
-    };
     // the copies start after whatever the lattice's stream still has queued
     CK(cudaEventRecord(start, st));
     CK(cudaStreamWaitEvent(h->copy_stream, start, 0));
     CK(cudaStreamWaitEvent(h->copy_stream2, start, 0));
-    if (per) {
-        RET(copy_rows(true, X[0], top0, ly, h->copy_stream));
-        RET(copy_rows(true, X[0], 0, base, h->copy_stream));
-        CK(cudaEventRecord(seam_up, h->copy_stream));
-    }
-    for (int k = 0; k < K; ++k) {
-        RET(copy_rows(true, X[0], edge[k], edge[k + 1], h->copy_stream));
-        CK(cudaEventRecord(uploaded[k], h->copy_stream));
-    }
-    if (per) {
-        CK(cudaStreamWaitEvent(st, seam_up, 0));
-        CK(launch_wrap6(X[0], g, st));
-        for (int s = 1; s <= S; ++s) {
-            RET(sweep(s, top0 + skew * s, ly));
-            RET(sweep(s, 0, base - skew * s));
-            CK(launch_wrap6(X[s & 1], g, st));
-        }
-        CK(cudaEventRecord(seam_swept, st));
-        CK(cudaStreamWaitEvent(h->copy_stream2, seam_swept, 0));
-        RET(copy_rows(false, X[S & 1], top0 + skew * S, ly, h->copy_stream2));
-        RET(copy_rows(false, X[S & 1], 0, base - skew * S, h->copy_stream2));
-    }
-    for (int k = 0; k < K; ++k) {
-        const bool last = k == K - 1;
-        CK(cudaStreamWaitEvent(st, uploaded[k], 0));
-        if (!per && k == 0) CK(launch_mirror6(X[0], g, fc, st, 1));
-        if (!per && last) CK(launch_mirror6(X[0], g, fc, st, 2));
-        int lo = 0, hi = 0;
-        for (int s = 1; s <= S; ++s) {
-            lo = !per && k == 0 ? 0 : std::max(0, edge[k] - skew * s);
-            hi = last ? (per ? top0 + skew * s : ly) : std::max(0, edge[k + 1] - skew * s);
-            RET(sweep(s, lo, hi));
-            if (!per && hi > lo && probe != 2) {
-                // wall images once the six rows they mirror are complete: the launch that wrote row 5 (a
-                // range clipped at row 0 may end below it; the chunk above then finishes the rows) / the
-                // last chunk's (it always reaches from below ly - 6 to ly)
-                const int mask = (lo < 2 * kHalo && hi >= 2 * kHalo ? 1 : 0) | (hi == ly ? 2 : 0);
-                if (mask) CK(launch_mirror6(X[s & 1], g, fc, st, mask));
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const StreamOp& op = ops[i];
+        switch (op.kind) {
+            case kOpUpload:
+                RET(copy_rows(true, X[0], op.a, op.b, h->copy_stream));
+                if (i + 1 == ops.size() || ops[i + 1].kind != kOpUpload || ops[i + 1].c != op.c)
+                    CK(cudaEventRecord(uploaded[op.c], h->copy_stream));
+                break;
+            case kOpWaitUpload: CK(cudaStreamWaitEvent(st, uploaded[op.c], 0)); break;
+            case kOpSweep: {
+                if (probe == 2) break;
+                // rows [a, b) of sweep c: the pair form on the pointer-shifted range, ghost faces
+                DevGeo gs = g;
+                gs.ly = op.b - op.a;
+                const int nb = (gs.ly + step2_band_rows() - 1) / step2_band_rows();
+                CK(launch_step2_pair(X[(op.c - 1) & 1] + op.a, X[op.c & 1] + op.a, gs, gf, h->mp, omega, h->d_flag, st, 0,
+                                     nb, h->nsm, lock));
+                break;
             }
+            case kOpMirror: CK(launch_mirror6(X[op.c & 1], g, fc, st, op.a)); break;
+            case kOpWrap: CK(launch_wrap6(X[op.c & 1], g, st)); break;
+            case kOpDownload:
+                CK(cudaEventRecord(ev[next_ev], st));
+                CK(cudaStreamWaitEvent(h->copy_stream2, ev[next_ev], 0));
+                ++next_ev;
+                RET(copy_rows(false, X[S & 1], op.a, op.b, h->copy_stream2));
+                break;
         }
-        CK(cudaEventRecord(swept[k], st));
-        CK(cudaStreamWaitEvent(h->copy_stream2, swept[k], 0));
-        RET(copy_rows(false, X[S & 1], lo, hi, h->copy_stream2));
     }
     h->cur = S & 1 ? 1 - h->cur : h->cur;
     h->time_step += nsteps;
@@ -1703,6 +1742,21 @@ int d2q37_run_canonical(d2q37_lattice* h, const double* host_in, double* host_ou
     return dump_canonical_impl(h, 0, host_out, n, false);
 }
 int d2q37_last_run_mode(const d2q37_lattice* h) { return h ? h->last_run_mode : -1; }
+
+int d2q37_debug_stream_plan(int ly, int nsteps, int bc, int* ops, int cap) {
+    if (ly < 1 || nsteps < 2 || nsteps % 2 != 0 || (bc != D2Q37_BC_WALL && bc != D2Q37_BC_PERIODIC))
+        return -fail(D2Q37_ERR_INVALID_ARGUMENT, "stream plan: ly >= 1, an even nsteps >= 2, wall or periodic bc");
+    const bool per = bc == D2Q37_BC_PERIODIC;
+    if (per && ly < 2 * seam_rows(nsteps / 2, stream_skew()) + 4 * step2_band_rows()) return 0;  // three verbs
+    const std::vector<StreamOp> plan = stream_plan(ly, nsteps / 2, per);
+    for (size_t i = 0; i < plan.size() && int(i) < cap && ops; ++i) {
+        ops[4 * i] = plan[i].kind;
+        ops[4 * i + 1] = plan[i].a;
+        ops[4 * i + 2] = plan[i].b;
+        ops[4 * i + 3] = plan[i].c;
+    }
+    return int(plan.size());
+}
 
 int d2q37_load_buffer(d2q37_lattice* h, int which, const double* host, size_t n) {
     return load_canonical_impl(h, which, host, n, false);
