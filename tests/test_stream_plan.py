@@ -137,6 +137,27 @@ def test_plans_of_other_chunk_heights_replay(lbm, rows, first, last, skew, ly, n
             assert bc == "periodic"
 
 
+def test_random_plans_replay(lbm):
+    """300 seeded random draws of height, step count, boundary mode, chunk heights and skew."""
+    rng = np.random.default_rng(20181804)
+    ran = 0
+    for _ in range(300):
+        ly = int(rng.integers(6, 6000))
+        nsteps = 2 * int(rng.integers(1, 60))
+        bc = "periodic" if rng.random() < 0.4 else "wall"
+        env = dict(D2Q37_STREAM_ROWS=int(rng.integers(6, 3000)), D2Q37_STREAM_FIRST=int(rng.integers(6, 800)),
+                   D2Q37_STREAM_LAST=int(rng.integers(6, 800)), D2Q37_STREAM_SKEW=int(rng.choice([6, 8, 10, 12, 16])))
+        with _Env(**env):
+            ops = lbm.stream_plan(ly, nsteps, bc)
+            if len(ops):
+                try:
+                    replay(ops.tolist(), ly, nsteps, bc)
+                except AssertionError as e:
+                    raise AssertionError(f"ly {ly} nsteps {nsteps} bc {bc} env {env}: {e}") from e
+                ran += 1
+    assert ran > 150
+
+
 def test_replay_catches_a_broken_plan(lbm):
     """The model is not vacuous: dropping an image refresh, or a sweep, fails the replay."""
     ops = lbm.stream_plan(2400, 20, "wall").tolist()
