@@ -1354,9 +1354,9 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
 
 // ---- streamed run: load -> nsteps FUSED2 steps -> dump, pipelined in y-chunks -------------------
 //
-// d2q37_run_canonical on a single SoA wall domain.  The canonical host array is [p][x][y]
-// (dump.hpp:19-21), so rows [r0, r1) of every population are one pitched copy each; chunk k of the
-// input is uploaded on the copy stream while the compute stream sweeps the chunks before it, and
+// d2q37_run_canonical on a single SoA domain (walls; y-periodic: stream_plan).  The canonical host array
+// is [p][x][y] (dump.hpp:19-21), so rows [r0, r1) of every population are one pitched copy each; chunk k
+// of the input is uploaded on the copy stream while the compute stream sweeps the chunks before it, and
 // finished rows are downloaded on a second copy stream (the other DMA direction) while later chunks
 // are still being swept.  A FUSED2 sweep s (two steps) of rows [a, b) needs sweep s - 1 on rows
 // [a - 6, b + 6), so chunk k is swept as a parallelogram: sweep s covers rows
@@ -1364,11 +1364,13 @@ int dump_canonical_impl(d2q37_lattice* h, int which, double* out, size_t n, bool
 // and every sweep's input rows are then final when it is launched (all in stream order on the compute
 // stream).  The two state buffers still alternate (X_s = sweep s's output; X_s and X_{s-2} share a
 // buffer): sweep s on chunk k overwrites X_{s-2} rows below edge[k+1] - d s, and the only reader of
-// X_{s-2} still to come -- sweep s - 1 on chunk k + 1 -- reads rows from edge[k+1] - d s + d - 6 on.  The sweep
-// of a row range is the pair form on a pointer-shifted geometry with ghost faces (k_step2_pair<true>,
-// rows beyond the range read as they stand, like a slab's deep ghost rows); the walls stay the wall
-// images of step2_local (k_mirror6 after every sweep that wrote rows 0..5 / ly-6..ly-1).  Results are
-// bit-identical to load + step + dump (same kernel, same values).
+// X_{s-2} still to come -- sweep s - 1 on chunk k + 1 -- reads rows from edge[k+1] - d s + d - 6 on.  The
+// sweep of a row range is the pair form on a pointer-shifted geometry with ghost faces
+// (k_step2_pair<true>, rows beyond the range read as they stand, like a slab's deep ghost rows); the
+// walls stay the wall images of step2_local (k_mirror6 once a sweep's rows 0..5 / ly-6..ly-1 are
+// complete).  Results are bit-identical to load + step + dump (same kernel, same values).  The schedule
+// is built as a list of operations (stream_plan) that run_streamed executes and
+// tests/test_stream_plan.py replays on a model of the two buffers.
 int seam_rows(int S, int skew);
 int stream_skew();
 
@@ -1380,10 +1382,8 @@ bool can_stream_run(const d2q37_lattice* h, int nsteps, int variant, int bc, con
           step2_supported(h->g, fc) && nsteps >= 2 && nsteps % 2 == 0 && h->g.ly >= 4 * step2_band_rows() &&
           !h->prof_on))
         return false;
-    if (per) {  // the two seam pieces (8 rows per sweep each, whatever D2Q37_STREAM_SKEW says below 8) and a wave
-        return h->g.ly >= 2 * seam_rows(nsteps / 2, stream_skew()) + 4 * step2_band_rows();
-    }
-    return true;
+    // y-periodic: room for the two seam pieces and a wave between them
+    return !per || h->g.ly >= 2 * seam_rows(nsteps / 2, stream_skew()) + 4 * step2_band_rows();
 }
 
 // Chunk edges (multiples of 4 rows).  The sweeps take longer than the copies, so only the first upload
