@@ -334,30 +334,71 @@ static inline size_t cidx(int lx, int ly, int p, int x, int y) {
 
 static inline int wrap(int v, int n) { return ((v % n) + n) % n; }
 
-int orc_propagate(const orc_model* m, int lx, int ly, int bc, const double* in, double* out) {
+typedef struct {
+    const orc_model* m;
+    int lx, ly, bc, r0, r1; /* rows r = p * lx + x of the canonical array, [r0, r1) */
+    const int* ybar;
+    const double* in;
+    double* out;
+} propagate_job;
+
+static void* propagate_worker(void* arg) {
+    const propagate_job* j = (const propagate_job*)arg;
+    const orc_model* m = j->m;
+    const int lx = j->lx, ly = j->ly, bc = j->bc;
+    for (int r = j->r0; r < j->r1; ++r) {
+        const int p = r / lx, x = r % lx;
+        const int xs = wrap(x - m->cx[p], lx);
+        for (int y = 0; y < ly; ++y) {
+            const int gy = y - m->cy[p];
+            int ys = gy, q = p;
+            if (bc == ORC_BC_PERIODIC) {
+                ys = wrap(gy, ly);
+            } else if (gy < 0) {
+                ys = -1 - gy;
+                q = j->ybar[p];
+            } else if (gy >= ly) {
+                ys = 2 * ly - 1 - gy;
+                q = j->ybar[p];
+            }
+            j->out[cidx(lx, ly, p, x, y)] = j->in[cidx(lx, ly, q, xs, ys)];
+        }
+    }
+    return NULL;
+}
+
+/* The pull copy is a pure permutation of values, so the result does not depend on the thread count. */
+int orc_propagate_mt(const orc_model* m, int lx, int ly, int bc, const double* in, double* out, int nthreads) {
     if (lx < 1 || ly < 1) return -1;
     if (bc == ORC_BC_WALL && ly < ORC_HALO) return -1;
     int ybar[ORC_NPOP];
     orc_ymirror(m, ybar);
-    for (int p = 0; p < ORC_NPOP; ++p)
-        for (int x = 0; x < lx; ++x) {
-            const int xs = wrap(x - m->cx[p], lx);
-            for (int y = 0; y < ly; ++y) {
-                const int gy = y - m->cy[p];
-                int ys = gy, q = p;
-                if (bc == ORC_BC_PERIODIC) {
-                    ys = wrap(gy, ly);
-                } else if (gy < 0) {
-                    ys = -1 - gy;
-                    q = ybar[p];
-                } else if (gy >= ly) {
-                    ys = 2 * ly - 1 - gy;
-                    q = ybar[p];
-                }
-                out[cidx(lx, ly, p, x, y)] = in[cidx(lx, ly, q, xs, ys)];
-            }
-        }
+    const long rows = (long)ORC_NPOP * lx;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if (nthreads > rows) nthreads = (int)rows;
+    if ((long)lx * ly < 65536) nthreads = 1; /* small lattices: not worth the thread start */
+    propagate_job jobs[256];
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t].m = m;
+        jobs[t].lx = lx;
+        jobs[t].ly = ly;
+        jobs[t].bc = bc;
+        jobs[t].r0 = (int)(rows * t / nthreads);
+        jobs[t].r1 = (int)(rows * (t + 1) / nthreads);
+        jobs[t].ybar = ybar;
+        jobs[t].in = in;
+        jobs[t].out = out;
+    }
+    for (int t = 1; t < nthreads; ++t) pthread_create(&th[t], NULL, propagate_worker, &jobs[t]);
+    propagate_worker(&jobs[0]);
+    for (int t = 1; t < nthreads; ++t) pthread_join(th[t], NULL);
     return 0;
+}
+
+int orc_propagate(const orc_model* m, int lx, int ly, int bc, const double* in, double* out) {
+    return orc_propagate_mt(m, lx, ly, bc, in, out, 1);
 }
 
 typedef struct {
@@ -413,7 +454,7 @@ int orc_step(const orc_model* m, int lx, int ly, int bc, double omega, int nstep
              double* scratch, int nthreads) {
     int bad = 0;
     for (int s = 0; s < nsteps; ++s) {
-        if (orc_propagate(m, lx, ly, bc, state, scratch) != 0) return -1;
+        if (orc_propagate_mt(m, lx, ly, bc, state, scratch, nthreads) != 0) return -1;
         bad |= orc_collide(m, lx, ly, omega, scratch, state, nthreads);
     }
     return bad;

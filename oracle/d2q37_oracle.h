@@ -58,6 +58,8 @@ int orc_collide_site(const orc_model* m, const double* f, double omega, double* 
 
 /* validation.cpp:13-25 (periodic) + builder wall rule, canonical arrays. */
 int orc_propagate(const orc_model* m, int lx, int ly, int bc, const double* in, double* out);
+/* the same pull copy split over threads by canonical rows (a permutation: thread-count invariant) */
+int orc_propagate_mt(const orc_model* m, int lx, int ly, int bc, const double* in, double* out, int nthreads);
 /* validation.cpp:27-38; returns 1 if any site is non-physical. */
 int orc_collide(const orc_model* m, int lx, int ly, double omega, const double* in, double* out,
                 int nthreads);

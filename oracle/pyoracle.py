@@ -65,6 +65,7 @@ def orc() -> C.CDLL:
             "orc_equilibrium": (None, [M, _dp, _dp]),
             "orc_collide_site": (C.c_int, [M, _dp, C.c_double, _dp]),
             "orc_propagate": (C.c_int, [M, C.c_int, C.c_int, C.c_int, _dp, _dp]),
+            "orc_propagate_mt": (C.c_int, [M, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_int]),
             "orc_collide": (C.c_int, [M, C.c_int, C.c_int, C.c_double, _dp, _dp, C.c_int]),
             "orc_step": (C.c_int, [M, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, C.c_int]),
             "orc_padded_elems": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
@@ -197,11 +198,12 @@ def _flat(a):
     return a.reshape(-1), a
 
 
-def orc_propagate(a, bc=BC_PERIODIC):
+def orc_propagate(a, bc=BC_PERIODIC, nthreads=None):
     _, lx, ly = a.shape
     fa, _ = _flat(a)
     out = _canon(lx, ly)
-    if orc().orc_propagate(C.byref(orc_model_struct()), lx, ly, bc, fa, out.reshape(-1)) != 0:
+    if orc().orc_propagate_mt(C.byref(orc_model_struct()), lx, ly, bc, fa, out.reshape(-1),
+                              nthreads or os.cpu_count() or 1) != 0:
         raise ValueError("orc_propagate: bad geometry")
     return out
 

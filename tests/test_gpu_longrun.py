@@ -73,12 +73,15 @@ def test_fused2_100_steps_vs_unmodified_reference(gpu, lbm, po, layout):
     _fields_close(po, s.dump(), _ref_steps(po, init, 100), 1e-9)
 
 
+_ORACLE_200: dict = {}
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("layout", ["soa", "banded"])
 def test_fused2_200_steps_walls_split_path_vs_oracle(gpu, lbm, po, layout):
     """validation.cpp:84-90 (the oracle stepped alongside) at the bench step's own code path: a
-    4096 x 2048 RT lattice with walls -- past the small-lattice threshold, so SoA runs one
-    k_step2_split launch per sweep (interior bands in the plain form beside the wall bands) -- 200
+    4096 x 2048 RT lattice with walls -- past the small-lattice threshold, so SoA runs the
+    bench's sweep kernel (k_step2_pair, one launch per sweep with the wall images in the ghost rows) -- 200
     steps (100 sweeps) within 1e-9 of the C oracle on populations and derived fields; after one sweep
     within 1e-12."""
     lx, ly = 4096, 2048
@@ -86,10 +89,13 @@ def test_fused2_200_steps_walls_split_path_vs_oracle(gpu, lbm, po, layout):
     s = lbm.Simulation(layout, lx, ly, 1, device=0, bc="wall", variant="fused2")
     s.load(init)
     s.step(OMEGA, 2)
-    want2, bad = po.orc_step(init, OMEGA, 2, po.BC_WALL)
-    assert not bad
-    _fields_close(po, s.dump(), want2, 1e-12)
+    if not _ORACLE_200:  # the oracle's 200 steps are the test's cost: stepped once for both stores
+        want2, bad2 = po.orc_step(init, OMEGA, 2, po.BC_WALL)
+        want, bad = po.orc_step(want2, OMEGA, 198, po.BC_WALL)
+        _ORACLE_200.update(want2=want2, want=want, bad=bad2 or bad)
+    assert not _ORACLE_200["bad"]
+    _fields_close(po, s.dump(), _ORACLE_200["want2"], 1e-12)
     s.step(OMEGA, 198)
-    want, bad = po.orc_step(want2, OMEGA, 198, po.BC_WALL)
-    assert not bad
-    _fields_close(po, s.dump(), want, 1e-9)
+    _fields_close(po, s.dump(), _ORACLE_200["want"], 1e-9)
+    if layout == "banded":  # the last user: drop the 2 x 2.5 GB of cached oracle states
+        _ORACLE_200.clear()
