@@ -733,8 +733,11 @@ def run_b200(args, dist: Dist):
     dom_ms = kt[dom][0] / max(1, kt[dom][1])
     form = None if STUB else lbm.set_fused2_tuning(-1, -1)[0]
     pair = args.variant == "fused2" and args.layout == "soa" and form == 4
-    # one launch per sweep (k_step2_pair; walls mirrored in the kernel) -- the bench's walls; a
-    # y-periodic domain adds k_wrap6 (periodic images into the deep ghost rows) per sweep
+    # single domain in the pair form: each timed "fused" interval is one k_step2_pair launch plus the
+    # refresh of the images in the deep ghost rows for the next sweep (k_mirror6 at walls, k_wrap6 on
+    # y-periodic domains; ~15 us, inside kernel_ms) -- two launches per sweep, as the ncu launch list shows
+    if pair and not transport and not STUB:
+        launches += fused_n
     # FUSED2: one sweep per timed "fused" interval (k_step2_pair + the face bands' k_step2_split beside it)
     # one launch reads and writes the lattice once (592 B/site) and advances `upd` time steps
     upd = steps_per_call(args.variant) if dom == "fused" else 1
@@ -746,8 +749,8 @@ def run_b200(args, dist: Dist):
                             "6-row halo pack, interior in lockstep beside the NCCL exchange; two fused steps per "
                             "HBM sweep, two threads per site)" if pair and transport else
                             "k_step2_pair (two fused pull+collide steps per HBM sweep, temporal blocking; two "
-                            "threads per site, 512-thread CTAs, lockstep band schedule; wall bands mirrored in "
-                            "the kernel)" if pair else
+                            "threads per site, 512-thread CTAs, lockstep band schedule; the walls as specular "
+                            "images in the deep ghost rows, refreshed by k_mirror6 after the sweep)" if pair else
                             "k_step2_split (two fused pull+collide steps per HBM sweep, temporal blocking; "
                             "interior bands beside the two wall bands in one launch)") if two else
                            "k_collide<FAST,SHIFT> (fused pull-gather + collide)"),
