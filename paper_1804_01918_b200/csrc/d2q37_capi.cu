@@ -1455,6 +1455,11 @@ int stream_skew() {
     return std::max(2 * kHalo, skew_env ? std::atoi(skew_env) & ~1 : 8);
 }
 
+int stream_min_download_rows() {
+    const char* e = std::getenv("D2Q37_STREAM_MIN_DOWNLOAD");
+    return e ? std::max(1, std::atoi(e)) : 240;
+}
+
 std::vector<StreamOp> stream_plan(int ly, int S, bool per) {
     const int skew = stream_skew();
     // y-periodic: the two pieces at the seam, BOT = [0, base) and TOP = [top0, ly), are uploaded first and
@@ -1488,6 +1493,10 @@ std::vector<StreamOp> stream_plan(int ly, int S, bool per) {
         ops.push_back({kOpDownload, top0 + skew * S, ly, 0});
         ops.push_back({kOpDownload, 0, base - skew * S, 0});
     }
+    // final rows narrower than this wait for the next chunk's download (a first download of a few dozen
+    // rows -- e.g. 170 or 400 steps on 4096 x 16384 -- measured 0.5-1 s slower per run; DESIGN 3.3)
+    const int min_dl = stream_min_download_rows();
+    int dl_lo = -1;
     for (int k = 0; k < K; ++k) {
         const bool last = k == K - 1;
         ops.push_back({kOpWaitUpload, 0, 0, up0 + k});
@@ -1506,7 +1515,15 @@ std::vector<StreamOp> stream_plan(int ly, int S, bool per) {
                 if (mask) ops.push_back({kOpMirror, mask, 0, s});
             }
         }
-        if (hi > lo) ops.push_back({kOpDownload, lo, hi, 0});
+        if (hi > lo) {
+            const int from = dl_lo >= 0 ? dl_lo : lo;
+            if (!last && hi - from < min_dl) {
+                dl_lo = from;
+            } else {
+                ops.push_back({kOpDownload, from, hi, 0});
+                dl_lo = -1;
+            }
+        }
     }
     return ops;
 }

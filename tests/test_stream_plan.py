@@ -110,7 +110,7 @@ def replay(ops, ly, nsteps, bc):
     assert (ghost[S & 1] == S).all(), "the ghost rows do not hold the final state's images"
 
 
-CASES = [(16384, 200), (16384, 2), (2400, 20), (2400, 100), (1201, 10), (486, 4), (700, 6), (40000, 60), (7, 2), (13, 4)]
+CASES = [(16384, 200), (16384, 170), (16384, 400), (16384, 2), (2400, 20), (2400, 100), (1201, 10), (486, 4), (700, 6), (40000, 60), (7, 2), (13, 4)]
 
 
 @pytest.mark.parametrize("ly,nsteps", CASES)
@@ -135,6 +135,26 @@ def test_plans_of_other_chunk_heights_replay(lbm, rows, first, last, skew, ly, n
             replay(ops.tolist(), ly, nsteps, bc)
         else:
             assert bc == "periodic"
+
+
+@pytest.mark.parametrize("ly,nsteps", [(16384, 170), (16384, 400), (16384, 200), (8192, 170), (16216, 200), (5000, 120)])
+@pytest.mark.parametrize("bc", ["wall", "periodic"])
+def test_no_narrow_download_between_chunks(lbm, ly, nsteps, bc):
+    """A chunk whose final rows are a sliver (its range clipped at row 0 after leaning back 8 rows per
+    sweep: 40 rows at 170 steps, 80 at 400 on 16384 rows) hands them to the next chunk's download: a
+    first download that narrow measured 0.4-0.9 s per run (DESIGN 3.3).  Only the last download may
+    be as narrow as the rows left."""
+    ops = lbm.stream_plan(ly, nsteps, bc).tolist()
+    downs = [(a, b) for kind, a, b, _ in ops if kind == DOWNLOAD]
+    assert downs
+    wave = downs[2:] if bc == "periodic" else downs  # the two seam pieces come first (two bands each)
+    for a, b in wave[:-1]:
+        assert b - a >= 240, (a, b)
+    with _Env(D2Q37_STREAM_MIN_DOWNLOAD=1):  # the rule off: the sliver is back (walls, 170 steps)
+        if (ly, nsteps, bc) == (16384, 170, "wall"):
+            raw = [(a, b) for kind, a, b, _ in lbm.stream_plan(ly, nsteps, bc).tolist() if kind == DOWNLOAD]
+            assert min(b - a for a, b in raw[:-1]) == 40
+            replay(lbm.stream_plan(ly, nsteps, bc).tolist(), ly, nsteps, bc)
 
 
 def test_random_plans_replay(lbm):

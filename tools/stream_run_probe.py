@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 import paper_1804_01918_b200 as lbm  # noqa: E402
 
-lx, ly, n = 4096, 16384, 200
+lx, ly, n = 4096, 16384, int(os.environ.get("PROBE_STEPS", "200"))
 combos = [tuple(int(v) for v in a.split(":")) for a in sys.argv[1:]] or [(4080, 480, 240)]
 s = lbm.Simulation("soa", lx, ly, device=0, bc="wall", variant="fused2")
 s.init_rt_device(2018)
